@@ -1,0 +1,225 @@
+/*
+ * tfg.h -- C-ABI of libtfg, the B200 (sm_100a) tile-fusion library for
+ * D = A (B C):  A square CSR, C dense, B dense (GeMM-SpMM) or CSR
+ * (SpMM-SpMM).
+ *
+ * This is the drop-in boundary under the reference's C++ operator API.  The
+ * reference (arXiv 2407.00243 artifact, /root/reference/proj) is a
+ * header-only C++ template library with no FFI; the C++ headers in
+ * include/tilefuse/ keep its names and signatures and forward to these
+ * entry points.  Each function cites the reference interface it replaces.
+ *
+ * Conventions
+ *   - plain pointers and sizes, no torch / C++ types;
+ *   - every function returns a tfg_status; tfg_last_error() holds the
+ *     message of the last failure on the calling thread;
+ *   - TFG_EINVAL maps to std::invalid_argument and TFG_ERUNTIME to
+ *     std::runtime_error in the C++ mirror, as the reference throws them;
+ *   - "d_" pointers are device (HBM) pointers, "h_" pointers host pointers;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *     All device work is asynchronous on that stream unless stated.
+ * There is no CPU fallback: every compute entry point launches sm_100a
+ * kernels and fails with TFG_ECUDA when no B200 is present.
+ */
+#ifndef TFG_H
+#define TFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TFG_OK = 0,
+  TFG_EINVAL = 1,   /* std::invalid_argument in the reference */
+  TFG_ERUNTIME = 2, /* std::runtime_error in the reference    */
+  TFG_ECUDA = 3     /* CUDA error / no device                  */
+} tfg_status;
+
+typedef enum { TFG_F32 = 0, TFG_F64 = 1 } tfg_dtype;
+
+/* == tilefuse::SchedulerConfig (include/tilefuse/scheduler.hpp:15-24),
+ * same field order, meaning and defaults (tfg_config_default). */
+typedef struct {
+  int32_t ct_size;              /* coarse tile width heuristic (2048)   */
+  int32_t num_workers;          /* p (1)                                 */
+  uint64_t cache_size_words;    /* per-worker budget in scalars (163840) */
+  int32_t b_cols;               /* columns of B when dense (32)          */
+  int32_t c_cols;               /* columns of C (32)                     */
+  double index_to_scalar_ratio; /* index word / scalar word (0.5)        */
+  int32_t b_is_dense;           /* GeMM-SpMM when 1 (1)                  */
+  int32_t whole_b_cost;         /* charge all of B (0)                   */
+} tfg_config;
+
+typedef struct tfg_schedule tfg_schedule; /* device-resident FusedSchedule */
+typedef struct tfg_plan tfg_plan;         /* executor plan bound to a problem */
+
+const char *tfg_last_error(void);
+void tfg_config_default(tfg_config *cfg);
+/* library build / device facts: writes the sm arch the code was built for
+ * (100 for sm_100a) and the number of SMs of the current device (0 if none) */
+tfg_status tfg_device_info(int32_t *built_arch, int32_t *sm_count);
+
+/* ---------------------------------------------------------------------
+ * Inspector (replaces scheduler.hpp:266-310 / scheduler.cpp:124-252)
+ * ------------------------------------------------------------------- */
+
+/* choose_tile_size -- scheduler.hpp:266, scheduler.cpp:124-129.
+ * Host arithmetic on three scalars.  EINVAL if any input < 1. */
+tfg_status tfg_choose_tile_size(int32_t n, int32_t num_workers,
+                                int32_t ct_size, int32_t *out);
+
+/* build_schedule -- scheduler.hpp:300-301, scheduler.cpp:212-245.
+ * GPU inspector over a device-resident CSR pattern (row_ptr n_rows+1,
+ * col_idx nnz; columns strictly increasing per row).  Produces a schedule
+ * bit-identical to the reference's (tile order, i ranges, j lists and
+ * double costs) for the same config.  EINVAL for non-square / empty input
+ * or config values < 1 (scheduler.cpp:115-128).  Synchronises `stream`
+ * before returning (the schedule's shape is needed on the host). */
+tfg_status tfg_build_schedule(int32_t n_rows, int32_t n_cols, int64_t nnz,
+                              const int32_t *d_row_ptr,
+                              const int32_t *d_col_idx,
+                              const tfg_config *cfg, void *stream,
+                              tfg_schedule **out);
+
+/* Same, from host arrays (copies the pattern to the device first): the
+ * entry the C++ mirror's build_schedule(const SparsityView&, ...) uses. */
+tfg_status tfg_build_schedule_host(int32_t n_rows, int32_t n_cols,
+                                   const int32_t *h_row_ptr,
+                                   const int32_t *h_col_idx,
+                                   const tfg_config *cfg, void *stream,
+                                   tfg_schedule **out);
+
+/* Sizes of a schedule: n, tile size t, tiles per wavefront, j rows per
+ * wavefront, and the inspector's device time in seconds. */
+tfg_status tfg_schedule_info(const tfg_schedule *s, int32_t *n,
+                             int32_t *tile_size, int64_t n_tiles[2],
+                             int64_t n_jrows[2], double *inspect_seconds);
+
+/* Flat export of wavefront `wave` into host buffers sized from
+ * tfg_schedule_info: i_lo/i_hi/cost[n_tiles], j_off[n_tiles+1] (int64),
+ * j_rows[n_jrows].  Any pointer may be NULL to skip that array. */
+tfg_status tfg_schedule_export(const tfg_schedule *s, int wave,
+                               int32_t *h_i_lo, int32_t *h_i_hi,
+                               double *h_cost, int64_t *h_j_off,
+                               int32_t *h_j_rows);
+
+/* Import a schedule built elsewhere (e.g. by the reference, or reloaded
+ * from schedule JSON, schedule_io.cpp:28-54) from host flat arrays. */
+tfg_status tfg_schedule_import(int32_t n, int32_t tile_size,
+                               const int64_t n_tiles[2],
+                               const int32_t *const h_i_lo[2],
+                               const int32_t *const h_i_hi[2],
+                               const double *const h_cost[2],
+                               const int64_t *const h_j_off[2],
+                               const int32_t *const h_j_rows[2],
+                               tfg_schedule **out);
+
+void tfg_schedule_destroy(tfg_schedule *s);
+
+/* fused_ratio -- scheduler.hpp:304, scheduler.cpp:247-252 (Eq. 2). */
+double tfg_fused_ratio(const tfg_schedule *s);
+
+/* validate_schedule -- scheduler.hpp:308-310, scheduler.cpp:254-390.
+ * Host-side checker over host CSR pattern + a schedule (the verify path,
+ * not the hot path).  *pass = 1 when no violation; the first message goes
+ * to msg (may be NULL). */
+tfg_status tfg_validate_schedule(int32_t n_rows, int32_t n_cols,
+                                 const int32_t *h_row_ptr,
+                                 const int32_t *h_col_idx,
+                                 const tfg_schedule *s, const tfg_config *cfg,
+                                 int32_t *pass, int64_t *n_violations,
+                                 int64_t *over_budget_width1, char *msg,
+                                 size_t msg_cap);
+
+/* ---------------------------------------------------------------------
+ * Executor (replaces kernels.hpp:182-236: fused_gemm_spmm,
+ * fused_spmm_spmm, unfused_gemm_spmm, unfused_spmm_spmm)
+ * ------------------------------------------------------------------- */
+
+/* FusedProblem<T> (kernels.hpp:16-43) as device pointers. */
+typedef struct {
+  int32_t dtype;      /* tfg_dtype                                    */
+  int32_t n;          /* A is n x n                                   */
+  int32_t b_is_dense; /* 1: B dense n x b_cols; 0: B CSR n x b_cols   */
+  int32_t b_rows;     /* must equal n   (kernels.hpp:38-39)           */
+  int32_t b_cols;
+  int32_t c_rows;     /* must equal b_cols (kernels.hpp:40-41)         */
+  int32_t c_cols;
+  int64_t a_nnz;
+  int64_t b_nnz;      /* CSR B only                                   */
+  const int32_t *d_a_row_ptr;
+  const int32_t *d_a_col_idx;
+  const void *d_a_val;
+  const int32_t *d_b_row_ptr; /* CSR B */
+  const int32_t *d_b_col_idx;
+  const void *d_b_val;
+  const void *d_b_dense;      /* dense B, row-major n x b_cols */
+  const void *d_c;            /* row-major c_rows x c_cols     */
+} tfg_problem;
+
+/* Bind a problem to a schedule (NULL = the unfused executor,
+ * kernels.hpp:128-155 / 212-236) and precompute the device execution plan:
+ * D1 spill set, tile work lists, long-row splits, scratch.  Checks exactly
+ * what the reference executors check: problem.check() (kernels.hpp:35-42),
+ * sched.n == n (kernels.hpp:93-94); the GeMM/SpMM distinction is the
+ * problem's b_is_dense.  The schedule may be destroyed after this call. */
+tfg_status tfg_plan_create(const tfg_problem *p, const tfg_schedule *s,
+                           void *stream, tfg_plan **out);
+
+/* D = A (B C) into the caller's device buffer d_d (n x c_cols row-major,
+ * fully overwritten).  Asynchronous on `stream`; no host synchronisation,
+ * no allocation, no host<->device traffic. */
+tfg_status tfg_plan_execute(tfg_plan *plan, void *d_d, void *stream);
+
+/* RunStats (kernels.hpp:46-50) the plan's execution performs:
+ * first_op_rows, second_op_rows (both n for a valid schedule). */
+tfg_status tfg_plan_stats(const tfg_plan *plan, int64_t *first_op_rows,
+                          int64_t *second_op_rows, int64_t *nnz_processed);
+
+/* Plan facts for roofline accounting: number of D1 rows spilled to HBM
+ * (|S|, rows read by wavefront 1), fused j rows, kernel launches per
+ * execute, and bytes of device scratch held. */
+tfg_status tfg_plan_info(const tfg_plan *plan, int64_t *spill_rows,
+                         int64_t *fused_rows, int32_t *launches,
+                         int64_t *scratch_bytes);
+
+void tfg_plan_destroy(tfg_plan *plan);
+
+/* One-shot host entry used by the C++ mirror for the reference's
+ * by-value API: copies host A, B, C to the device, builds the plan, runs
+ * it and copies D back into h_d (n x c_cols).  Host pointers in `p`
+ * (the d_ fields are read as host addresses).  s may be NULL (unfused). */
+tfg_status tfg_run_host(const tfg_problem *host_problem,
+                        const tfg_schedule *s, void *h_d);
+
+/* ---------------------------------------------------------------------
+ * Multi-GPU row-block partition helpers: halo pack / unpack of
+ * D1 rows around the NCCL exchange.  rows: device int32 list.
+ * ------------------------------------------------------------------- */
+tfg_status tfg_gather_rows(int32_t dtype, const void *d_src, int32_t cols,
+                           const int32_t *d_rows, int64_t n_rows,
+                           void *d_dst, void *stream);
+tfg_status tfg_scatter_rows(int32_t dtype, const void *d_src, int32_t cols,
+                            const int32_t *d_rows, int64_t n_rows,
+                            void *d_dst, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Host generators the reference's Python module exposes
+ * (generate.hpp:15-94; bindings.cpp:111-114).  malloc'd outputs, release
+ * with tfg_free.  Deterministic for (n, density, seed).
+ * ------------------------------------------------------------------- */
+tfg_status tfg_gen_random_sparse(int32_t n, double density, uint64_t seed,
+                                 int32_t **row_ptr, int32_t **col_idx,
+                                 double **values);
+tfg_status tfg_gen_banded(int32_t n, int32_t half_bandwidth,
+                          int32_t **row_ptr, int32_t **col_idx,
+                          double **values);
+void tfg_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TFG_H */

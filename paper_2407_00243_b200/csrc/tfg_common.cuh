@@ -1,0 +1,135 @@
+// tfg_common.cuh -- shared plumbing for libtfg (errors, device buffers,
+// CUB scratch, launch helpers).  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "tfg.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libtfg is written for sm_100a only (compile with -gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace tfg {
+
+// Error classes mirror the reference's exception types.
+struct invalid_argument : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct runtime_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_last_error(const std::string& msg);
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what,
+                                    const char* file, int line) {
+  throw cuda_error(std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                   cudaGetErrorString(e) + ") at " + file + ":" +
+                   std::to_string(line) + ": " + what);
+}
+
+#define TFG_CUDA(expr)                                            \
+  do {                                                            \
+    cudaError_t e__ = (expr);                                     \
+    if (e__ != cudaSuccess) ::tfg::throw_cuda(e__, #expr, __FILE__, __LINE__); \
+  } while (0)
+#define TFG_LAUNCH_CHECK() TFG_CUDA(cudaGetLastError())
+
+template <class F>
+tfg_status guard(F&& f) {
+  try {
+    f();
+    return TFG_OK;
+  } catch (const invalid_argument& e) {
+    set_last_error(e.what());
+    return TFG_EINVAL;
+  } catch (const cuda_error& e) {
+    set_last_error(e.what());
+    return TFG_ECUDA;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return TFG_ERUNTIME;
+  }
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Owning device allocation (cudaMalloc; plans and schedules are built once
+// and executed many times, so allocation is never on the execute path).
+template <class T>
+struct dbuf {
+  T* p = nullptr;
+  size_t n = 0;
+  dbuf() = default;
+  explicit dbuf(size_t count) { alloc(count); }
+  dbuf(const dbuf&) = delete;
+  dbuf& operator=(const dbuf&) = delete;
+  dbuf(dbuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  dbuf& operator=(dbuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~dbuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) TFG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  T* get() const { return p; }
+};
+
+inline int ceil_log2_bits(uint64_t x) {  // bits needed to represent x
+  int b = 0;
+  while (x) { ++b; x >>= 1; }
+  return b < 1 ? 1 : b;
+}
+
+inline int sm_count() {
+  static int cached = -1;
+  if (cached < 0) {
+    int dev = 0;
+    TFG_CUDA(cudaGetDevice(&dev));
+    TFG_CUDA(cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return cached;
+}
+
+template <class T>
+inline void h2d(T* d, const T* h, size_t count, cudaStream_t s) {
+  if (count) TFG_CUDA(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <class T>
+inline void d2h(T* h, const T* d, size_t count, cudaStream_t s) {
+  if (count) TFG_CUDA(cudaMemcpyAsync(h, d, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+}  // namespace tfg
+
+// The device-resident schedule behind the opaque tfg_schedule handle.
+struct tfg_schedule {
+  int32_t n = 0;
+  int32_t tile_size = 0;
+  int64_t n_tiles[2] = {0, 0};
+  int64_t n_jrows[2] = {0, 0};
+  double inspect_seconds = 0.0;
+  tfg::dbuf<int32_t> i_lo[2], i_hi[2];
+  tfg::dbuf<double> cost[2];
+  tfg::dbuf<int64_t> j_off[2];
+  tfg::dbuf<int32_t> j_rows[2];
+};

@@ -1,0 +1,962 @@
+// tfg_executor.cu -- sm_100a executors for D = A (B C) under a two-wavefront
+// tile-fusion schedule (kernels.hpp:88-155 fused_run / unfused_run).
+//
+// Execution of a plan (one stream, kernel boundaries = wavefront barriers):
+//
+//   (a) first op for wavefront-0 tiles that fuse no second-op row: a dense
+//       register-tiled GEMM (B dense) or a CSR SpMM with X = C (B sparse),
+//       writing D1 rows to HBM -- every such row is read by wavefront 1.
+//   (b) the fused wavefront-0 kernel: one CTA per (tile, column slice).  The
+//       tile's D1 slice is computed into shared memory; only rows that some
+//       wavefront-1 row reads (the spill set S) are also written to HBM; the
+//       tile's fused D rows are then computed from shared memory.  D1 rows
+//       outside S never touch HBM (the paper's fused tile).  Tiles too wide
+//       for shared memory stage through HBM/L2 inside the same CTA.
+//   (c) wavefront 1: CSR SpMM over the wavefront-1 rows reading D1 from HBM;
+//       rows longer than kLongRow are split into fixed segments whose
+//       partial rows are combined in a fixed order (no atomics: the result is
+//       bitwise reproducible run to run).
+//
+// Numerics.  The SpMM kernels reproduce the reference's per-element order
+// exactly: out[q] = ((0 + a0*x0) + a1*x1) + ... in ascending nonzero order
+// with separately rounded products and sums (kernels.hpp:71-80), so every
+// SpMM row shorter than kLongRow is bit-identical to the reference.  The
+// dense first op accumulates B[i,j]*C[j,k] in ascending j with fused
+// multiply-add (within the north-star tolerance); fused and unfused paths
+// use the same per-element order, so they agree bitwise with each other.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "tfg_common.cuh"
+
+namespace tfg {
+namespace {
+
+constexpr int kLongRow = 4096;  // rows with more nonzeros are segmented
+constexpr int kSegLen = 2048;   // nonzeros per segment
+
+template <class T>
+struct fops;
+template <>
+struct fops<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+};
+template <>
+struct fops<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+};
+
+template <class T, int VEC>
+struct VT;
+template <> struct VT<double, 1> { using type = double; };
+template <> struct VT<double, 2> { using type = double2; };
+template <> struct VT<float, 1> { using type = float; };
+template <> struct VT<float, 2> { using type = float2; };
+template <> struct VT<float, 4> { using type = float4; };
+
+template <class T, int VEC>
+__device__ __forceinline__ void ldv(T (&r)[VEC], const T* p) {
+  using V = typename VT<T, VEC>::type;
+  const V x = *reinterpret_cast<const V*>(p);
+  memcpy(r, &x, sizeof(V));
+}
+template <class T, int VEC>
+__device__ __forceinline__ void stv(T* p, const T (&r)[VEC]) {
+  using V = typename VT<T, VEC>::type;
+  V x;
+  memcpy(&x, r, sizeof(V));
+  *reinterpret_cast<V*>(p) = x;
+}
+// streaming store for D (written once, never re-read by this launch)
+template <class T, int VEC>
+__device__ __forceinline__ void stv_cs(T* p, const T (&r)[VEC]) {
+  using V = typename VT<T, VEC>::type;
+  V x;
+  memcpy(&x, r, sizeof(V));
+  __stcs(reinterpret_cast<V*>(p), x);
+}
+
+__device__ __forceinline__ unsigned group_mask(int lpr) {
+  if (lpr == 32) return 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  return ((1u << lpr) - 1u) << (lane & ~(lpr - 1));
+}
+
+// One CSR row times X, LPR lanes per row, each lane NCH x VEC columns.
+// Per-element order = ascending nonzeros, separate mul and add
+// (kernels.hpp:75-79).  XL(c, ch, out[VEC]) loads X row c, chunk ch.
+template <class T, int VEC, int LPR, int NCH, class XL>
+__device__ __forceinline__ void spmm_row(int kb, int ke,
+                                         const int* __restrict__ ci,
+                                         const T* __restrict__ av, int gl,
+                                         unsigned gmask, XL xl,
+                                         T (&acc)[NCH][VEC]) {
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[ch][e] = T(0);
+  for (int k0 = kb; k0 < ke; k0 += LPR) {
+    const int kk = k0 + gl;
+    int c = 0;
+    T a = T(0);
+    if (kk < ke) {
+      c = __ldg(ci + kk);
+      a = __ldg(av + kk);
+    }
+    const int cnt = min(LPR, ke - k0);
+    int u = 0;
+    for (; u + 4 <= cnt; u += 4) {
+      int cu[4];
+      T au[4];
+      T x[4][NCH][VEC];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cu[q] = __shfl_sync(gmask, c, u + q, LPR);
+        au[q] = __shfl_sync(gmask, a, u + q, LPR);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) xl(cu[q], ch, x[q][ch]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            acc[ch][e] = fops<T>::add(acc[ch][e], fops<T>::mul(au[q], x[q][ch][e]));
+    }
+    for (; u < cnt; ++u) {
+      const int cu = __shfl_sync(gmask, c, u, LPR);
+      const T au = __shfl_sync(gmask, a, u, LPR);
+      T x[NCH][VEC];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) xl(cu, ch, x[ch]);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          acc[ch][e] = fops<T>::add(acc[ch][e], fops<T>::mul(au, x[ch][e]));
+    }
+  }
+}
+
+// ---- SpMM over a row list (short rows) ------------------------------------
+template <class T, int VEC, int LPR, int NCH>
+__global__ void __launch_bounds__(256)
+    k_spmm_rows(int64_t nrows, const int* __restrict__ rows, int row0,
+                const int* __restrict__ rp, const int* __restrict__ ci,
+                const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                T* __restrict__ out, int ldo) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  if (g >= nrows) return;
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int r = rows ? __ldg(rows + g) : row0 + (int)g;
+  const int kb = __ldg(rp + r), ke = __ldg(rp + r + 1);
+  auto xl = [&](int c, int ch, T(&x)[VEC]) {
+    ldv<T, VEC>(x, X + (size_t)c * ldx + (ch * LPR + gl) * VEC);
+  };
+  T acc[NCH][VEC];
+  spmm_row<T, VEC, LPR, NCH>(kb, ke, ci, av, gl, gmask, xl, acc);
+  T* o = out + (size_t)r * ldo;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+}
+
+// Generic SpMM (any column count): one warp per row, scalar columns.
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_spmm_rows_generic(int64_t nrows, const int* __restrict__ rows, int row0,
+                        const int* __restrict__ rp, const int* __restrict__ ci,
+                        const T* __restrict__ av, const T* __restrict__ X,
+                        int ldx, int cc, T* __restrict__ out, int ldo) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= nrows) return;
+  const int lane = threadIdx.x & 31;
+  const int r = rows ? __ldg(rows + g) : row0 + (int)g;
+  const int kb = __ldg(rp + r), ke = __ldg(rp + r + 1);
+  for (int cb = 0; cb < cc; cb += 32) {
+    const int col = cb + lane;
+    T acc = T(0);
+    for (int k = kb; k < ke; ++k) {
+      const int c = __ldg(ci + k);
+      const T a = __ldg(av + k);
+      if (col < cc) acc = fops<T>::add(acc, fops<T>::mul(a, X[(size_t)c * ldx + col]));
+    }
+    if (col < cc) out[(size_t)r * ldo + col] = acc;
+  }
+}
+
+// Long rows: segment partials then an ordered combine.
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_spmm_segments(int64_t nseg, const int* __restrict__ seg_k0,
+                    const int* __restrict__ seg_k1, const int* __restrict__ ci,
+                    const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                    int cc, T* __restrict__ partial) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= nseg) return;
+  const int lane = threadIdx.x & 31;
+  const int kb = seg_k0[g], ke = seg_k1[g];
+  for (int cb = 0; cb < cc; cb += 32) {
+    const int col = cb + lane;
+    T acc = T(0);
+    int k = kb;
+    for (; k + 4 <= ke; k += 4) {
+      int c[4];
+      T a[4], x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        c[q] = __ldg(ci + k + q);
+        a[q] = __ldg(av + k + q);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = col < cc ? X[(size_t)c[q] * ldx + col] : T(0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc = fops<T>::add(acc, fops<T>::mul(a[q], x[q]));
+    }
+    for (; k < ke; ++k) {
+      const int c = __ldg(ci + k);
+      const T a = __ldg(av + k);
+      if (col < cc) acc = fops<T>::add(acc, fops<T>::mul(a, X[(size_t)c * ldx + col]));
+    }
+    if (col < cc) partial[(size_t)g * cc + col] = acc;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_segment_combine(int64_t nlong, const int* __restrict__ long_rows,
+                      const int64_t* __restrict__ long_seg_off,
+                      const T* __restrict__ partial, int cc,
+                      T* __restrict__ out, int ldo) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= nlong) return;
+  const int lane = threadIdx.x & 31;
+  const int r = long_rows[g];
+  const int64_t s0 = long_seg_off[g], s1 = long_seg_off[g + 1];
+  for (int col = lane; col < cc; col += 32) {
+    T acc = partial[(size_t)s0 * cc + col];
+    for (int64_t s = s0 + 1; s < s1; ++s)
+      acc = fops<T>::add(acc, partial[(size_t)s * cc + col]);
+    out[(size_t)r * ldo + col] = acc;
+  }
+}
+
+// ---- dense first op: D1[rows, :] = B[rows, :] C, register tiled ----------
+// Per element: acc = fma(B[i,j], C[j,k], acc) for j ascending from 0, the
+// same sequence the fused kernel uses, so fused and unfused agree bitwise.
+template <class T, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    k_gemm_blocks(int64_t nblk, const int* __restrict__ blk_r0,
+                  const int* __restrict__ blk_cnt, const T* __restrict__ B,
+                  int bc, const T* __restrict__ C, int cc,
+                  T* __restrict__ D1, int ldd) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  __shared__ __align__(16) T As[BK][BM];
+  __shared__ __align__(16) T Cs[BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int n0 = blockIdx.y * BN;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int r0 = blk_r0[blk], cnt = blk_cnt[blk];
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    for (int k0 = 0; k0 < bc; k0 += BK) {
+      const int kn = min(BK, bc - k0);
+      for (int e = tid; e < BM * BK; e += NT) {
+        const int m = e / BK, kk = e % BK;
+        As[kk][m] = (m < cnt && kk < kn) ? B[(size_t)(r0 + m) * bc + k0 + kk] : T(0);
+      }
+      for (int e = tid; e < BK * BN; e += NT) {
+        const int kk = e / BN, nn = e % BN;
+        Cs[kk][nn] = (kk < kn && n0 + nn < cc) ? C[(size_t)(k0 + kk) * cc + n0 + nn] : T(0);
+      }
+      __syncthreads();
+      for (int kk = 0; kk < kn; ++kk) {
+        T a[TM], b[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = Cs[kk][tx * TN + j];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fops<T>::fma(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = ty * TM + i;
+      if (m >= cnt) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int col = n0 + tx * TN + j;
+        if (col < cc) D1[(size_t)(r0 + m) * ldd + col] = acc[i][j];
+      }
+    }
+  }
+}
+
+// ---- fused wavefront-0 kernel ----------------------------------------------
+// blockIdx.x = fused tile, blockIdx.y = column slice [c0, c0+cs).
+// smem: [stage: w_cap x cs][C slice: bc x cs (dense B only)]
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_fused_tiles(int64_t ntiles, const int* __restrict__ t_ilo,
+                  const int* __restrict__ t_ihi,
+                  const int64_t* __restrict__ t_joff,
+                  const int* __restrict__ jrows, int w_cap, int cs, int cc,
+                  int b_dense, const T* __restrict__ Bd, int bc,
+                  const int* __restrict__ brp, const int* __restrict__ bci,
+                  const T* __restrict__ bv, const T* __restrict__ C,
+                  const int* __restrict__ arp, const int* __restrict__ aci,
+                  const T* __restrict__ av, const uint8_t* __restrict__ spill,
+                  T* D1, T* __restrict__ D) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* stage = reinterpret_cast<T*>(smem_raw);
+  T* Cs = stage + (size_t)w_cap * cs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int c0 = blockIdx.y * cs;
+  const int csn = min(cs, cc - c0);  // columns in this slice
+  constexpr int MAXQ = 4;            // cs <= 128
+  if (b_dense) {
+    for (int e = threadIdx.x; e < bc * cs; e += blockDim.x) {
+      const int j = e / cs, col = e % cs;
+      Cs[e] = col < csn ? C[(size_t)j * cc + c0 + col] : T(0);
+    }
+    __syncthreads();
+  }
+  for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+    const int ilo = t_ilo[v], ihi = t_ihi[v];
+    const bool in_smem = (ihi - ilo) <= w_cap;
+    // phase 1: D1 slice of rows [ilo, ihi)
+    for (int i = ilo + warp; i < ihi; i += nwarps) {
+      T acc[MAXQ];
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) acc[q] = T(0);
+      if (b_dense) {
+        const T* brow = Bd + (size_t)i * bc;
+        for (int j0 = 0; j0 < bc; j0 += 32) {
+          const T bvv = j0 + lane < bc ? brow[j0 + lane] : T(0);
+          const int cnt = min(32, bc - j0);
+          for (int u = 0; u < cnt; ++u) {
+            const T b = __shfl_sync(0xffffffffu, bvv, u);
+            const T* crow = Cs + (size_t)(j0 + u) * cs;
+#pragma unroll
+            for (int q = 0; q < MAXQ; ++q) {
+              const int col = lane + 32 * q;
+              if (col < csn) acc[q] = fops<T>::fma(b, crow[col], acc[q]);
+            }
+          }
+        }
+      } else {
+        const int kb = brp[i], ke = brp[i + 1];
+        for (int k = kb; k < ke; ++k) {
+          const int c = __ldg(bci + k);
+          const T a = __ldg(bv + k);
+          const T* xrow = C + (size_t)c * cc + c0;
+#pragma unroll
+          for (int q = 0; q < MAXQ; ++q) {
+            const int col = lane + 32 * q;
+            if (col < csn) acc[q] = fops<T>::add(acc[q], fops<T>::mul(a, xrow[col]));
+          }
+        }
+      }
+      const bool sp = spill[i] != 0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int col = lane + 32 * q;
+        if (col < csn) {
+          if (in_smem) stage[(size_t)(i - ilo) * cs + col] = acc[q];
+          if (sp || !in_smem) D1[(size_t)i * cc + c0 + col] = acc[q];
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2: fused D rows from the staged slice
+    const int64_t jb = t_joff[v], je = t_joff[v + 1];
+    for (int64_t q0 = jb + warp; q0 < je; q0 += nwarps) {
+      const int j = jrows[q0];
+      const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
+      T acc[MAXQ];
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) acc[q] = T(0);
+      for (int k = kb; k < ke; ++k) {
+        const int c = __ldg(aci + k);
+        const T a = __ldg(av + k);
+        const T* xrow = in_smem ? stage + (size_t)(c - ilo) * cs
+                                : D1 + (size_t)c * cc + c0;
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int col = lane + 32 * q;
+          if (col < csn) acc[q] = fops<T>::add(acc[q], fops<T>::mul(a, xrow[col]));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int col = lane + 32 * q;
+        if (col < csn) D[(size_t)j * cc + c0 + col] = acc[q];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// spill[c] = 1 for every column c of every wavefront-1 row
+__global__ void k_mark_spill(int64_t nrows, const int* __restrict__ rows,
+                             const int* __restrict__ rp,
+                             const int* __restrict__ ci, uint8_t* spill) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= nrows) return;
+  const int lane = threadIdx.x & 31;
+  const int r = rows[g];
+  for (int k = rp[r] + lane; k < rp[r + 1]; k += 32) spill[ci[k]] = 1;
+}
+
+__global__ void k_count_u8(int64_t n, const uint8_t* f, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += f[i];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+template <class T>
+__global__ void k_gather_rows(const T* __restrict__ src, int cols,
+                              const int* __restrict__ rows, int64_t n,
+                              T* __restrict__ dst) {
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = (int)(e % cols);
+    dst[e] = src[(size_t)rows[r] * cols + c];
+  }
+}
+template <class T>
+__global__ void k_scatter_rows(const T* __restrict__ src, int cols,
+                               const int* __restrict__ rows, int64_t n,
+                               T* __restrict__ dst) {
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = (int)(e % cols);
+    dst[(size_t)rows[r] * cols + c] = src[e];
+  }
+}
+
+inline int blocks_for(int64_t threads, int per_block = 256) {
+  int64_t b = (threads + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, b);
+}
+
+}  // namespace
+
+// ===========================================================================
+// Row-SpMM work list: short rows (one group per row) + segmented long rows.
+// ===========================================================================
+struct SpmmWork {
+  int64_t n_short = 0, n_long = 0, n_seg = 0;
+  bool identity = false;  // short rows are exactly [row0, row0 + n_short)
+  int row0 = 0;
+  dbuf<int> short_rows, long_rows, seg_k0, seg_k1;
+  dbuf<int64_t> long_seg_off;
+  dbuf<unsigned char> partial;
+
+  // rows: host row list (ascending not required); rp: host row_ptr
+  void build(const std::vector<int>& rows, const std::vector<int>& rp, int cc,
+             size_t elem, cudaStream_t st) {
+    std::vector<int> sh, lg, k0, k1;
+    std::vector<int64_t> off{0};
+    sh.reserve(rows.size());
+    for (int r : rows) {
+      const int b = rp[r], e = rp[r + 1];
+      if (e - b <= kLongRow) {
+        sh.push_back(r);
+      } else {
+        lg.push_back(r);
+        for (int k = b; k < e; k += kSegLen) {
+          k0.push_back(k);
+          k1.push_back(std::min(e, k + kSegLen));
+        }
+        off.push_back((int64_t)k0.size());
+      }
+    }
+    n_short = (int64_t)sh.size();
+    n_long = (int64_t)lg.size();
+    n_seg = (int64_t)k0.size();
+    identity = false;
+    if (n_short > 0 && n_long == 0) {
+      bool id = true;
+      for (int64_t q = 1; q < n_short && id; ++q) id = sh[q] == sh[q - 1] + 1;
+      if (id) {
+        identity = true;
+        row0 = sh[0];
+      }
+    }
+    if (!identity) {
+      short_rows.alloc(sh.size());
+      h2d(short_rows.p, sh.data(), sh.size(), st);
+    }
+    long_rows.alloc(lg.size());
+    h2d(long_rows.p, lg.data(), lg.size(), st);
+    seg_k0.alloc(k0.size());
+    seg_k1.alloc(k1.size());
+    h2d(seg_k0.p, k0.data(), k0.size(), st);
+    h2d(seg_k1.p, k1.data(), k1.size(), st);
+    long_seg_off.alloc(off.size());
+    h2d(long_seg_off.p, off.data(), off.size(), st);
+    partial.alloc((size_t)n_seg * cc * elem);
+    TFG_CUDA(cudaStreamSynchronize(st));
+  }
+  size_t bytes() const {
+    return short_rows.bytes() + long_rows.bytes() + seg_k0.bytes() +
+           seg_k1.bytes() + long_seg_off.bytes() + partial.bytes();
+  }
+  int launches() const { return (n_short > 0) + 2 * (n_long > 0); }
+};
+
+template <class T>
+static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
+                                const T* av, const T* X, int cc, T* out,
+                                cudaStream_t st) {
+  if (w.n_short == 0) return;
+  const int* rows = w.identity ? nullptr : w.short_rows.p;
+  const int row0 = w.identity ? w.row0 : 0;
+  const int64_t n = w.n_short;
+  constexpr int VEC = 16 / sizeof(T);
+#define TFG_SPMM_CASE(LPR, NCH)                                                  \
+  k_spmm_rows<T, VEC, LPR, NCH><<<blocks_for(n * LPR), 256, 0, st>>>(            \
+      n, rows, row0, rp, ci, av, X, cc, out, cc);                                \
+  TFG_LAUNCH_CHECK();                                                            \
+  return;
+  if (cc % VEC == 0) {
+    const int L = cc / VEC;
+    switch (L) {
+      case 4: TFG_SPMM_CASE(4, 1)
+      case 8: TFG_SPMM_CASE(8, 1)
+      case 16: TFG_SPMM_CASE(16, 1)
+      case 32: TFG_SPMM_CASE(32, 1)
+      case 64: TFG_SPMM_CASE(32, 2)
+      default: break;
+    }
+  }
+#undef TFG_SPMM_CASE
+  k_spmm_rows_generic<T><<<blocks_for(n * 32), 256, 0, st>>>(n, rows, row0, rp, ci, av,
+                                                               X, cc, cc, out, cc);
+  TFG_LAUNCH_CHECK();
+}
+
+template <class T>
+static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
+                     const T* av, const T* X, int cc, T* out, cudaStream_t st) {
+  spmm_dispatch_short<T>(w, rp, ci, av, X, cc, out, st);
+  if (w.n_long) {
+    T* partial = reinterpret_cast<T*>(w.partial.p);
+    k_spmm_segments<T><<<blocks_for(w.n_seg * 32), 256, 0, st>>>(
+        w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, cc, partial);
+    TFG_LAUNCH_CHECK();
+    k_segment_combine<T><<<blocks_for(w.n_long * 32), 256, 0, st>>>(
+        w.n_long, w.long_rows.p, w.long_seg_off.p, partial, cc, out, cc);
+    TFG_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace tfg
+
+// ===========================================================================
+// The plan behind tfg_plan.
+// ===========================================================================
+struct tfg_plan {
+  tfg_problem p{};
+  size_t elem = 8;
+  bool has_sched = false;
+  bool zero_d = false;  // schedule does not cover every j row
+  // (a) first op for j-less wavefront-0 tiles / all rows when unfused
+  int64_t n_fo_blocks = 0;
+  tfg::dbuf<int> fo_r0, fo_cnt;  // dense B: GEMM row blocks
+  tfg::SpmmWork fo_sparse;       // sparse B: SpMM rows with X = C
+  // (b) fused tiles
+  int64_t n_ftiles = 0;
+  tfg::dbuf<int> ft_ilo, ft_ihi, ft_jrows;
+  tfg::dbuf<int64_t> ft_joff;
+  int w_cap = 0, cs = 0, n_slices = 0;
+  size_t fused_smem = 0;
+  // (c) wavefront 1 / unfused second op
+  tfg::SpmmWork second;
+  tfg::dbuf<uint8_t> spill;
+  tfg::dbuf<unsigned char> d1;
+  // accounting
+  int64_t spill_rows = 0, fused_rows = 0;
+  int64_t first_rows = 0, second_rows = 0, nnz_processed = 0;
+  int launches = 0;
+};
+
+namespace tfg {
+
+static constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16, kGemmTM = 4, kGemmTN = 4;
+static constexpr size_t kFusedSmemCap = 200 * 1024;
+
+void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
+                 tfg_plan& pl) {
+  // problem.check() -- kernels.hpp:35-42; require_workers is the caller's.
+  if (pr.dtype != TFG_F32 && pr.dtype != TFG_F64)
+    throw invalid_argument("problem: unknown dtype");
+  if (pr.n < 1) throw invalid_argument("problem: A must be square");
+  if (pr.b_rows != pr.n) throw invalid_argument("problem: B must have n rows");
+  if (pr.c_rows != pr.b_cols)
+    throw invalid_argument("problem: C rows must match B cols");
+  if (pr.c_cols < 1 || pr.b_cols < 1)
+    throw invalid_argument("problem: B and C need at least one column");
+  if (s && s->n != pr.n)
+    throw invalid_argument("schedule and problem disagree on n");
+
+  pl.p = pr;
+  pl.elem = pr.dtype == TFG_F64 ? 8 : 4;
+  pl.has_sched = s != nullptr;
+  const int n = pr.n, cc = pr.c_cols, bc = pr.b_cols;
+
+  std::vector<int> arp(n + 1), brp;
+  d2h(arp.data(), pr.d_a_row_ptr, n + 1, st);
+  if (!pr.b_is_dense) {
+    brp.resize(n + 1);
+    d2h(brp.data(), pr.d_b_row_ptr, n + 1, st);
+  }
+  TFG_CUDA(cudaStreamSynchronize(st));
+  pl.nnz_processed = arp[n];
+  pl.d1.alloc((size_t)n * cc * pl.elem);
+  pl.spill.alloc(n);
+
+  std::vector<int> fo_rows;  // first-op rows handled by stage (a)
+  std::vector<int> second_rows;
+  if (!s) {
+    fo_rows.resize(n);
+    for (int i = 0; i < n; ++i) fo_rows[i] = i;
+    second_rows = fo_rows;
+    pl.first_rows = n;
+    pl.second_rows = n;
+    pl.spill_rows = n;
+  } else {
+    const int64_t nt0 = s->n_tiles[0];
+    std::vector<int> ilo(nt0), ihi(nt0);
+    std::vector<int64_t> joff(nt0 + 1);
+    d2h(ilo.data(), s->i_lo[0].p, nt0, st);
+    d2h(ihi.data(), s->i_hi[0].p, nt0, st);
+    d2h(joff.data(), s->j_off[0].p, nt0 + 1, st);
+    const int64_t nj1 = s->n_jrows[1];
+    second_rows.resize(nj1);
+    d2h(second_rows.data(), s->j_rows[1].p, nj1, st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> f_ilo, f_ihi;
+    std::vector<int64_t> f_joff{0};
+    std::vector<int64_t> f_src;  // source offset of each fused tile's j list
+    int w_max = 0;
+    for (int64_t v = 0; v < nt0; ++v) {
+      const int64_t nj = joff[v + 1] - joff[v];
+      pl.first_rows += ihi[v] - ilo[v];
+      if (nj == 0) {
+        for (int i = ilo[v]; i < ihi[v]; ++i) fo_rows.push_back(i);
+      } else {
+        f_ilo.push_back(ilo[v]);
+        f_ihi.push_back(ihi[v]);
+        f_src.push_back(joff[v]);
+        f_joff.push_back(f_joff.back() + nj);
+        w_max = std::max(w_max, ihi[v] - ilo[v]);
+      }
+    }
+    pl.fused_rows = s->n_jrows[0];
+    pl.second_rows = s->n_jrows[0] + s->n_jrows[1];
+    pl.zero_d = pl.second_rows != n;
+    pl.n_ftiles = (int64_t)f_ilo.size();
+    if (pl.n_ftiles) {
+      pl.ft_ilo.alloc(pl.n_ftiles);
+      pl.ft_ihi.alloc(pl.n_ftiles);
+      pl.ft_joff.alloc(pl.n_ftiles + 1);
+      h2d(pl.ft_ilo.p, f_ilo.data(), f_ilo.size(), st);
+      h2d(pl.ft_ihi.p, f_ihi.data(), f_ihi.size(), st);
+      h2d(pl.ft_joff.p, f_joff.data(), f_joff.size(), st);
+      // gather the fused tiles' j lists contiguously
+      pl.ft_jrows.alloc(f_joff.back());
+      for (size_t k = 0; k < f_src.size(); ++k)
+        TFG_CUDA(cudaMemcpyAsync(pl.ft_jrows.p + f_joff[k], s->j_rows[0].p + f_src[k],
+                                 (f_joff[k + 1] - f_joff[k]) * sizeof(int),
+                                 cudaMemcpyDeviceToDevice, st));
+      // column slice: whole cc when the widest tile fits, else halve
+      int cs = std::min(cc, 128);
+      auto need = [&](int w, int c) {
+        return (size_t)w * c * pl.elem + (pr.b_is_dense ? (size_t)bc * c * pl.elem : 0);
+      };
+      while (cs > 32 && need(w_max, cs) > kFusedSmemCap) cs = (cs + 1) / 2;
+      const size_t c_bytes = pr.b_is_dense ? (size_t)bc * cs * pl.elem : 0;
+      if (c_bytes + (size_t)cs * pl.elem > kFusedSmemCap)
+        throw runtime_error("fused executor: C slice does not fit in shared memory");
+      int w_cap = (int)std::min<size_t>((size_t)w_max,
+                                        (kFusedSmemCap - c_bytes) / ((size_t)cs * pl.elem));
+      pl.cs = cs;
+      pl.w_cap = std::max(w_cap, 0);
+      pl.n_slices = (cc + cs - 1) / cs;
+      pl.fused_smem = (size_t)pl.w_cap * cs * pl.elem + c_bytes;
+    }
+    // spill set S = columns of wavefront-1 rows
+    TFG_CUDA(cudaMemsetAsync(pl.spill.p, 0, n, st));
+    if (nj1) {
+      k_mark_spill<<<blocks_for(nj1 * 32), 256, 0, st>>>(nj1, s->j_rows[1].p, pr.d_a_row_ptr,
+                                                          pr.d_a_col_idx, pl.spill.p);
+      TFG_LAUNCH_CHECK();
+    }
+    dbuf<unsigned long long> cnt(1);
+    TFG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+    k_count_u8<<<256, 256, 0, st>>>(n, pl.spill.p, cnt.p);
+    TFG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    d2h(&h, cnt.p, 1, st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+    pl.spill_rows = (int64_t)h;
+  }
+  if (!s) TFG_CUDA(cudaMemsetAsync(pl.spill.p, 1, n, st));
+
+  // (a) first-op work
+  if (pr.b_is_dense) {
+    std::vector<int> r0, cnt;
+    size_t q = 0;
+    while (q < fo_rows.size()) {
+      size_t e = q + 1;
+      while (e < fo_rows.size() && fo_rows[e] == fo_rows[e - 1] + 1 &&
+             (int)(e - q) < kGemmBM)
+        ++e;
+      r0.push_back(fo_rows[q]);
+      cnt.push_back((int)(e - q));
+      q = e;
+    }
+    pl.n_fo_blocks = (int64_t)r0.size();
+    pl.fo_r0.alloc(r0.size());
+    pl.fo_cnt.alloc(cnt.size());
+    h2d(pl.fo_r0.p, r0.data(), r0.size(), st);
+    h2d(pl.fo_cnt.p, cnt.data(), cnt.size(), st);
+  } else {
+    pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st);
+  }
+  // (c) second-op work
+  pl.second.build(second_rows, arp, cc, pl.elem, st);
+
+  pl.launches = 0;
+  if (pr.b_is_dense)
+    pl.launches += pl.n_fo_blocks > 0;
+  else
+    pl.launches += pl.fo_sparse.launches();
+  pl.launches += pl.n_ftiles > 0;
+  pl.launches += pl.second.launches();
+  TFG_CUDA(cudaStreamSynchronize(st));
+}
+
+template <class T>
+static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st) {
+  const tfg_problem& pr = pl.p;
+  const int cc = pr.c_cols, bc = pr.b_cols;
+  T* D1 = reinterpret_cast<T*>(pl.d1.p);
+  const T* C = static_cast<const T*>(pr.d_c);
+  if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
+  // (a)
+  if (pr.b_is_dense) {
+    if (pl.n_fo_blocks) {
+      const int gy = (cc + kGemmBN - 1) / kGemmBN;
+      const int64_t gx = std::min<int64_t>(pl.n_fo_blocks, (int64_t)sm_count() * 16);
+      k_gemm_blocks<T, kGemmBM, kGemmBN, kGemmBK, kGemmTM, kGemmTN>
+          <<<dim3((unsigned)gx, gy), (kGemmBM / kGemmTM) * (kGemmBN / kGemmTN), 0, st>>>(
+              pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p, static_cast<const T*>(pr.d_b_dense),
+              bc, C, cc, D1, cc);
+      TFG_LAUNCH_CHECK();
+    }
+  } else {
+    spmm_run<T>(pl.fo_sparse, pr.d_b_row_ptr, pr.d_b_col_idx,
+                static_cast<const T*>(pr.d_b_val), C, cc, D1, st);
+  }
+  // (b)
+  if (pl.n_ftiles) {
+    if (pl.fused_smem > 48 * 1024)
+      TFG_CUDA(cudaFuncSetAttribute(k_fused_tiles<T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)pl.fused_smem));
+    const int64_t gx = std::min<int64_t>(pl.n_ftiles, 65535);
+    k_fused_tiles<T><<<dim3((unsigned)gx, pl.n_slices), 256, pl.fused_smem, st>>>(
+        pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, pl.ft_joff.p, pl.ft_jrows.p, pl.w_cap,
+        pl.cs, cc, pr.b_is_dense, static_cast<const T*>(pr.d_b_dense), bc, pr.d_b_row_ptr,
+        pr.d_b_col_idx, static_cast<const T*>(pr.d_b_val), C, pr.d_a_row_ptr,
+        pr.d_a_col_idx, static_cast<const T*>(pr.d_a_val), pl.spill.p, D1, D);
+    TFG_LAUNCH_CHECK();
+  }
+  // (c)
+  spmm_run<T>(pl.second, pr.d_a_row_ptr, pr.d_a_col_idx,
+              static_cast<const T*>(pr.d_a_val), D1, cc, D, st);
+}
+
+void plan_execute(tfg_plan& pl, void* d, cudaStream_t st) {
+  if (pl.p.dtype == TFG_F64)
+    plan_execute_t<double>(pl, static_cast<double*>(d), st);
+  else
+    plan_execute_t<float>(pl, static_cast<float*>(d), st);
+}
+
+void gather_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
+                 void* dst, cudaStream_t st) {
+  if (n == 0) return;
+  const int g = (int)std::min<int64_t>((n * cols + 255) / 256, (int64_t)sm_count() * 16);
+  if (dtype == TFG_F64)
+    k_gather_rows<double><<<g, 256, 0, st>>>(static_cast<const double*>(src), cols, rows, n,
+                                             static_cast<double*>(dst));
+  else
+    k_gather_rows<float><<<g, 256, 0, st>>>(static_cast<const float*>(src), cols, rows, n,
+                                            static_cast<float*>(dst));
+  TFG_LAUNCH_CHECK();
+}
+
+void scatter_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
+                  void* dst, cudaStream_t st) {
+  if (n == 0) return;
+  const int g = (int)std::min<int64_t>((n * cols + 255) / 256, (int64_t)sm_count() * 16);
+  if (dtype == TFG_F64)
+    k_scatter_rows<double><<<g, 256, 0, st>>>(static_cast<const double*>(src), cols, rows, n,
+                                              static_cast<double*>(dst));
+  else
+    k_scatter_rows<float><<<g, 256, 0, st>>>(static_cast<const float*>(src), cols, rows, n,
+                                             static_cast<float*>(dst));
+  TFG_LAUNCH_CHECK();
+}
+
+size_t plan_scratch_bytes(const tfg_plan& pl) {
+  return pl.d1.bytes() + pl.spill.bytes() + pl.fo_r0.bytes() + pl.fo_cnt.bytes() +
+         pl.fo_sparse.bytes() + pl.ft_ilo.bytes() + pl.ft_ihi.bytes() + pl.ft_joff.bytes() +
+         pl.ft_jrows.bytes() + pl.second.bytes();
+}
+
+}  // namespace tfg
+
+// ===========================================================================
+// C-ABI: plans (include/tfg.h)
+// ===========================================================================
+using namespace tfg;
+
+extern "C" {
+
+tfg_status tfg_plan_create(const tfg_problem* p, const tfg_schedule* s, void* stream,
+                           tfg_plan** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!p) throw invalid_argument("plan_create: null problem");
+    auto* pl = new tfg_plan;
+    try {
+      plan_create(*p, s, as_stream(stream), *pl);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    *out = pl;
+  });
+}
+
+tfg_status tfg_plan_execute(tfg_plan* pl, void* d, void* stream) {
+  return guard([&] {
+    if (!pl || !d) throw invalid_argument("plan_execute: null plan or output");
+    plan_execute(*pl, d, as_stream(stream));
+  });
+}
+
+tfg_status tfg_plan_stats(const tfg_plan* pl, int64_t* fr, int64_t* sr, int64_t* nnz) {
+  return guard([&] {
+    if (!pl) throw invalid_argument("plan_stats: null plan");
+    if (fr) *fr = pl->first_rows;
+    if (sr) *sr = pl->second_rows;
+    if (nnz) *nnz = pl->nnz_processed;
+  });
+}
+
+tfg_status tfg_plan_info(const tfg_plan* pl, int64_t* spill_rows, int64_t* fused_rows,
+                         int32_t* launches, int64_t* scratch_bytes) {
+  return guard([&] {
+    if (!pl) throw invalid_argument("plan_info: null plan");
+    if (spill_rows) *spill_rows = pl->spill_rows;
+    if (fused_rows) *fused_rows = pl->fused_rows;
+    if (launches) *launches = pl->launches + (pl->zero_d ? 1 : 0);
+    if (scratch_bytes) *scratch_bytes = (int64_t)plan_scratch_bytes(*pl);
+  });
+}
+
+void tfg_plan_destroy(tfg_plan* pl) { delete pl; }
+
+tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d) {
+  return guard([&] {
+    if (!hp) throw invalid_argument("run_host: null problem");
+    const tfg_problem& h = *hp;
+    if (h.n < 1) throw invalid_argument("problem: A must be square");
+    const size_t el = h.dtype == TFG_F64 ? 8 : 4;
+    cudaStream_t st = nullptr;
+    const int64_t annz = h.d_a_row_ptr[h.n];
+    dbuf<int32_t> arp(h.n + 1), aci(std::max<int64_t>(annz, 1));
+    dbuf<unsigned char> av(std::max<int64_t>(annz, 1) * el);
+    h2d(arp.p, h.d_a_row_ptr, h.n + 1, st);
+    h2d(aci.p, h.d_a_col_idx, annz, st);
+    h2d(av.p, static_cast<const unsigned char*>(h.d_a_val), annz * el, st);
+    dbuf<int32_t> brp, bci;
+    dbuf<unsigned char> bv, bd, c;
+    tfg_problem d = h;
+    d.a_nnz = annz;
+    d.d_a_row_ptr = arp.p;
+    d.d_a_col_idx = aci.p;
+    d.d_a_val = av.p;
+    if (h.b_is_dense) {
+      bd.alloc((size_t)std::max(h.b_rows, 1) * std::max(h.b_cols, 1) * el);
+      h2d(bd.p, static_cast<const unsigned char*>(h.d_b_dense), (size_t)h.b_rows * h.b_cols * el,
+          st);
+      d.d_b_dense = bd.p;
+    } else {
+      const int64_t bnnz = h.d_b_row_ptr[h.b_rows];
+      brp.alloc(h.b_rows + 1);
+      bci.alloc(std::max<int64_t>(bnnz, 1));
+      bv.alloc(std::max<int64_t>(bnnz, 1) * el);
+      h2d(brp.p, h.d_b_row_ptr, h.b_rows + 1, st);
+      h2d(bci.p, h.d_b_col_idx, bnnz, st);
+      h2d(bv.p, static_cast<const unsigned char*>(h.d_b_val), bnnz * el, st);
+      d.b_nnz = bnnz;
+      d.d_b_row_ptr = brp.p;
+      d.d_b_col_idx = bci.p;
+      d.d_b_val = bv.p;
+    }
+    c.alloc((size_t)std::max(h.c_rows, 1) * std::max(h.c_cols, 1) * el);
+    h2d(c.p, static_cast<const unsigned char*>(h.d_c), (size_t)h.c_rows * h.c_cols * el, st);
+    d.d_c = c.p;
+    tfg_plan pl;
+    plan_create(d, s, st, pl);
+    dbuf<unsigned char> dd((size_t)h.n * h.c_cols * el);
+    plan_execute(pl, dd.p, st);
+    d2h(static_cast<unsigned char*>(h_d), dd.p, (size_t)h.n * h.c_cols * el, st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+tfg_status tfg_gather_rows(int32_t dtype, const void* src, int32_t cols, const int32_t* rows,
+                           int64_t n, void* dst, void* stream) {
+  return guard([&] { gather_rows(dtype, src, cols, rows, n, dst, as_stream(stream)); });
+}
+
+tfg_status tfg_scatter_rows(int32_t dtype, const void* src, int32_t cols, const int32_t* rows,
+                            int64_t n, void* dst, void* stream) {
+  return guard([&] { scatter_rows(dtype, src, cols, rows, n, dst, as_stream(stream)); });
+}
+
+}  // extern "C"
