@@ -186,6 +186,15 @@ tfg_status tfg_plan_info(const tfg_plan *plan, int64_t *spill_rows,
                          int64_t *fused_rows, int32_t *launches,
                          int64_t *scratch_bytes);
 
+/* Execute once with CUDA events around each stage on `stream`, wait, and
+ * report device milliseconds and algorithmic HBM bytes (each input byte read
+ * once, each output byte written once) per stage:
+ *   [0] first op of wavefront-0 tiles that fuse no row (or all rows, unfused)
+ *   [1] fused wavefront-0 tiles      [2] wavefront-1 / second-op SpMM.
+ * Used for the roofline numbers; not for the hot loop. */
+tfg_status tfg_plan_profile(tfg_plan *plan, void *d_d, void *stream,
+                            double stage_ms[3], int64_t stage_bytes[3]);
+
 void tfg_plan_destroy(tfg_plan *plan);
 
 /* One-shot host entry used by the C++ mirror for the reference's

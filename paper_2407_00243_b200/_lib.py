@@ -84,6 +84,7 @@ SIGNATURES = [
     ("tfg_plan_execute", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tfg_plan_stats", C.c_int, [C.c_void_p, i64p, i64p, i64p]),
     ("tfg_plan_info", C.c_int, [C.c_void_p, i64p, i64p, i32p, i64p]),
+    ("tfg_plan_profile", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, f64p, i64p]),
     ("tfg_plan_destroy", None, [C.c_void_p]),
     ("tfg_run_host", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p]),
     ("tfg_gather_rows", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,

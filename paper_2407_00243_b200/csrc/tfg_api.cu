@@ -19,7 +19,7 @@ void build_schedule_device(int32_t n_rows, int32_t n_cols, int64_t nnz,
                            tfg_schedule& out);
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                  tfg_plan& pl);
-void plan_execute(tfg_plan& pl, void* d, cudaStream_t st);
+void plan_execute(tfg_plan& pl, void* d, cudaStream_t st, cudaEvent_t* ev);
 size_t plan_scratch_bytes(const tfg_plan& pl);
 void gather_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
                  void* dst, cudaStream_t st);

@@ -427,6 +427,17 @@ __global__ void k_mark_spill(int64_t nrows, const int* __restrict__ rows,
   for (int k = rp[r] + lane; k < rp[r + 1]; k += 32) spill[ci[k]] = 1;
 }
 
+// mark[c] = 1 for every column of the listed rows (distinct-row accounting)
+__global__ void k_mark_cols(int64_t nrows, const int* __restrict__ rows,
+                            const int* __restrict__ rp, const int* __restrict__ ci,
+                            uint8_t* mark) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= nrows) return;
+  const int lane = threadIdx.x & 31;
+  const int r = rows[g];
+  for (int k = rp[r] + lane; k < rp[r + 1]; k += 32) mark[ci[k]] = 1;
+}
+
 __global__ void k_count_u8(int64_t n, const uint8_t* f, unsigned long long* out) {
   unsigned long long c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -606,6 +617,10 @@ struct tfg_plan {
   int64_t spill_rows = 0, fused_rows = 0;
   int64_t first_rows = 0, second_rows = 0, nnz_processed = 0;
   int launches = 0;
+  // algorithmic (compulsory) HBM bytes per stage: (a) first op, (b) fused
+  // tiles, (c) wavefront-1 SpMM -- each input byte read once, each output
+  // byte written once (the roofline numerator)
+  int64_t stage_bytes[3] = {0, 0, 0};
 };
 
 namespace tfg {
@@ -755,6 +770,74 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   // (c) second-op work
   pl.second.build(second_rows, arp, cc, pl.elem, st);
 
+  // ---- algorithmic bytes per stage ------------------------------------
+  {
+    const int64_t el = (int64_t)pl.elem;
+    auto csr_rows_bytes = [&](const std::vector<int>& rows, const std::vector<int>& rp) {
+      int64_t b = 0;
+      for (int r : rows) b += 4 + (int64_t)(rp[r + 1] - rp[r]) * (4 + el);
+      return b;
+    };
+    // distinct X rows referenced by `rows` of the CSR (rp_d, ci_d)
+    auto distinct_cols = [&](const std::vector<int>& rows, const int* rp_d, const int* ci_d,
+                             int ncols) -> int64_t {
+      if (rows.empty()) return 0;
+      dbuf<int> rows_d(rows.size());
+      h2d(rows_d.p, rows.data(), rows.size(), st);
+      dbuf<uint8_t> mark(ncols);
+      TFG_CUDA(cudaMemsetAsync(mark.p, 0, ncols, st));
+      k_mark_cols<<<blocks_for((int64_t)rows.size() * 32), 256, 0, st>>>(
+          (int64_t)rows.size(), rows_d.p, rp_d, ci_d, mark.p);
+      TFG_LAUNCH_CHECK();
+      dbuf<unsigned long long> cnt(1);
+      TFG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+      k_count_u8<<<256, 256, 0, st>>>(ncols, mark.p, cnt.p);
+      TFG_LAUNCH_CHECK();
+      unsigned long long h = 0;
+      d2h(&h, cnt.p, 1, st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+      return (int64_t)h;
+    };
+    const int64_t ra = (int64_t)fo_rows.size();
+    if (ra) {
+      if (pr.b_is_dense)
+        pl.stage_bytes[0] = ra * bc * el + (int64_t)bc * cc * el + ra * cc * el;
+      else
+        pl.stage_bytes[0] = csr_rows_bytes(fo_rows, brp) +
+                            distinct_cols(fo_rows, pr.d_b_row_ptr, pr.d_b_col_idx, bc) * cc * el +
+                            ra * cc * el;
+    }
+    if (pl.n_ftiles) {
+      std::vector<int> ti, tj;  // first-op rows and fused j rows of fused tiles
+      std::vector<int> ilo(pl.n_ftiles), ihi(pl.n_ftiles);
+      d2h(ilo.data(), pl.ft_ilo.p, pl.n_ftiles, st);
+      d2h(ihi.data(), pl.ft_ihi.p, pl.n_ftiles, st);
+      tj.resize(pl.fused_rows);
+      d2h(tj.data(), pl.ft_jrows.p, pl.fused_rows, st);
+      std::vector<uint8_t> sp(n);
+      d2h(sp.data(), pl.spill.p, n, st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+      int64_t spilled = 0;
+      for (int64_t v = 0; v < pl.n_ftiles; ++v)
+        for (int i = ilo[v]; i < ihi[v]; ++i) {
+          ti.push_back(i);
+          spilled += sp[i];
+        }
+      const int64_t w = (int64_t)ti.size();
+      int64_t b = 0;
+      if (pr.b_is_dense)
+        b = w * bc * el + (int64_t)bc * cc * el;
+      else
+        b = csr_rows_bytes(ti, brp) + distinct_cols(ti, pr.d_b_row_ptr, pr.d_b_col_idx, bc) * cc * el;
+      b += csr_rows_bytes(tj, arp) + (int64_t)tj.size() * cc * el + spilled * cc * el;
+      pl.stage_bytes[1] = b;
+    }
+    if (!second_rows.empty())
+      pl.stage_bytes[2] = csr_rows_bytes(second_rows, arp) +
+                          distinct_cols(second_rows, pr.d_a_row_ptr, pr.d_a_col_idx, n) * cc * el +
+                          (int64_t)second_rows.size() * cc * el;
+  }
+
   pl.launches = 0;
   if (pr.b_is_dense)
     pl.launches += pl.n_fo_blocks > 0;
@@ -766,12 +849,13 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
 }
 
 template <class T>
-static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st) {
+static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev = nullptr) {
   const tfg_problem& pr = pl.p;
   const int cc = pr.c_cols, bc = pr.b_cols;
   T* D1 = reinterpret_cast<T*>(pl.d1.p);
   const T* C = static_cast<const T*>(pr.d_c);
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
+  if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
   // (a)
   if (pr.b_is_dense) {
     if (pl.n_fo_blocks) {
@@ -787,6 +871,7 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st) {
     spmm_run<T>(pl.fo_sparse, pr.d_b_row_ptr, pr.d_b_col_idx,
                 static_cast<const T*>(pr.d_b_val), C, cc, D1, st);
   }
+  if (ev) TFG_CUDA(cudaEventRecord(ev[1], st));
   // (b)
   if (pl.n_ftiles) {
     if (pl.fused_smem > 48 * 1024)
@@ -801,16 +886,18 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st) {
         pr.d_a_col_idx, static_cast<const T*>(pr.d_a_val), pl.spill.p, D1, D);
     TFG_LAUNCH_CHECK();
   }
+  if (ev) TFG_CUDA(cudaEventRecord(ev[2], st));
   // (c)
   spmm_run<T>(pl.second, pr.d_a_row_ptr, pr.d_a_col_idx,
               static_cast<const T*>(pr.d_a_val), D1, cc, D, st);
+  if (ev) TFG_CUDA(cudaEventRecord(ev[3], st));
 }
 
-void plan_execute(tfg_plan& pl, void* d, cudaStream_t st) {
+void plan_execute(tfg_plan& pl, void* d, cudaStream_t st, cudaEvent_t* ev = nullptr) {
   if (pl.p.dtype == TFG_F64)
-    plan_execute_t<double>(pl, static_cast<double*>(d), st);
+    plan_execute_t<double>(pl, static_cast<double*>(d), st, ev);
   else
-    plan_execute_t<float>(pl, static_cast<float*>(d), st);
+    plan_execute_t<float>(pl, static_cast<float*>(d), st, ev);
 }
 
 void gather_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
@@ -898,6 +985,25 @@ tfg_status tfg_plan_info(const tfg_plan* pl, int64_t* spill_rows, int64_t* fused
 }
 
 void tfg_plan_destroy(tfg_plan* pl) { delete pl; }
+
+tfg_status tfg_plan_profile(tfg_plan* pl, void* d, void* stream, double stage_ms[3],
+                            int64_t stage_bytes[3]) {
+  return guard([&] {
+    if (!pl || !d) throw invalid_argument("plan_profile: null plan or output");
+    cudaStream_t st = as_stream(stream);
+    cudaEvent_t ev[4];
+    for (auto& e : ev) TFG_CUDA(cudaEventCreate(&e));
+    plan_execute(*pl, d, st, ev);
+    TFG_CUDA(cudaEventSynchronize(ev[3]));
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      TFG_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      if (stage_ms) stage_ms[k] = ms;
+      if (stage_bytes) stage_bytes[k] = pl->stage_bytes[k];
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
 
 tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d) {
   return guard([&] {

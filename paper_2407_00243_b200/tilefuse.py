@@ -463,6 +463,21 @@ class Plan:
         check(lib().tfg_plan_execute(self._h, C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
+    def profile(self, out=None, stream=None):
+        """One execution with per-stage CUDA events: returns
+        [(stage, ms, algorithmic_bytes)] for first-op / fused / wavefront-1."""
+        torch = _torch()
+        pr = self.problem
+        if out is None:
+            out = torch.empty((pr.n, pr.c_cols), dtype=getattr(torch, pr.dtype.name),
+                              device=pr.device)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        ms = (C.c_double * 3)()
+        by = (C.c_int64 * 3)()
+        check(lib().tfg_plan_profile(self._h, C.c_void_p(out.data_ptr()), _stream_ptr(stream), ms, by))
+        return [(name, ms[k], by[k]) for k, name in enumerate(("first_op", "fused_tiles", "wave1_spmm"))]
+
     def close(self):
         if self._h and self._h.value:
             lib().tfg_plan_destroy(self._h)
