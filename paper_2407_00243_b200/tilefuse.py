@@ -463,6 +463,20 @@ class Plan:
         check(lib().tfg_plan_execute(self._h, C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
+    def execute_from_host(self, host_inputs, device_inputs, out, host_out, stream=None):
+        """End-to-end step with host operands: copy each pinned host tensor
+        into its HBM twin, execute, copy D back to pinned host memory -- all
+        asynchronous on `stream` (the caller synchronises)."""
+        torch = _torch()
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        with torch.cuda.stream(stream):
+            for h, d in zip(host_inputs, device_inputs):
+                d.copy_(h, non_blocking=True)
+            self.execute(out, stream)
+            host_out.copy_(out, non_blocking=True)
+        return host_out
+
     def profile(self, out=None, stream=None):
         """One execution with per-stage CUDA events: returns
         [(stage, ms, algorithmic_bytes)] for first-op / fused / wavefront-1."""
