@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--flush-mib", type=int, default=256)
+    ap.add_argument("--quick", action="store_true",
+                    help="timed loop only (no clock tail / profile / e2e / cpu legs): for ncu")
     return ap.parse_args()
 
 
@@ -241,6 +243,12 @@ def run_ours(args, rank, world, dist):
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    if args.quick:
+        sampler.stop()
+        if rank == 0:
+            print(json.dumps({"quick": True, "config": args.config, "ms_per_step": total_ms / args.steps,
+                              "value": world * w.flops() * args.steps / (total_ms * 1e-3) / 1e9}))
+        return
     # a short same-kernel load tail so the clock sampler sees steady clocks
     t_end = time.perf_counter() + 1.0
     while time.perf_counter() < t_end:
