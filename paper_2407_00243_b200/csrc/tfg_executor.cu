@@ -27,6 +27,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -149,26 +150,104 @@ __device__ __forceinline__ void spmm_row(int kb, int ke,
 }
 
 // ---- SpMM over a row list (short rows) ------------------------------------
-template <class T, int VEC, int LPR, int NCH>
-__global__ void __launch_bounds__(256)
-    k_spmm_rows(int64_t nrows, const int* __restrict__ rows, int row0,
-                const int* __restrict__ rp, const int* __restrict__ ci,
-                const T* __restrict__ av, const T* __restrict__ X, int ldx,
-                T* __restrict__ out, int ldo) {
+// A group of LPR lanes walks a strip of STRIP rows (STRIP <= LPR) in order.
+// The strip's row bounds are loaded once (lane q holds row q), the index
+// chunk of the next row is prefetched while the current row's X rows are
+// gathered, and X gathers are issued UNR at a time (predicated), so each
+// row costs about one dependent memory round trip.  Per-element order stays
+// ascending with separately rounded mul/add (kernels.hpp:75-79).
+template <class T, int VEC, int LPR, int NCH, int UNR, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
+    k_spmm_strip(int64_t nrows, const int* __restrict__ rows, int row0,
+                 const int* __restrict__ rp, const int* __restrict__ ci,
+                 const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                 T* __restrict__ out, int ldo) {
+  constexpr int STRIP = LPR;
   const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
-  if (g >= nrows) return;
+  const int64_t base = g * STRIP;
+  if (base >= nrows) return;
   const int gl = threadIdx.x & (LPR - 1);
   const unsigned gmask = group_mask(LPR);
-  const int r = rows ? __ldg(rows + g) : row0 + (int)g;
-  const int kb = __ldg(rp + r), ke = __ldg(rp + r + 1);
-  auto xl = [&](int c, int ch, T(&x)[VEC]) {
-    ldv<T, VEC>(x, X + (size_t)c * ldx + (ch * LPR + gl) * VEC);
-  };
+  const int cnt = (int)(nrows - base < STRIP ? nrows - base : STRIP);
+  int my_r = 0, my_b = 0, my_e = 0;
+  if (gl < cnt) {
+    my_r = rows ? __ldg(rows + base + gl) : row0 + (int)(base + gl);
+    my_b = __ldg(rp + my_r);
+    my_e = __ldg(rp + my_r + 1);
+  }
+  int q = 0;
+  int e = __shfl_sync(gmask, my_e, 0, LPR);
+  int k0 = __shfl_sync(gmask, my_b, 0, LPR);
+  int c = 0;
+  T a = T(0);
+  if (k0 + gl < e) {
+    c = __ldg(ci + k0 + gl);
+    a = __ldg(av + k0 + gl);
+  }
   T acc[NCH][VEC];
-  spmm_row<T, VEC, LPR, NCH>(kb, ke, ci, av, gl, gmask, xl, acc);
-  T* o = out + (size_t)r * ldo;
 #pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+  while (q < cnt) {
+    const int n_here = min(LPR, e - k0);
+    // next cursor: same row, next chunk -- or the next row's first chunk
+    const bool row_done = k0 + LPR >= e;
+    int nq = q, nk0 = k0 + LPR, ne = e;
+    if (row_done) {
+      nq = q + 1;
+      const int src = nq < cnt ? nq : 0;
+      nk0 = __shfl_sync(gmask, my_b, src, LPR);
+      ne = __shfl_sync(gmask, my_e, src, LPR);
+    }
+    int c2 = 0;
+    T a2 = T(0);
+    if (nq < cnt && nk0 + gl < ne) {
+      c2 = __ldg(ci + nk0 + gl);
+      a2 = __ldg(av + nk0 + gl);
+    }
+    for (int u0 = 0; u0 < n_here; u0 += UNR) {
+      int cu[UNR];
+      T au[UNR];
+      T x[UNR][NCH][VEC];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        cu[u] = __shfl_sync(gmask, c, (u0 + u) & (LPR - 1), LPR);
+        au[u] = __shfl_sync(gmask, a, (u0 + u) & (LPR - 1), LPR);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (u0 + u < n_here) {
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+            ldv<T, VEC>(x[u][ch], X + (size_t)cu[u] * ldx + (ch * LPR + gl) * VEC);
+        }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (u0 + u < n_here) {
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au[u], x[u][ch][v]));
+        }
+    }
+    if (row_done) {
+      const int r = __shfl_sync(gmask, my_r, q, LPR);
+      T* o = out + (size_t)r * ldo;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+      }
+    }
+    q = nq;
+    k0 = nk0;
+    e = ne;
+    c = c2;
+    a = a2;
+  }
 }
 
 // Generic SpMM (any column count): one warp per row, scalar columns.
@@ -553,10 +632,42 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   const int64_t n = w.n_short;
   constexpr int VEC = 16 / sizeof(T);
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  k_spmm_rows<T, VEC, LPR, NCH><<<blocks_for(n * LPR), 256, 0, st>>>(            \
+  k_spmm_strip<T, VEC, LPR, NCH, 8><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
       n, rows, row0, rp, ci, av, X, cc, out, cc);                                \
   TFG_LAUNCH_CHECK();                                                            \
   return;
+  if constexpr (sizeof(T) == 8) {
+    // experiment knob (TFG_SPMM_VARIANT=u*4+m): unroll {4,8,16}, min blocks {1,2,3,4}
+    static const int variant = [] {
+      const char* e = getenv("TFG_SPMM_VARIANT");
+      return e ? atoi(e) : -1;
+    }();
+    if (variant >= 0 && (cc == 64 || cc == 128)) {
+      const int nb = blocks_for((n + 31) / 32 * 32);
+#define TFG_V(U, M)                                                                      \
+  if (cc == 64)                                                                          \
+    k_spmm_strip<T, VEC, 32, 1, U, M><<<nb, 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
+  else                                                                                   \
+    k_spmm_strip<T, VEC, 32, 2, U, M><<<nb, 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
+  TFG_LAUNCH_CHECK();                                                                    \
+  return;
+      switch (variant) {
+        case 0: TFG_V(4, 1)
+        case 1: TFG_V(4, 2)
+        case 2: TFG_V(4, 3)
+        case 3: TFG_V(4, 4)
+        case 4: TFG_V(8, 1)
+        case 5: TFG_V(8, 2)
+        case 6: TFG_V(8, 3)
+        case 7: TFG_V(8, 4)
+        case 8: TFG_V(16, 1)
+        case 9: TFG_V(16, 2)
+        case 10: TFG_V(16, 3)
+        default: break;
+      }
+#undef TFG_V
+    }
+  }
   if (cc % VEC == 0) {
     const int L = cc / VEC;
     switch (L) {
