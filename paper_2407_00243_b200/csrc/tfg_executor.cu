@@ -250,6 +250,93 @@ __global__ void __launch_bounds__(256, MINB)
   }
 }
 
+// ---- row-group union SpMM ----------------------------------------------------
+// A warp owns a group of up to R rows of the row list.  The plan merged the
+// rows' column lists into one ascending list U of distinct columns, each with
+// a mask of the group rows that use it.  The warp walks U in order, gathers
+// every distinct X row ONCE (UNR gathers in flight) and adds it into the
+// accumulators of the rows in its mask, reading each row's values from the
+// unmodified CSR through a per-row running pointer.  Every row therefore
+// still sums its terms in ascending column order with separately rounded mul
+// and add (kernels.hpp:75-79: bit-identical to the reference), while the X
+// bytes pulled through L1 drop by the group's column sharing (about 2.4x for
+// a 9-point stencil at R = 8).
+template <class T, int VEC, int NCH, int R, int UNR, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_spmm_group(int64_t ngroups, const int* __restrict__ g_rows,
+                 const int64_t* __restrict__ g_uoff, const int* __restrict__ ucol,
+                 const uint8_t* __restrict__ umask, const int* __restrict__ rp,
+                 const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                 T* __restrict__ out, int ldo) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= ngroups) return;
+  const int lane = threadIdx.x & 31;
+  int my_row = -1, my_ptr = 0;
+  if (lane < R) {
+    my_row = __ldg(g_rows + g * R + lane);
+    if (my_row >= 0) my_ptr = __ldg(rp + my_row);
+  }
+  int ptr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) ptr[r] = __shfl_sync(0xffffffffu, my_ptr, r);
+  T acc[R][NCH][VEC];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[r][ch][v] = T(0);
+  const int64_t ub = g_uoff[g], ue = g_uoff[g + 1];
+  for (int64_t u0 = ub; u0 < ue; u0 += 32) {
+    int c = 0, m = 0;
+    if (u0 + lane < ue) {
+      c = __ldg(ucol + u0 + lane);
+      m = __ldg(umask + u0 + lane);
+    }
+    const int cnt = (int)min((int64_t)32, ue - u0);
+    for (int q0 = 0; q0 < cnt; q0 += UNR) {
+      int cu[UNR], mu[UNR];
+      T x[UNR][NCH][VEC];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        cu[q] = __shfl_sync(0xffffffffu, c, (q0 + q) & 31);
+        mu[q] = q0 + q < cnt ? __shfl_sync(0xffffffffu, m, (q0 + q) & 31) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q)
+        if (mu[q]) {
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+            ldv<T, VEC>(x[q][ch], X + (size_t)cu[q] * ldx + (ch * 32 + lane) * VEC);
+        }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (mu[q] & (1 << r)) {
+            const T a = __ldg(av + ptr[r]);
+            ++ptr[r];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+              for (int v = 0; v < VEC; ++v)
+                acc[r][ch][v] = fops<T>::add(acc[r][ch][v], fops<T>::mul(a, x[q][ch][v]));
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = __shfl_sync(0xffffffffu, my_row, r);
+    if (row >= 0) {
+      T* o = out + (size_t)row * ldo;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * 32 + lane) * VEC, acc[r][ch]);
+    }
+  }
+}
+
 // Generic SpMM (any column count): one warp per row, scalar columns.
 template <class T>
 __global__ void __launch_bounds__(256)
@@ -389,6 +476,147 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   }
 }
 
+// ---- dense first op v2: cp.async 3-stage pipeline -------------------------
+// CTA tile BM rows x BN columns of D1 = B C, K streamed in BK chunks (both
+// the B row block and the C chunk) through a 3-stage cp.async ring; each
+// thread owns a TM x TN register tile.  Per element the k loop ascends with
+// fused multiply-add from 0 -- the same sequence k_gemm_blocks and the fused
+// kernel use, so every path produces identical bits.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
+struct GemmCfg {
+  static constexpr int V = 16 / (int)sizeof(T);  // elements per 16 B
+  static constexpr int PAD = V;                  // keeps 16 B alignment, shifts banks
+  static constexpr int THREADS = (BM / TM) * (BN / TN);
+  static constexpr int B_LD = BK + PAD;
+  static constexpr int C_LD = BN + PAD;
+  static constexpr size_t SMEM =
+      (size_t)STAGES * ((size_t)BM * B_LD + (size_t)BK * C_LD) * sizeof(T);
+  static_assert(THREADS == 256, "256 threads per CTA");
+  static_assert(BK % V == 0 && TN % V == 0, "vector widths");
+};
+
+// acc[TM][TN] += B[r0 .. r0+cnt) x C[:, n0 .. n0+BN) ; rows >= cnt read zeros.
+template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
+__device__ __forceinline__ void gemm_block(const T* __restrict__ B, int bc,
+                                           const T* __restrict__ C, int cc, int n0,
+                                           int r0, int cnt, T* smem, T (&acc)[TM][TN]) {
+  using G = GemmCfg<T, BM, BN, BK, TM, TN, STAGES>;
+  constexpr int V = G::V;
+  T* sb = smem;                                        // [STAGES][BM][B_LD]
+  T* sc = smem + (size_t)STAGES * BM * G::B_LD;        // [STAGES][BK][C_LD]
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int nk = (bc + BK - 1) / BK;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+  auto load_stage = [&](int stg, int kc) {
+    const int k0 = kc * BK;
+    T* bdst = sb + (size_t)stg * BM * G::B_LD;
+    for (int e = tid; e < BM * (BK / V); e += G::THREADS) {
+      const int m = e / (BK / V), kv = (e % (BK / V)) * V;
+      const bool ok = m < cnt && k0 + kv < bc;
+      const T* src = ok ? B + (size_t)(r0 + m) * bc + k0 + kv : B;
+      cp_async16(bdst + m * G::B_LD + kv, src, ok ? 16 : 0);
+    }
+    T* cdst = sc + (size_t)stg * BK * G::C_LD;
+    for (int e = tid; e < BK * (BN / V); e += G::THREADS) {
+      const int kk = e / (BN / V), nv = (e % (BN / V)) * V;
+      const bool ok = k0 + kk < bc;
+      const T* src = ok ? C + (size_t)(k0 + kk) * cc + n0 + nv : C;
+      cp_async16(cdst + kk * G::C_LD + nv, src, ok ? 16 : 0);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kc + STAGES - 1;
+      if (nxt < nk) load_stage(nxt % STAGES, nxt);
+      cp_async_commit();
+    }
+    const int stg = kc % STAGES;
+    const T* bs = sb + (size_t)stg * BM * G::B_LD;
+    const T* cs = sc + (size_t)stg * BK * G::C_LD;
+    const int kn = min(BK, bc - kc * BK);
+    for (int k0 = 0; k0 < kn; k0 += V) {
+      T a[TM][V];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) ldv<T, V>(a[i], bs + (ty * TM + i) * G::B_LD + k0);
+      const int kv = min(V, kn - k0);
+#pragma unroll
+      for (int kk = 0; kk < V; ++kk) {
+        if (kk < kv) {
+          T b[TN];
+#pragma unroll
+          for (int j = 0; j < TN; j += V) {
+            T tmp[V];
+            ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + tx * TN + j);
+#pragma unroll
+            for (int q = 0; q < V; ++q) b[j + q] = tmp[q];
+          }
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fops<T>::fma(a[i][kk], b[j], acc[i][j]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
+__global__ void __launch_bounds__(256)
+    k_gemm_v2(int64_t nblk, const int* __restrict__ blk_r0, const int* __restrict__ blk_cnt,
+              const T* __restrict__ B, int bc, const T* __restrict__ C, int cc,
+              T* __restrict__ D1, int ldd) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  const int n0 = blockIdx.y * BN;
+  const int tx = threadIdx.x % (BN / TN), ty = threadIdx.x / (BN / TN);
+  constexpr int V = 16 / (int)sizeof(T);
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int r0 = blk_r0[blk], cnt = blk_cnt[blk];
+    T acc[TM][TN];
+    gemm_block<T, BM, BN, BK, TM, TN, STAGES>(B, bc, C, cc, n0, r0, cnt, smem, acc);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int m = ty * TM + i;
+      if (m < cnt) {
+        T* o = D1 + (size_t)(r0 + m) * ldd + n0 + tx * TN;
+#pragma unroll
+        for (int j = 0; j < TN; j += V) {
+          T tmp[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
+          stv<T, V>(o + j, tmp);
+        }
+      }
+    }
+  }
+}
+
 // ---- fused wavefront-0 kernel ----------------------------------------------
 // blockIdx.x = fused tile, blockIdx.y = column slice [c0, c0+cs).
 // smem: [stage: w_cap x cs][C slice: bc x cs (dense B only)]
@@ -495,6 +723,105 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- fused wavefront-0 kernel v2 (dense B) ----------------------------------
+// Persistent CTAs over fused tiles; blockIdx.y = column slice of width BN.
+// Phase 1 runs the pipelined GEMM over the tile's i-range in BM-row blocks;
+// the epilogue writes D1 rows that wavefront 1 reads (spill) to HBM and the
+// rows the tile's own fused rows read (slot >= 0) to a shared-memory stage.
+// Phase 2 computes the tile's fused D rows from the stage (LPR lanes per row,
+// reference order).  Tiles whose staged set exceeds the stage capacity were
+// marked "wide" at plan time: all their rows spill and phase 2 reads HBM/L2.
+template <class T, int BM, int BN, int BK, int TM, int TN, int LPR>
+__global__ void __launch_bounds__(256)
+    k_fused_gemm_tiles(int64_t ntiles, const int* __restrict__ t_ilo,
+                       const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
+                       const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
+                       const int* __restrict__ slot, const T* __restrict__ B, int bc,
+                       const T* __restrict__ C, int cc, const int* __restrict__ arp,
+                       const int* __restrict__ aci, const T* __restrict__ av,
+                       const uint8_t* __restrict__ spill, T* D1, T* __restrict__ D) {
+  using G = GemmCfg<T, BM, BN, BK, TM, TN, 3>;
+  constexpr int V = G::V;
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int NCH = BN / (LPR * VEC);
+  static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* gsm = reinterpret_cast<T*>(smem_raw);
+  T* stage = gsm + G::SMEM / sizeof(T);
+  const int n0 = blockIdx.y * BN;
+  const int tx = threadIdx.x % (BN / TN), ty = threadIdx.x / (BN / TN);
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int group = threadIdx.x / LPR, ngroups = blockDim.x / LPR;
+  for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+    const int ilo = t_ilo[v], ihi = t_ihi[v];
+    const bool wide = t_wide[v] != 0;
+    for (int r0 = ilo; r0 < ihi; r0 += BM) {
+      const int cnt = min(BM, ihi - r0);
+      T acc[TM][TN];
+      gemm_block<T, BM, BN, BK, TM, TN, 3>(B, bc, C, cc, n0, r0, cnt, gsm, acc);
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int m = ty * TM + i;
+        if (m >= cnt) continue;
+        const int row = r0 + m;
+        const int sl = wide ? -1 : __ldg(slot + row);
+        const bool sp = wide || spill[row];
+#pragma unroll
+        for (int j = 0; j < TN; j += V) {
+          T tmp[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
+          if (sp) stv<T, V>(D1 + (size_t)row * cc + n0 + tx * TN + j, tmp);
+          if (sl >= 0) stv<T, V>(stage + (size_t)sl * BN + tx * TN + j, tmp);
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t jb = t_joff[v], je = t_joff[v + 1];
+    for (int64_t q = jb + group; q < je; q += ngroups) {
+      const int j = jrows[q];
+      const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
+      T acc[NCH][VEC];
+      if (wide) {
+        auto xl = [&](int c, int ch, T(&x)[VEC]) {
+          ldv<T, VEC>(x, D1 + (size_t)c * cc + n0 + (ch * LPR + gl) * VEC);
+        };
+        spmm_row<T, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc);
+      } else {
+        auto xl = [&](int c, int ch, T(&x)[VEC]) {
+          ldv<T, VEC>(x, stage + (size_t)__ldg(slot + c) * BN + (ch * LPR + gl) * VEC);
+        };
+        spmm_row<T, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc);
+      }
+      T* o = D + (size_t)j * cc + n0;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+    }
+    __syncthreads();
+  }
+}
+
+// slot[i] = position of D1 row i in its tile's stage (-1: not read by the
+// tile's fused rows).  One warp per fused tile, rows ascending.
+__global__ void k_assign_slots(int64_t ntiles, const int* __restrict__ t_ilo,
+                               const int* __restrict__ t_ihi, const uint8_t* __restrict__ mark,
+                               int* slot, int* t_count) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= ntiles) return;
+  const int lane = threadIdx.x & 31;
+  const int ilo = t_ilo[w], ihi = t_ihi[w];
+  int base = 0;
+  for (int i0 = ilo; i0 < ihi; i0 += 32) {
+    const int i = i0 + lane;
+    const bool m = i < ihi && mark[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    if (i < ihi) slot[i] = m ? base + __popc(bal & ((1u << lane) - 1u)) : -1;
+    base += __popc(bal);
+  }
+  if (lane == 0) t_count[w] = base;
+}
+
 // spill[c] = 1 for every column c of every wavefront-1 row
 __global__ void k_mark_spill(int64_t nrows, const int* __restrict__ rows,
                              const int* __restrict__ rp,
@@ -563,6 +890,13 @@ inline int blocks_for(int64_t threads, int per_block = 256) {
 // ===========================================================================
 struct SpmmWork {
   int64_t n_short = 0, n_long = 0, n_seg = 0;
+  // row-group union layout of the short rows (used when it cuts X gathers)
+  static constexpr int kGroupR = 8;
+  bool grouped = false;
+  int64_t n_groups = 0, n_ucols = 0;
+  dbuf<int> g_rows, ucol;
+  dbuf<int64_t> g_uoff;
+  dbuf<uint8_t> umask;
   bool identity = false;  // short rows are exactly [row0, row0 + n_short)
   int row0 = 0;
   dbuf<int> short_rows, long_rows, seg_k0, seg_k1;
@@ -570,8 +904,53 @@ struct SpmmWork {
   dbuf<unsigned char> partial;
 
   // rows: host row list (ascending not required); rp: host row_ptr
+  // Merge the column lists of each group of kGroupR consecutive short rows.
+  // Uses the group layout only when it removes >= 25% of the X gathers.
+  void build_groups(const std::vector<int>& sh, const std::vector<int>& rp,
+                    const std::vector<int>& ci, cudaStream_t st) {
+    const int R = kGroupR;
+    const int64_t ng = ((int64_t)sh.size() + R - 1) / R;
+    std::vector<int> grows((size_t)ng * R, -1), uc;
+    std::vector<uint8_t> um;
+    std::vector<int64_t> uoff{0};
+    int64_t nnz = 0;
+    std::vector<std::pair<int, int>> tmp;
+    for (int64_t g = 0; g < ng; ++g) {
+      tmp.clear();
+      for (int r = 0; r < R && g * R + r < (int64_t)sh.size(); ++r) {
+        const int row = sh[g * R + r];
+        grows[g * R + r] = row;
+        for (int k = rp[row]; k < rp[row + 1]; ++k) tmp.emplace_back(ci[k], r);
+        nnz += rp[row + 1] - rp[row];
+      }
+      std::sort(tmp.begin(), tmp.end());
+      for (size_t q = 0; q < tmp.size();) {
+        size_t e = q;
+        int mask = 0;
+        while (e < tmp.size() && tmp[e].first == tmp[q].first) mask |= 1 << tmp[e++].second;
+        uc.push_back(tmp[q].first);
+        um.push_back((uint8_t)mask);
+        q = e;
+      }
+      uoff.push_back((int64_t)uc.size());
+    }
+    if (nnz == 0 || (double)uc.size() > 0.75 * (double)nnz) return;
+    grouped = true;
+    n_groups = ng;
+    n_ucols = (int64_t)uc.size();
+    g_rows.alloc(grows.size());
+    h2d(g_rows.p, grows.data(), grows.size(), st);
+    g_uoff.alloc(uoff.size());
+    h2d(g_uoff.p, uoff.data(), uoff.size(), st);
+    ucol.alloc(uc.size() + 1);
+    h2d(ucol.p, uc.data(), uc.size(), st);
+    umask.alloc(um.size() + 1);
+    h2d(umask.p, um.data(), um.size(), st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+  }
+
   void build(const std::vector<int>& rows, const std::vector<int>& rp, int cc,
-             size_t elem, cudaStream_t st) {
+             size_t elem, cudaStream_t st, const std::vector<int>* ci = nullptr) {
     std::vector<int> sh, lg, k0, k1;
     std::vector<int64_t> off{0};
     sh.reserve(rows.size());
@@ -614,10 +993,13 @@ struct SpmmWork {
     h2d(long_seg_off.p, off.data(), off.size(), st);
     partial.alloc((size_t)n_seg * cc * elem);
     TFG_CUDA(cudaStreamSynchronize(st));
+    const int vec = 16 / (int)elem;
+    if (ci && (cc == 32 * vec || cc == 64 * vec) && !sh.empty()) build_groups(sh, rp, *ci, st);
   }
   size_t bytes() const {
-    return short_rows.bytes() + long_rows.bytes() + seg_k0.bytes() +
-           seg_k1.bytes() + long_seg_off.bytes() + partial.bytes();
+    return short_rows.bytes() + long_rows.bytes() + seg_k0.bytes() + seg_k1.bytes() +
+           long_seg_off.bytes() + partial.bytes() + g_rows.bytes() + ucol.bytes() +
+           g_uoff.bytes() + umask.bytes();
   }
   int launches() const { return (n_short > 0) + 2 * (n_long > 0); }
 };
@@ -627,6 +1009,18 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
                                 const T* av, const T* X, int cc, T* out,
                                 cudaStream_t st) {
   if (w.n_short == 0) return;
+  if (w.grouped) {
+    constexpr int VEC = 16 / sizeof(T);
+    const int nb = blocks_for(w.n_groups * 32);
+    if (cc == 32 * VEC)
+      k_spmm_group<T, VEC, 1, SpmmWork::kGroupR, 4, 2><<<nb, 256, 0, st>>>(
+          w.n_groups, w.g_rows.p, w.g_uoff.p, w.ucol.p, w.umask.p, rp, av, X, cc, out, cc);
+    else
+      k_spmm_group<T, VEC, 2, SpmmWork::kGroupR, 4, 1><<<nb, 256, 0, st>>>(
+          w.n_groups, w.g_rows.p, w.g_uoff.p, w.ucol.p, w.umask.p, rp, av, X, cc, out, cc);
+    TFG_LAUNCH_CHECK();
+    return;
+  }
   const int* rows = w.identity ? nullptr : w.short_rows.p;
   const int row0 = w.identity ? w.row0 : 0;
   const int64_t n = w.n_short;
@@ -712,6 +1106,8 @@ struct tfg_plan {
   bool zero_d = false;  // schedule does not cover every j row
   // (a) first op for j-less wavefront-0 tiles / all rows when unfused
   int64_t n_fo_blocks = 0;
+  int gemm_kind = 0;             // 0 generic k_gemm_blocks, else k_gemm_v2 config id
+  int gemm_bm = 64;
   tfg::dbuf<int> fo_r0, fo_cnt;  // dense B: GEMM row blocks
   tfg::SpmmWork fo_sparse;       // sparse B: SpMM rows with X = C
   // (b) fused tiles
@@ -720,6 +1116,12 @@ struct tfg_plan {
   tfg::dbuf<int64_t> ft_joff;
   int w_cap = 0, cs = 0, n_slices = 0;
   size_t fused_smem = 0;
+  int64_t ft_nrows = 0;      // fused (non-empty) j rows in the fused tiles
+  bool fused_v2 = false;     // dense-B pipelined GEMM tiles with slot staging
+  tfg::dbuf<int> slot;       // D1 row -> stage slot within its tile (-1 none)
+  tfg::dbuf<uint8_t> ft_wide;
+  int stage_cap = 0;
+  int64_t n_wide = 0;
   // (c) wavefront 1 / unfused second op
   tfg::SpmmWork second;
   tfg::dbuf<uint8_t> spill;
@@ -738,6 +1140,18 @@ namespace tfg {
 
 static constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16, kGemmTM = 4, kGemmTN = 4;
 static constexpr size_t kFusedSmemCap = 200 * 1024;
+// the row-group layout is analysed on the host at plan time up to this nnz
+static constexpr int64_t kGroupMaxNnz = 96ll << 20;
+static constexpr size_t kFusedSmemMax = 227 * 1024;  // sm_100 opt-in max per CTA
+
+// shared memory of the pipelined GEMM configuration a plan uses
+static size_t fused_gemm_smem(const tfg_plan& pl) {
+  if (pl.elem == 4)
+    return pl.gemm_kind == 2 ? GemmCfg<float, 64, 128, 32, 4, 8, 3>::SMEM
+                             : GemmCfg<float, 128, 64, 32, 8, 4, 3>::SMEM;
+  return pl.gemm_kind == 2 ? GemmCfg<double, 64, 128, 16, 4, 8, 3>::SMEM
+                           : GemmCfg<double, 64, 64, 16, 4, 4, 3>::SMEM;
+}
 
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                  tfg_plan& pl) {
@@ -771,6 +1185,20 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
 
   std::vector<int> fo_rows;  // first-op rows handled by stage (a)
   std::vector<int> second_rows;
+  std::vector<int> zero_rows;  // empty fused rows, written by the SpMM stage
+  if (pr.b_is_dense) {
+    // fast path: cp.async pipelined GEMM when the shapes and pointers allow
+    const int V = 16 / (int)pl.elem;
+    const bool aligned = ((uintptr_t)pr.d_b_dense % 16 == 0) && ((uintptr_t)pr.d_c % 16 == 0) &&
+                         (bc % V == 0);
+    pl.gemm_kind = 0;
+    pl.gemm_bm = kGemmBM;
+    if (aligned && cc % 128 == 0)
+      pl.gemm_kind = 2;  // BN = 128
+    else if (aligned && cc % 64 == 0)
+      pl.gemm_kind = 1;  // BN = 64
+    if (pl.gemm_kind) pl.gemm_bm = (pl.elem == 4 && pl.gemm_kind == 1) ? 128 : 64;
+  }
   if (!s) {
     fo_rows.resize(n);
     for (int i = 0; i < n; ++i) fo_rows[i] = i;
@@ -789,20 +1217,29 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     second_rows.resize(nj1);
     d2h(second_rows.data(), s->j_rows[1].p, nj1, st);
     TFG_CUDA(cudaStreamSynchronize(st));
-    std::vector<int> f_ilo, f_ihi;
+    std::vector<int> jr0(s->n_jrows[0]);
+    d2h(jr0.data(), s->j_rows[0].p, jr0.size(), st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> f_ilo, f_ihi, f_rows;
     std::vector<int64_t> f_joff{0};
-    std::vector<int64_t> f_src;  // source offset of each fused tile's j list
     int w_max = 0;
     for (int64_t v = 0; v < nt0; ++v) {
-      const int64_t nj = joff[v + 1] - joff[v];
       pl.first_rows += ihi[v] - ilo[v];
-      if (nj == 0) {
+      // empty fused rows need no D1 (D row = 0): the SpMM stage writes them
+      const size_t before = f_rows.size();
+      for (int64_t q = joff[v]; q < joff[v + 1]; ++q) {
+        const int j = jr0[q];
+        if (arp[j + 1] > arp[j])
+          f_rows.push_back(j);
+        else
+          zero_rows.push_back(j);
+      }
+      if (f_rows.size() == before) {
         for (int i = ilo[v]; i < ihi[v]; ++i) fo_rows.push_back(i);
       } else {
         f_ilo.push_back(ilo[v]);
         f_ihi.push_back(ihi[v]);
-        f_src.push_back(joff[v]);
-        f_joff.push_back(f_joff.back() + nj);
+        f_joff.push_back((int64_t)f_rows.size());
         w_max = std::max(w_max, ihi[v] - ilo[v]);
       }
     }
@@ -817,27 +1254,60 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       h2d(pl.ft_ilo.p, f_ilo.data(), f_ilo.size(), st);
       h2d(pl.ft_ihi.p, f_ihi.data(), f_ihi.size(), st);
       h2d(pl.ft_joff.p, f_joff.data(), f_joff.size(), st);
-      // gather the fused tiles' j lists contiguously
-      pl.ft_jrows.alloc(f_joff.back());
-      for (size_t k = 0; k < f_src.size(); ++k)
-        TFG_CUDA(cudaMemcpyAsync(pl.ft_jrows.p + f_joff[k], s->j_rows[0].p + f_src[k],
-                                 (f_joff[k + 1] - f_joff[k]) * sizeof(int),
-                                 cudaMemcpyDeviceToDevice, st));
-      // column slice: whole cc when the widest tile fits, else halve
-      int cs = std::min(cc, 128);
-      auto need = [&](int w, int c) {
-        return (size_t)w * c * pl.elem + (pr.b_is_dense ? (size_t)bc * c * pl.elem : 0);
-      };
-      while (cs > 32 && need(w_max, cs) > kFusedSmemCap) cs = (cs + 1) / 2;
-      const size_t c_bytes = pr.b_is_dense ? (size_t)bc * cs * pl.elem : 0;
-      if (c_bytes + (size_t)cs * pl.elem > kFusedSmemCap)
-        throw runtime_error("fused executor: C slice does not fit in shared memory");
-      int w_cap = (int)std::min<size_t>((size_t)w_max,
-                                        (kFusedSmemCap - c_bytes) / ((size_t)cs * pl.elem));
-      pl.cs = cs;
-      pl.w_cap = std::max(w_cap, 0);
-      pl.n_slices = (cc + cs - 1) / cs;
-      pl.fused_smem = (size_t)pl.w_cap * cs * pl.elem + c_bytes;
+      pl.ft_jrows.alloc(f_rows.size());
+      h2d(pl.ft_jrows.p, f_rows.data(), f_rows.size(), st);
+      pl.ft_nrows = (int64_t)f_rows.size();
+      if (pr.b_is_dense && pl.gemm_kind) {
+        // v2: stage only the D1 rows the tile's fused rows read
+        const int BN = pl.gemm_kind == 2 ? 128 : 64;
+        pl.fused_v2 = true;
+        pl.cs = BN;
+        pl.n_slices = cc / BN;
+        dbuf<uint8_t> mark(n);
+        TFG_CUDA(cudaMemsetAsync(mark.p, 0, n, st));
+        k_mark_cols<<<blocks_for((int64_t)f_rows.size() * 32), 256, 0, st>>>(
+            (int64_t)f_rows.size(), pl.ft_jrows.p, pr.d_a_row_ptr, pr.d_a_col_idx, mark.p);
+        TFG_LAUNCH_CHECK();
+        pl.slot.alloc(n);
+        TFG_CUDA(cudaMemsetAsync(pl.slot.p, 0xff, (size_t)n * 4, st));
+        dbuf<int> tcount(pl.n_ftiles);
+        k_assign_slots<<<blocks_for(pl.n_ftiles * 32), 256, 0, st>>>(
+            pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, mark.p, pl.slot.p, tcount.p);
+        TFG_LAUNCH_CHECK();
+        std::vector<int> tc(pl.n_ftiles);
+        d2h(tc.data(), tcount.p, tc.size(), st);
+        TFG_CUDA(cudaStreamSynchronize(st));
+        const size_t gsm = fused_gemm_smem(pl);
+        const size_t cap_bytes = kFusedSmemMax > gsm ? kFusedSmemMax - gsm : 0;
+        int max_need = 0;
+        for (int c : tc) max_need = std::max(max_need, c);
+        const int cap = (int)std::min<size_t>(cap_bytes / ((size_t)BN * pl.elem), (size_t)max_need);
+        std::vector<uint8_t> wide(pl.n_ftiles);
+        for (int64_t v = 0; v < pl.n_ftiles; ++v) {
+          wide[v] = tc[v] > cap;
+          pl.n_wide += wide[v];
+        }
+        pl.ft_wide.alloc(pl.n_ftiles);
+        h2d(pl.ft_wide.p, wide.data(), wide.size(), st);
+        pl.stage_cap = cap;
+        pl.fused_smem = gsm + (size_t)cap * BN * pl.elem;
+      } else {
+        // generic fused kernel: column slice = whole cc when the widest tile fits
+        int cs = std::min(cc, 128);
+        auto need = [&](int w, int c) {
+          return (size_t)w * c * pl.elem + (pr.b_is_dense ? (size_t)bc * c * pl.elem : 0);
+        };
+        while (cs > 32 && need(w_max, cs) > kFusedSmemCap) cs = (cs + 1) / 2;
+        const size_t c_bytes = pr.b_is_dense ? (size_t)bc * cs * pl.elem : 0;
+        if (c_bytes + (size_t)cs * pl.elem > kFusedSmemCap)
+          throw runtime_error("fused executor: C slice does not fit in shared memory");
+        int w_cap = (int)std::min<size_t>((size_t)w_max,
+                                          (kFusedSmemCap - c_bytes) / ((size_t)cs * pl.elem));
+        pl.cs = cs;
+        pl.w_cap = std::max(w_cap, 0);
+        pl.n_slices = (cc + cs - 1) / cs;
+        pl.fused_smem = (size_t)pl.w_cap * cs * pl.elem + c_bytes;
+      }
     }
     // spill set S = columns of wavefront-1 rows
     TFG_CUDA(cudaMemsetAsync(pl.spill.p, 0, n, st));
@@ -859,12 +1329,13 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
 
   // (a) first-op work
   if (pr.b_is_dense) {
+    const int BMb = pl.gemm_bm;
     std::vector<int> r0, cnt;
     size_t q = 0;
     while (q < fo_rows.size()) {
       size_t e = q + 1;
       while (e < fo_rows.size() && fo_rows[e] == fo_rows[e - 1] + 1 &&
-             (int)(e - q) < kGemmBM)
+             (int)(e - q) < BMb)
         ++e;
       r0.push_back(fo_rows[q]);
       cnt.push_back((int)(e - q));
@@ -876,10 +1347,28 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     h2d(pl.fo_r0.p, r0.data(), r0.size(), st);
     h2d(pl.fo_cnt.p, cnt.data(), cnt.size(), st);
   } else {
-    pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st);
+    std::vector<int> bci;
+    if (pr.b_nnz > 0 && pr.b_nnz <= kGroupMaxNnz) {
+      bci.resize(pr.b_nnz);
+      d2h(bci.data(), pr.d_b_col_idx, bci.size(), st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+    }
+    pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st, bci.empty() ? nullptr : &bci);
   }
-  // (c) second-op work
-  pl.second.build(second_rows, arp, cc, pl.elem, st);
+  // (c) second-op work (wavefront-1 rows, then the empty fused rows)
+  if (!zero_rows.empty()) {
+    second_rows.insert(second_rows.end(), zero_rows.begin(), zero_rows.end());
+    std::sort(second_rows.begin(), second_rows.end());
+  }
+  {
+    std::vector<int> aci;
+    if (arp[n] > 0 && arp[n] <= kGroupMaxNnz) {
+      aci.resize(arp[n]);
+      d2h(aci.data(), pr.d_a_col_idx, aci.size(), st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+    }
+    pl.second.build(second_rows, arp, cc, pl.elem, st, aci.empty() ? nullptr : &aci);
+  }
 
   // ---- algorithmic bytes per stage ------------------------------------
   {
@@ -923,8 +1412,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       std::vector<int> ilo(pl.n_ftiles), ihi(pl.n_ftiles);
       d2h(ilo.data(), pl.ft_ilo.p, pl.n_ftiles, st);
       d2h(ihi.data(), pl.ft_ihi.p, pl.n_ftiles, st);
-      tj.resize(pl.fused_rows);
-      d2h(tj.data(), pl.ft_jrows.p, pl.fused_rows, st);
+      tj.resize(pl.ft_nrows);
+      d2h(tj.data(), pl.ft_jrows.p, pl.ft_nrows, st);
       std::vector<uint8_t> sp(n);
       d2h(sp.data(), pl.spill.p, n, st);
       TFG_CUDA(cudaStreamSynchronize(st));
@@ -959,6 +1448,72 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   TFG_CUDA(cudaStreamSynchronize(st));
 }
 
+template <class T, int BM, int BN, int BK, int TM, int TN>
+static void launch_gemm_v2_cfg(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
+                               cudaStream_t st) {
+  using G = GemmCfg<T, BM, BN, BK, TM, TN, 3>;
+  auto kern = k_gemm_v2<T, BM, BN, BK, TM, TN, 3>;
+  static bool attr = false;
+  if (!attr) {
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    attr = true;
+  }
+  int per_sm = 1;
+  TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, G::SMEM));
+  const int64_t gx = std::min<int64_t>(pl.n_fo_blocks, (int64_t)sm_count() * std::max(per_sm, 1));
+  kern<<<dim3((unsigned)gx, cc / BN), 256, G::SMEM, st>>>(pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p,
+                                                          B, bc, C, cc, D1, cc);
+  TFG_LAUNCH_CHECK();
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, int LPR>
+static void launch_fused_v2_cfg(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
+  const tfg_problem& pr = pl.p;
+  auto kern = k_fused_gemm_tiles<T, BM, BN, BK, TM, TN, LPR>;
+  TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pl.fused_smem));
+  int per_sm = 1;
+  TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, pl.fused_smem));
+  const int64_t gx = std::min<int64_t>(pl.n_ftiles, (int64_t)sm_count() * std::max(per_sm, 1));
+  kern<<<dim3((unsigned)gx, pl.n_slices), 256, pl.fused_smem, st>>>(
+      pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, pl.ft_joff.p, pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p,
+      static_cast<const T*>(pr.d_b_dense), pr.b_cols, static_cast<const T*>(pr.d_c),
+      pr.c_cols, pr.d_a_row_ptr, pr.d_a_col_idx, static_cast<const T*>(pr.d_a_val), pl.spill.p, D1,
+      D);
+  TFG_LAUNCH_CHECK();
+}
+
+template <class T>
+static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (pl.gemm_kind == 2)
+      launch_fused_v2_cfg<T, 64, 128, 32, 4, 8, 32>(pl, D1, D, st);
+    else
+      launch_fused_v2_cfg<T, 128, 64, 32, 8, 4, 16>(pl, D1, D, st);
+  } else {
+    if (pl.gemm_kind == 2)
+      launch_fused_v2_cfg<T, 64, 128, 16, 4, 8, 32>(pl, D1, D, st);
+    else
+      launch_fused_v2_cfg<T, 64, 64, 16, 4, 4, 32>(pl, D1, D, st);
+  }
+}
+
+template <class T>
+static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
+                           cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (pl.gemm_kind == 2)
+      launch_gemm_v2_cfg<T, 64, 128, 32, 4, 8>(pl, B, bc, C, cc, D1, st);
+    else
+      launch_gemm_v2_cfg<T, 128, 64, 32, 8, 4>(pl, B, bc, C, cc, D1, st);
+  } else {
+    if (pl.gemm_kind == 2)
+      launch_gemm_v2_cfg<T, 64, 128, 16, 4, 8>(pl, B, bc, C, cc, D1, st);
+    else
+      launch_gemm_v2_cfg<T, 64, 64, 16, 4, 4>(pl, B, bc, C, cc, D1, st);
+  }
+}
+
 template <class T>
 static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev = nullptr) {
   const tfg_problem& pr = pl.p;
@@ -969,7 +1524,9 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
   // (a)
   if (pr.b_is_dense) {
-    if (pl.n_fo_blocks) {
+    if (pl.n_fo_blocks && pl.gemm_kind) {
+      launch_gemm_v2<T>(pl, static_cast<const T*>(pr.d_b_dense), bc, C, cc, D1, st);
+    } else if (pl.n_fo_blocks) {
       const int gy = (cc + kGemmBN - 1) / kGemmBN;
       const int64_t gx = std::min<int64_t>(pl.n_fo_blocks, (int64_t)sm_count() * 16);
       k_gemm_blocks<T, kGemmBM, kGemmBN, kGemmBK, kGemmTM, kGemmTN>
@@ -984,7 +1541,9 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   }
   if (ev) TFG_CUDA(cudaEventRecord(ev[1], st));
   // (b)
-  if (pl.n_ftiles) {
+  if (pl.n_ftiles && pl.fused_v2) {
+    launch_fused_v2<T>(pl, D1, D, st);
+  } else if (pl.n_ftiles) {
     if (pl.fused_smem > 48 * 1024)
       TFG_CUDA(cudaFuncSetAttribute(k_fused_tiles<T>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
