@@ -264,21 +264,14 @@ __global__ void __launch_bounds__(256, MINB)
 template <class T, int VEC, int NCH, int R, int UNR, int MINB>
 __global__ void __launch_bounds__(256, MINB)
     k_spmm_group(int64_t ngroups, const int* __restrict__ g_rows,
-                 const int64_t* __restrict__ g_uoff, const int* __restrict__ ucol,
-                 const uint8_t* __restrict__ umask, const int* __restrict__ rp,
-                 const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                 const int64_t* __restrict__ g_uoff, const int64_t* __restrict__ g_poff,
+                 const int* __restrict__ ucol, const uint8_t* __restrict__ umask,
+                 const T* __restrict__ gval, const T* __restrict__ X, int ldx,
                  T* __restrict__ out, int ldo) {
   const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (g >= ngroups) return;
   const int lane = threadIdx.x & 31;
-  int my_row = -1, my_ptr = 0;
-  if (lane < R) {
-    my_row = __ldg(g_rows + g * R + lane);
-    if (my_row >= 0) my_ptr = __ldg(rp + my_row);
-  }
-  int ptr[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) ptr[r] = __shfl_sync(0xffffffffu, my_ptr, r);
+  const int my_row = lane < R ? __ldg(g_rows + g * R + lane) : -1;
   T acc[R][NCH][VEC];
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -287,6 +280,12 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[r][ch][v] = T(0);
   const int64_t ub = g_uoff[g], ue = g_uoff[g + 1];
+  // value stream: pairs (u, row) in order; lane l holds pair pc0 + l
+  const int64_t pe = g_poff[g + 1];
+  int64_t pc0 = g_poff[g];
+  int pi = 0;  // index of the next pair within the current 32-value chunk
+  T vcur = pc0 + lane < pe ? __ldg(gval + pc0 + lane) : T(0);
+  T vnext = pc0 + 32 + lane < pe ? __ldg(gval + pc0 + 32 + lane) : T(0);
   for (int64_t u0 = ub; u0 < ue; u0 += 32) {
     int c = 0, m = 0;
     if (u0 + lane < ue) {
@@ -314,8 +313,13 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (mu[q] & (1 << r)) {
-            const T a = __ldg(av + ptr[r]);
-            ++ptr[r];
+            const T a = __shfl_sync(0xffffffffu, vcur, pi);
+            if (++pi == 32) {
+              pi = 0;
+              pc0 += 32;
+              vcur = vnext;
+              vnext = pc0 + 32 + lane < pe ? __ldg(gval + pc0 + 32 + lane) : T(0);
+            }
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
@@ -335,6 +339,16 @@ __global__ void __launch_bounds__(256, MINB)
       for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * 32 + lane) * VEC, acc[r][ch]);
     }
   }
+}
+
+// gval[p] = av[gperm[p]]: refresh the group-ordered value stream from the
+// live CSR values (first kernel of every execution that uses groups).
+template <class T>
+__global__ void k_permute_values(int64_t np, const int* __restrict__ perm,
+                                 const T* __restrict__ av, T* __restrict__ gval) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x)
+    gval[p] = __ldg(av + __ldg(perm + p));
 }
 
 // Generic SpMM (any column count): one warp per row, scalar columns.
@@ -892,11 +906,14 @@ struct SpmmWork {
   int64_t n_short = 0, n_long = 0, n_seg = 0;
   // row-group union layout of the short rows (used when it cuts X gathers)
   static constexpr int kGroupR = 8;
+  size_t elem_ = 8;
   bool grouped = false;
   int64_t n_groups = 0, n_ucols = 0;
-  dbuf<int> g_rows, ucol;
-  dbuf<int64_t> g_uoff;
+  int64_t n_pairs = 0;
+  dbuf<int> g_rows, ucol, gperm;
+  dbuf<int64_t> g_uoff, g_poff;
   dbuf<uint8_t> umask;
+  dbuf<unsigned char> gval;
   bool identity = false;  // short rows are exactly [row0, row0 + n_short)
   int row0 = 0;
   dbuf<int> short_rows, long_rows, seg_k0, seg_k1;
@@ -910,29 +927,37 @@ struct SpmmWork {
                     const std::vector<int>& ci, cudaStream_t st) {
     const int R = kGroupR;
     const int64_t ng = ((int64_t)sh.size() + R - 1) / R;
-    std::vector<int> grows((size_t)ng * R, -1), uc;
+    std::vector<int> grows((size_t)ng * R, -1), uc, perm;
     std::vector<uint8_t> um;
-    std::vector<int64_t> uoff{0};
+    std::vector<int64_t> uoff{0}, poff{0};
     int64_t nnz = 0;
-    std::vector<std::pair<int, int>> tmp;
+    struct E { int col, row, k; };
+    std::vector<E> tmp;
     for (int64_t g = 0; g < ng; ++g) {
       tmp.clear();
       for (int r = 0; r < R && g * R + r < (int64_t)sh.size(); ++r) {
         const int row = sh[g * R + r];
         grows[g * R + r] = row;
-        for (int k = rp[row]; k < rp[row + 1]; ++k) tmp.emplace_back(ci[k], r);
+        for (int k = rp[row]; k < rp[row + 1]; ++k) tmp.push_back({ci[k], r, k});
         nnz += rp[row + 1] - rp[row];
       }
-      std::sort(tmp.begin(), tmp.end());
+      std::sort(tmp.begin(), tmp.end(), [](const E& x, const E& y) {
+        return x.col < y.col || (x.col == y.col && x.row < y.row);
+      });
       for (size_t q = 0; q < tmp.size();) {
         size_t e = q;
         int mask = 0;
-        while (e < tmp.size() && tmp[e].first == tmp[q].first) mask |= 1 << tmp[e++].second;
-        uc.push_back(tmp[q].first);
+        while (e < tmp.size() && tmp[e].col == tmp[q].col) {
+          mask |= 1 << tmp[e].row;
+          perm.push_back(tmp[e].k);  // pair order: column, then row
+          ++e;
+        }
+        uc.push_back(tmp[q].col);
         um.push_back((uint8_t)mask);
         q = e;
       }
       uoff.push_back((int64_t)uc.size());
+      poff.push_back((int64_t)perm.size());
     }
     if (nnz == 0 || (double)uc.size() > 0.75 * (double)nnz) return;
     grouped = true;
@@ -946,6 +971,12 @@ struct SpmmWork {
     h2d(ucol.p, uc.data(), uc.size(), st);
     umask.alloc(um.size() + 1);
     h2d(umask.p, um.data(), um.size(), st);
+    n_pairs = (int64_t)perm.size();
+    g_poff.alloc(poff.size());
+    h2d(g_poff.p, poff.data(), poff.size(), st);
+    gperm.alloc(perm.size() + 1);
+    h2d(gperm.p, perm.data(), perm.size(), st);
+    gval.alloc((perm.size() + 64) * elem_);
     TFG_CUDA(cudaStreamSynchronize(st));
   }
 
@@ -994,14 +1025,20 @@ struct SpmmWork {
     partial.alloc((size_t)n_seg * cc * elem);
     TFG_CUDA(cudaStreamSynchronize(st));
     const int vec = 16 / (int)elem;
-    if (ci && (cc == 32 * vec || cc == 64 * vec) && !sh.empty()) build_groups(sh, rp, *ci, st);
+    elem_ = elem;
+    static const bool groups_on = [] {
+      const char* e = getenv("TFG_SPMM_GROUPS");
+      return e && atoi(e) > 0;
+    }();
+    if (groups_on && ci && (cc == 32 * vec || cc == 64 * vec) && !sh.empty())
+      build_groups(sh, rp, *ci, st);
   }
   size_t bytes() const {
     return short_rows.bytes() + long_rows.bytes() + seg_k0.bytes() + seg_k1.bytes() +
            long_seg_off.bytes() + partial.bytes() + g_rows.bytes() + ucol.bytes() +
-           g_uoff.bytes() + umask.bytes();
+           g_uoff.bytes() + umask.bytes() + g_poff.bytes() + gperm.bytes() + gval.bytes();
   }
-  int launches() const { return (n_short > 0) + 2 * (n_long > 0); }
+  int launches() const { return (n_short > 0) + 2 * (n_long > 0) + (grouped ? 1 : 0); }
 };
 
 template <class T>
@@ -1011,13 +1048,18 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   if (w.n_short == 0) return;
   if (w.grouped) {
     constexpr int VEC = 16 / sizeof(T);
+    T* gval = reinterpret_cast<T*>(w.gval.p);
+    k_permute_values<T><<<blocks_for(w.n_pairs), 256, 0, st>>>(w.n_pairs, w.gperm.p, av, gval);
+    TFG_LAUNCH_CHECK();
     const int nb = blocks_for(w.n_groups * 32);
     if (cc == 32 * VEC)
       k_spmm_group<T, VEC, 1, SpmmWork::kGroupR, 4, 2><<<nb, 256, 0, st>>>(
-          w.n_groups, w.g_rows.p, w.g_uoff.p, w.ucol.p, w.umask.p, rp, av, X, cc, out, cc);
+          w.n_groups, w.g_rows.p, w.g_uoff.p, w.g_poff.p, w.ucol.p, w.umask.p, gval, X, cc, out,
+          cc);
     else
       k_spmm_group<T, VEC, 2, SpmmWork::kGroupR, 4, 1><<<nb, 256, 0, st>>>(
-          w.n_groups, w.g_rows.p, w.g_uoff.p, w.ucol.p, w.umask.p, rp, av, X, cc, out, cc);
+          w.n_groups, w.g_rows.p, w.g_uoff.p, w.g_poff.p, w.ucol.p, w.umask.p, gval, X, cc, out,
+          cc);
     TFG_LAUNCH_CHECK();
     return;
   }
@@ -1026,7 +1068,7 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   const int64_t n = w.n_short;
   constexpr int VEC = 16 / sizeof(T);
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  k_spmm_strip<T, VEC, LPR, NCH, 8><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
+  k_spmm_strip<T, VEC, LPR, NCH, 4, 4><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
       n, rows, row0, rp, ci, av, X, cc, out, cc);                                \
   TFG_LAUNCH_CHECK();                                                            \
   return;

@@ -27,9 +27,13 @@ print(json.dumps({k: [float(np.median([m for m, _ in v])), v[0][1] / float(np.me
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-    variants = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [-1] + list(range(11))
+    variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
     for v in variants:
         env = dict(os.environ)
+        if v.startswith("g"):
+            env["TFG_SPMM_GROUPS"] = "1"
+            v = v[1:] or "-1"
+        v = int(v)
         if v >= 0:
             env["TFG_SPMM_VARIANT"] = str(v)
         r = subprocess.run([sys.executable, "-c", CODE % (ROOT, cfg)], capture_output=True, text=True, env=env)
