@@ -156,13 +156,13 @@ __device__ __forceinline__ void spmm_row(int kb, int ke,
 // gathered, and X gathers are issued UNR at a time (predicated), so each
 // row costs about one dependent memory round trip.  Per-element order stays
 // ascending with separately rounded mul/add (kernels.hpp:75-79).
-template <class T, int VEC, int LPR, int NCH, int UNR, int MINB = 1>
+template <class T, int VEC, int LPR, int NCH, int UNR, int MINB = 1, int STRIP = LPR>
 __global__ void __launch_bounds__(256, MINB)
     k_spmm_strip(int64_t nrows, const int* __restrict__ rows, int row0,
                  const int* __restrict__ rp, const int* __restrict__ ci,
                  const T* __restrict__ av, const T* __restrict__ X, int ldx,
                  T* __restrict__ out, int ldo) {
-  constexpr int STRIP = LPR;
+  static_assert(STRIP >= 1 && STRIP <= LPR, "strip");
   const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
   const int64_t base = g * STRIP;
   if (base >= nrows) return;
@@ -351,6 +351,182 @@ __global__ void k_permute_values(int64_t np, const int* __restrict__ perm,
     gval[p] = __ldg(av + __ldg(perm + p));
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---- band-staged SpMM (TMA bulk copies into shared memory) -------------------
+// For matrices whose consecutive rows reuse a few contiguous ranges of X rows
+// (stencils, banded matrices), the plan cuts the row list into blocks of R
+// rows and records, per block, the union of X rows it reads as <= kBandRuns
+// contiguous runs plus a compact local index record (uint16 row offsets and
+// uint16 stage slots).  A persistent CTA double-buffers blocks: one thread
+// issues cp.async.bulk copies of the runs (row-major X rows are contiguous)
+// and of the index record, completing on an mbarrier; all threads cp.async
+// the block's values from the live CSR.  Rows are then summed from shared
+// memory in the reference order (bit-identical), so each X row crosses
+// L2->SM once per block instead of once per nonzero.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "n"(BYTES));
+}
+
+constexpr int kBandRuns = 32;
+
+template <class T, int VEC, int LPR, int NCH>
+__global__ void __launch_bounds__(256, 1)
+    k_spmm_band(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
+                const T* __restrict__ av, const int* __restrict__ run_begin,
+                const int* __restrict__ run_start, const int* __restrict__ run_len,
+                const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
+                int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
+                T* __restrict__ out, int ldo) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int cc = ldx;
+  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
+  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
+  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
+  const size_t bufbytes = xbytes + ibytes + vbytes;
+  __shared__ __align__(8) uint64_t mbar[2];
+  const int tid = threadIdx.x;
+  const int gl = tid & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int group = tid / LPR, ngroups = blockDim.x / LPR;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int b, int buf) {
+    unsigned char* base = smem_raw + (size_t)buf * bufbytes;
+    T* xs = reinterpret_cast<T*>(base);
+    uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
+    T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
+    const int r_lo = row0 + b * R;
+    const int r_hi = min(r_lo + R, row0 + nrows);
+    const int k0 = __ldg(rp + r_lo), k1 = __ldg(rp + r_hi);
+    if (tid == 0) {
+      const int rb = run_begin[b], re = run_begin[b + 1];
+      const int64_t i0 = idx_off[b], i1 = idx_off[b + 1];
+      unsigned total = (unsigned)((i1 - i0) * 2);
+      for (int q = rb; q < re; ++q) total += (unsigned)run_len[q] * cc * sizeof(T);
+      mbar_expect_tx(&mbar[buf], total);
+      int off = 0;
+      for (int q = rb; q < re; ++q) {
+        const int len = run_len[q];
+        const char* src = reinterpret_cast<const char*>(X + (size_t)run_start[q] * cc);
+        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
+        size_t left = (size_t)len * cc * sizeof(T);
+        while (left) {
+          const unsigned chunk = (unsigned)min(left, (size_t)32768);
+          bulk_g2s(dst, src, chunk, &mbar[buf]);
+          dst += chunk;
+          src += chunk;
+          left -= chunk;
+        }
+        off += len;
+      }
+      if (i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &mbar[buf]);
+    }
+    for (int k = k0 + tid; k < k1; k += blockDim.x) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
+    cp_async_commit();
+  };
+
+  int it = 0;
+  int b = blockIdx.x;
+  if (b < nblk) issue(b, 0);
+  for (; b < nblk; b += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int bn = b + gridDim.x;
+    if (bn < nblk)
+      issue(bn, buf ^ 1);
+    else
+      cp_async_commit();
+    mbar_wait(&mbar[buf], (unsigned)((it >> 1) & 1));
+    cp_async_wait<1>();
+    __syncthreads();
+    unsigned char* base = smem_raw + (size_t)buf * bufbytes;
+    const T* xs = reinterpret_cast<const T*>(base);
+    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
+    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
+    const int r_lo = row0 + b * R;
+    const int nr = min(R, row0 + nrows - r_lo);
+    const uint16_t* lrp = is;          // nr + 1 local offsets
+    const uint16_t* lsl = is + nr + 1; // slots
+    for (int r = group; r < nr; r += ngroups) {
+      const int eb = lrp[r], ee = lrp[r + 1];
+      T acc[NCH][VEC];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+      for (int e0 = eb; e0 < ee; e0 += LPR) {
+        int sl = 0;
+        T a = T(0);
+        if (e0 + gl < ee) {
+          sl = lsl[e0 + gl];
+          a = vs[e0 + gl];
+        }
+        const int cnt = min(LPR, ee - e0);
+        for (int u = 0; u < cnt; ++u) {
+          const int su = __shfl_sync(gmask, sl, u, LPR);
+          const T au = __shfl_sync(gmask, a, u, LPR);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            T x[VEC];
+            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+          }
+        }
+      }
+      T* o = out + (size_t)(r_lo + r) * ldo;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
 // Generic SpMM (any column count): one warp per row, scalar columns.
 template <class T>
 __global__ void __launch_bounds__(256)
@@ -496,17 +672,6 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 // thread owns a TM x TN register tile.  Per element the k loop ascends with
 // fused multiply-add from 0 -- the same sequence k_gemm_blocks and the fused
 // kernel use, so every path produces identical bits.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
 struct GemmCfg {
   static constexpr int V = 16 / (int)sizeof(T);  // elements per 16 B
@@ -907,6 +1072,107 @@ struct SpmmWork {
   // row-group union layout of the short rows (used when it cuts X gathers)
   static constexpr int kGroupR = 8;
   size_t elem_ = 8;
+  bool skewed = false;  // row lengths vary a lot: one row per lane group
+  // band-staged layout (k_spmm_band)
+  bool banded = false;
+  int band_R = 0, band_blocks = 0, stage_cap = 0, idx_cap = 0, val_cap = 0;
+  size_t band_smem = 0;
+  dbuf<int> run_begin, run_start, run_len;
+  dbuf<int64_t> idx_off;
+  dbuf<uint16_t> lidx;
+
+  // Blocks of R consecutive rows whose X rows form <= kBandRuns contiguous
+  // runs; adopted only when it at least halves the X rows gathered.
+  void build_band(int row0, int64_t nrows, const std::vector<int>& rp,
+                  const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st) {
+    const size_t row_bytes = (size_t)cc * elem;
+    const size_t budget = 100 * 1024;
+    int64_t nnz_total = (int64_t)rp[row0 + nrows] - rp[row0];
+    if (nnz_total <= 0) return;
+    for (int R : {128, 64, 32, 16, 8}) {
+      const int nb = (int)((nrows + R - 1) / R);
+      std::vector<int> rb{0}, rs, rl, li;
+      std::vector<int64_t> io{0};
+      int64_t staged_total = 0;
+      int scap = 0, icap = 0, vcap = 0;
+      bool ok = true;
+      std::vector<int> cols;
+      for (int b = 0; b < nb && ok; ++b) {
+        const int r_lo = row0 + b * R;
+        const int r_hi = (int)std::min<int64_t>(r_lo + R, row0 + nrows);
+        const int k0 = rp[r_lo], k1 = rp[r_hi];
+        cols.assign(ci.begin() + k0, ci.begin() + k1);
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        // runs, merging gaps of up to 2 rows
+        std::vector<std::pair<int, int>> runs;
+        for (int c : cols) {
+          if (!runs.empty() && c <= runs.back().first + runs.back().second + 2)
+            runs.back().second = c - runs.back().first + 1;
+          else
+            runs.emplace_back(c, 1);
+        }
+        int staged = 0;
+        for (auto& r : runs) staged += r.second;
+        const int nr = r_hi - r_lo;
+        const int irec = ((nr + 1 + (k1 - k0)) + 7) / 8 * 8;
+        const size_t need = (size_t)staged * row_bytes + (size_t)irec * 2 +
+                            ((size_t)(k1 - k0) * elem + 15) / 16 * 16;
+        if ((int)runs.size() > kBandRuns || staged > 65535 || need > budget) {
+          ok = false;
+          break;
+        }
+        scap = std::max(scap, staged);
+        icap = std::max(icap, irec);
+        vcap = std::max(vcap, k1 - k0);
+        staged_total += staged;
+        // local index record: row offsets then slots
+        int off = 0;
+        std::vector<int> run_off;
+        for (auto& r : runs) {
+          rs.push_back(r.first);
+          rl.push_back(r.second);
+          run_off.push_back(off);
+          off += r.second;
+        }
+        rb.push_back((int)rs.size());
+        const size_t rec0 = li.size();
+        for (int r = r_lo; r <= r_hi; ++r) li.push_back(rp[r] - k0);
+        for (int k = k0; k < k1; ++k) {
+          const int c = ci[k];
+          size_t q = std::upper_bound(runs.begin(), runs.end(), std::make_pair(c, INT32_MAX)) -
+                     runs.begin() - 1;
+          li.push_back(run_off[q] + (c - runs[q].first));
+        }
+        while ((li.size() - rec0) % 8) li.push_back(0);
+        io.push_back((int64_t)li.size());
+      }
+      if (!ok) continue;
+      if ((double)staged_total > 0.5 * (double)nnz_total) return;  // not worth it
+      banded = true;
+      band_R = R;
+      band_blocks = nb;
+      stage_cap = scap;
+      idx_cap = icap;
+      val_cap = vcap;
+      std::vector<uint16_t> l16(li.begin(), li.end());
+      run_begin.alloc(rb.size());
+      h2d(run_begin.p, rb.data(), rb.size(), st);
+      run_start.alloc(rs.size() + 1);
+      h2d(run_start.p, rs.data(), rs.size(), st);
+      run_len.alloc(rl.size() + 1);
+      h2d(run_len.p, rl.data(), rl.size(), st);
+      idx_off.alloc(io.size());
+      h2d(idx_off.p, io.data(), io.size(), st);
+      lidx.alloc(l16.size() + 8);
+      h2d(lidx.p, l16.data(), l16.size(), st);
+      const size_t buf = (size_t)scap * row_bytes + ((size_t)icap * 2 + 15) / 16 * 16 +
+                         ((size_t)vcap * elem + 15) / 16 * 16;
+      band_smem = 2 * buf;
+      TFG_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+  }
   bool grouped = false;
   int64_t n_groups = 0, n_ucols = 0;
   int64_t n_pairs = 0;
@@ -1026,6 +1292,23 @@ struct SpmmWork {
     TFG_CUDA(cudaStreamSynchronize(st));
     const int vec = 16 / (int)elem;
     elem_ = elem;
+    if (!sh.empty()) {  // skew: longest short row vs the mean
+      int64_t tot = 0;
+      int mx = 0;
+      for (int r : sh) {
+        tot += rp[r + 1] - rp[r];
+        mx = std::max(mx, rp[r + 1] - rp[r]);
+      }
+      const double mean = (double)tot / (double)sh.size();
+      skewed = mx > 8.0 * std::max(mean, 1.0);
+    }
+    static const bool band_on = [] {
+      const char* e = getenv("TFG_SPMM_BAND");
+      return !e || atoi(e) > 0;
+    }();
+    if (band_on && ci && identity && (cc % vec == 0) &&
+        (cc / vec == 8 || cc / vec == 16 || cc / vec == 32 || cc / vec == 64))
+      build_band(row0, n_short, rp, *ci, cc, elem, st);
     static const bool groups_on = [] {
       const char* e = getenv("TFG_SPMM_GROUPS");
       return e && atoi(e) > 0;
@@ -1036,7 +1319,9 @@ struct SpmmWork {
   size_t bytes() const {
     return short_rows.bytes() + long_rows.bytes() + seg_k0.bytes() + seg_k1.bytes() +
            long_seg_off.bytes() + partial.bytes() + g_rows.bytes() + ucol.bytes() +
-           g_uoff.bytes() + umask.bytes() + g_poff.bytes() + gperm.bytes() + gval.bytes();
+           g_uoff.bytes() + umask.bytes() + g_poff.bytes() + gperm.bytes() + gval.bytes() +
+           run_begin.bytes() + run_start.bytes() + run_len.bytes() + idx_off.bytes() +
+           lidx.bytes();
   }
   int launches() const { return (n_short > 0) + 2 * (n_long > 0) + (grouped ? 1 : 0); }
 };
@@ -1046,6 +1331,28 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
                                 const T* av, const T* X, int cc, T* out,
                                 cudaStream_t st) {
   if (w.n_short == 0) return;
+  if (w.banded) {
+    constexpr int VEC = 16 / sizeof(T);
+    const int L = cc / VEC;
+    const int grid = std::min<int>(w.band_blocks, sm_count());
+#define TFG_BAND(LPR, NCH)                                                                   \
+  {                                                                                          \
+    auto kern = k_spmm_band<T, VEC, LPR, NCH>;                                               \
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                  (int)w.band_smem));                                        \
+    kern<<<grid, 256, w.band_smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av, \
+                                         w.run_begin.p, w.run_start.p, w.run_len.p,          \
+                                         w.idx_off.p, w.lidx.p, w.stage_cap, w.idx_cap,      \
+                                         w.val_cap, X, cc, out, cc);                         \
+    TFG_LAUNCH_CHECK();                                                                      \
+    return;                                                                                  \
+  }
+    if (L == 8) TFG_BAND(8, 1)
+    if (L == 16) TFG_BAND(16, 1)
+    if (L == 32) TFG_BAND(32, 1)
+    if (L == 64) TFG_BAND(32, 2)
+#undef TFG_BAND
+  }
   if (w.grouped) {
     constexpr int VEC = 16 / sizeof(T);
     T* gval = reinterpret_cast<T*>(w.gval.p);
@@ -1068,8 +1375,12 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   const int64_t n = w.n_short;
   constexpr int VEC = 16 / sizeof(T);
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  k_spmm_strip<T, VEC, LPR, NCH, 4, 4><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
-      n, rows, row0, rp, ci, av, X, cc, out, cc);                                \
+  if (w.skewed)                                                                  \
+    k_spmm_strip<T, VEC, LPR, NCH, 4, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
+  else                                                                           \
+    k_spmm_strip<T, VEC, LPR, NCH, 4, 4><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
   TFG_LAUNCH_CHECK();                                                            \
   return;
   if constexpr (sizeof(T) == 8) {
