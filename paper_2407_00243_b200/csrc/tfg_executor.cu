@@ -765,6 +765,125 @@ __device__ __forceinline__ void gemm_block(const T* __restrict__ B, int bc,
   __syncthreads();
 }
 
+// Pipeline pieces shared by the streamed GEMM kernels: one K-chunk load of
+// (B row block, C chunk) into ring stage `stg`, and one chunk of FMAs.
+template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
+__device__ __forceinline__ void gemm_load_chunk(const T* __restrict__ B, int bc,
+                                                const T* __restrict__ C, int cc, int n0,
+                                                int r0, int cnt, int kc, int stg, T* smem) {
+  using G = GemmCfg<T, BM, BN, BK, TM, TN, STAGES>;
+  constexpr int V = G::V;
+  T* bdst = smem + (size_t)stg * BM * G::B_LD;
+  T* cdst = smem + (size_t)STAGES * BM * G::B_LD + (size_t)stg * BK * G::C_LD;
+  const int k0 = kc * BK;
+  for (int e = threadIdx.x; e < BM * (BK / V); e += G::THREADS) {
+    const int m = e / (BK / V), kv = (e % (BK / V)) * V;
+    const bool ok = m < cnt && k0 + kv < bc;
+    cp_async16(bdst + m * G::B_LD + kv, ok ? B + (size_t)(r0 + m) * bc + k0 + kv : B, ok ? 16 : 0);
+  }
+  for (int e = threadIdx.x; e < BK * (BN / V); e += G::THREADS) {
+    const int kk = e / (BN / V), nv = (e % (BN / V)) * V;
+    const bool ok = k0 + kk < bc;
+    cp_async16(cdst + kk * G::C_LD + nv, ok ? C + (size_t)(k0 + kk) * cc + n0 + nv : C, ok ? 16 : 0);
+  }
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
+__device__ __forceinline__ void gemm_compute_chunk(int bc, int kc, int stg, const T* smem,
+                                                   T (&acc)[TM][TN]) {
+  using G = GemmCfg<T, BM, BN, BK, TM, TN, STAGES>;
+  constexpr int V = G::V;
+  const int tx = threadIdx.x % (BN / TN), ty = threadIdx.x / (BN / TN);
+  const T* bs = smem + (size_t)stg * BM * G::B_LD;
+  const T* cs = smem + (size_t)STAGES * BM * G::B_LD + (size_t)stg * BK * G::C_LD;
+  const int kn = min(BK, bc - kc * BK);
+  for (int k0 = 0; k0 < kn; k0 += V) {
+    T a[TM][V];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) ldv<T, V>(a[i], bs + (ty * TM + i) * G::B_LD + k0);
+    const int kv = min(V, kn - k0);
+#pragma unroll
+    for (int kk = 0; kk < V; ++kk) {
+      if (kk < kv) {
+        T b[TN];
+#pragma unroll
+        for (int j = 0; j < TN; j += V) {
+          T tmp[V];
+          ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + tx * TN + j);
+#pragma unroll
+          for (int q = 0; q < V; ++q) b[j + q] = tmp[q];
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fops<T>::fma(a[i][kk], b[j], acc[i][j]);
+      }
+    }
+  }
+}
+
+// Streamed GEMM: the CTA's row blocks blk = blockIdx.x + j*gridDim.x are
+// flattened with their K chunks into one cp.async ring, so loads of the next
+// block overlap the current block's FMAs and epilogue.
+template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
+__global__ void __launch_bounds__(256)
+    k_gemm_stream(int64_t nblk, const int* __restrict__ blk_r0, const int* __restrict__ blk_cnt,
+                  const T* __restrict__ B, int bc, const T* __restrict__ C, int cc,
+                  T* __restrict__ D1, int ldd) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  constexpr int V = 16 / (int)sizeof(T);
+  const int n0 = blockIdx.y * BN;
+  const int tx = threadIdx.x % (BN / TN), ty = threadIdx.x / (BN / TN);
+  const int nk = (bc + BK - 1) / BK;
+  const int64_t nmine = blockIdx.x < nblk ? (nblk - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nmine * nk;
+  auto load = [&](int64_t t) {
+    const int64_t blk = blockIdx.x + (t / nk) * gridDim.x;
+    gemm_load_chunk<T, BM, BN, BK, TM, TN, STAGES>(B, bc, C, cc, n0, blk_r0[blk], blk_cnt[blk],
+                                                   (int)(t % nk), (int)(t % STAGES), smem);
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < total) load(s);
+    cp_async_commit();
+  }
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+  for (int64_t t = 0; t < total; ++t) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (t + STAGES - 1 < total) load(t + STAGES - 1);
+    cp_async_commit();
+    const int kc = (int)(t % nk);
+    gemm_compute_chunk<T, BM, BN, BK, TM, TN, STAGES>(bc, kc, (int)(t % STAGES), smem, acc);
+    if (kc == nk - 1) {
+      const int64_t blk = blockIdx.x + (t / nk) * gridDim.x;
+      const int r0 = blk_r0[blk], cnt = blk_cnt[blk];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int m = ty * TM + i;
+        if (m < cnt) {
+          T* o = D1 + (size_t)(r0 + m) * ldd + n0 + tx * TN;
+#pragma unroll
+          for (int j = 0; j < TN; j += V) {
+            T tmp[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
+            stv<T, V>(o + j, tmp);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
 __global__ void __launch_bounds__(256)
     k_gemm_v2(int64_t nblk, const int* __restrict__ blk_r0, const int* __restrict__ blk_cnt,
@@ -919,7 +1038,8 @@ __global__ void __launch_bounds__(256)
                        const T* __restrict__ C, int cc, const int* __restrict__ arp,
                        const int* __restrict__ aci, const T* __restrict__ av,
                        const uint8_t* __restrict__ spill, T* D1, T* __restrict__ D) {
-  using G = GemmCfg<T, BM, BN, BK, TM, TN, 3>;
+  constexpr int STAGES = 3;
+  using G = GemmCfg<T, BM, BN, BK, TM, TN, STAGES>;
   constexpr int V = G::V;
   constexpr int VEC = 16 / (int)sizeof(T);
   constexpr int NCH = BN / (LPR * VEC);
@@ -932,53 +1052,112 @@ __global__ void __launch_bounds__(256)
   const int gl = threadIdx.x & (LPR - 1);
   const unsigned gmask = group_mask(LPR);
   const int group = threadIdx.x / LPR, ngroups = blockDim.x / LPR;
-  for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
-    const int ilo = t_ilo[v], ihi = t_ihi[v];
-    const bool wide = t_wide[v] != 0;
-    for (int r0 = ilo; r0 < ihi; r0 += BM) {
-      const int cnt = min(BM, ihi - r0);
-      T acc[TM][TN];
-      gemm_block<T, BM, BN, BK, TM, TN, 3>(B, bc, C, cc, n0, r0, cnt, gsm, acc);
+  const int nk = (bc + BK - 1) / BK;
+
+  // cursor over this CTA's (tile, row block, k chunk) sequence
+  struct Cur {
+    int64_t v;
+    int r0, ihi, kc;
+  };
+  auto start = [&](Cur& c) {
+    c.v = blockIdx.x;
+    c.kc = 0;
+    if (c.v < ntiles) {
+      c.r0 = t_ilo[c.v];
+      c.ihi = t_ihi[c.v];
+    }
+  };
+  auto next = [&](Cur& c) {
+    if (++c.kc < nk) return;
+    c.kc = 0;
+    c.r0 += BM;
+    if (c.r0 >= c.ihi) {
+      c.v += gridDim.x;
+      if (c.v < ntiles) {
+        c.r0 = t_ilo[c.v];
+        c.ihi = t_ihi[c.v];
+      }
+    }
+  };
+  Cur lc, cu;
+  start(lc);
+  start(cu);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (lc.v < ntiles) {
+      gemm_load_chunk<T, BM, BN, BK, TM, TN, STAGES>(B, bc, C, cc, n0, lc.r0,
+                                                     min(BM, lc.ihi - lc.r0), lc.kc, s, gsm);
+      next(lc);
+    }
+    cp_async_commit();
+  }
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+  for (int64_t t = 0; cu.v < ntiles; ++t) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (lc.v < ntiles) {
+      gemm_load_chunk<T, BM, BN, BK, TM, TN, STAGES>(B, bc, C, cc, n0, lc.r0,
+                                                     min(BM, lc.ihi - lc.r0), lc.kc,
+                                                     (int)((t + STAGES - 1) % STAGES), gsm);
+      next(lc);
+    }
+    cp_async_commit();
+    gemm_compute_chunk<T, BM, BN, BK, TM, TN, STAGES>(bc, cu.kc, (int)(t % STAGES), gsm, acc);
+    if (cu.kc == nk - 1) {
+      const int64_t v = cu.v;
+      const int r0 = cu.r0, cnt = min(BM, cu.ihi - cu.r0);
+      const bool wide = t_wide[v] != 0;
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
         const int m = ty * TM + i;
-        if (m >= cnt) continue;
-        const int row = r0 + m;
-        const int sl = wide ? -1 : __ldg(slot + row);
-        const bool sp = wide || spill[row];
+        if (m < cnt) {
+          const int row = r0 + m;
+          const int sl = wide ? -1 : __ldg(slot + row);
+          const bool sp = wide || spill[row];
 #pragma unroll
-        for (int j = 0; j < TN; j += V) {
-          T tmp[V];
+          for (int j = 0; j < TN; j += V) {
+            T tmp[V];
 #pragma unroll
-          for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
-          if (sp) stv<T, V>(D1 + (size_t)row * cc + n0 + tx * TN + j, tmp);
-          if (sl >= 0) stv<T, V>(stage + (size_t)sl * BN + tx * TN + j, tmp);
+            for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
+            if (sp) stv<T, V>(D1 + (size_t)row * cc + n0 + tx * TN + j, tmp);
+            if (sl >= 0) stv<T, V>(stage + (size_t)sl * BN + tx * TN + j, tmp);
+          }
         }
-      }
-    }
-    __syncthreads();
-    const int64_t jb = t_joff[v], je = t_joff[v + 1];
-    for (int64_t q = jb + group; q < je; q += ngroups) {
-      const int j = jrows[q];
-      const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
-      T acc[NCH][VEC];
-      if (wide) {
-        auto xl = [&](int c, int ch, T(&x)[VEC]) {
-          ldv<T, VEC>(x, D1 + (size_t)c * cc + n0 + (ch * LPR + gl) * VEC);
-        };
-        spmm_row<T, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc);
-      } else {
-        auto xl = [&](int c, int ch, T(&x)[VEC]) {
-          ldv<T, VEC>(x, stage + (size_t)__ldg(slot + c) * BN + (ch * LPR + gl) * VEC);
-        };
-        spmm_row<T, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc);
-      }
-      T* o = D + (size_t)j * cc + n0;
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+      }
+      if (r0 + BM >= cu.ihi) {  // last block of the tile: fused rows from the stage
+        __syncthreads();
+        const int64_t jb = t_joff[v], je = t_joff[v + 1];
+        for (int64_t q = jb + group; q < je; q += ngroups) {
+          const int j = jrows[q];
+          const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
+          T acc2[NCH][VEC];
+          if (wide) {
+            auto xl = [&](int c, int ch, T(&x)[VEC]) {
+              ldv<T, VEC>(x, D1 + (size_t)c * cc + n0 + (ch * LPR + gl) * VEC);
+            };
+            spmm_row<T, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc2);
+          } else {
+            auto xl = [&](int c, int ch, T(&x)[VEC]) {
+              ldv<T, VEC>(x, stage + (size_t)__ldg(slot + c) * BN + (ch * LPR + gl) * VEC);
+            };
+            spmm_row<T, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc2);
+          }
+          T* o = D + (size_t)j * cc + n0;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc2[ch]);
+        }
+        __syncthreads();
+      }
     }
-    __syncthreads();
+    next(cu);
   }
+  cp_async_wait<0>();
 }
 
 // slot[i] = position of D1 row i in its tile's stage (-1: not read by the
@@ -1086,10 +1265,13 @@ struct SpmmWork {
   void build_band(int row0, int64_t nrows, const std::vector<int>& rp,
                   const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st) {
     const size_t row_bytes = (size_t)cc * elem;
-    const size_t budget = 100 * 1024;
+    static const size_t budget = [] {
+      const char* e = getenv("TFG_BAND_KB");
+      return (size_t)(e ? atoi(e) : 24) * 1024;
+    }();
     int64_t nnz_total = (int64_t)rp[row0 + nrows] - rp[row0];
     if (nnz_total <= 0) return;
-    for (int R : {128, 64, 32, 16, 8}) {
+    for (int R : {256, 128, 64, 32, 16, 8, 4}) {
       const int nb = (int)((nrows + R - 1) / R);
       std::vector<int> rb{0}, rs, rl, li;
       std::vector<int64_t> io{0};
@@ -1805,7 +1987,7 @@ template <class T, int BM, int BN, int BK, int TM, int TN>
 static void launch_gemm_v2_cfg(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
                                cudaStream_t st) {
   using G = GemmCfg<T, BM, BN, BK, TM, TN, 3>;
-  auto kern = k_gemm_v2<T, BM, BN, BK, TM, TN, 3>;
+  auto kern = k_gemm_stream<T, BM, BN, BK, TM, TN, 3>;
   static bool attr = false;
   if (!attr) {
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));

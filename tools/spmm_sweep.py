@@ -30,6 +30,12 @@ def main():
     variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
     for v in variants:
         env = dict(os.environ)
+        if v.startswith("b"):
+            env["TFG_BAND_KB"] = v[1:]
+            v = "-1"
+        if v.startswith("n"):
+            env["TFG_SPMM_BAND"] = "0"
+            v = "-1"
         if v.startswith("g"):
             env["TFG_SPMM_GROUPS"] = "1"
             v = v[1:] or "-1"
