@@ -169,6 +169,27 @@ typedef struct {
 tfg_status tfg_plan_create(const tfg_problem *p, const tfg_schedule *s,
                            void *stream, tfg_plan **out);
 
+/* Multi-GPU row-block partition: the plan of the rank owning
+ * rows [row_lo, row_hi).  It runs the wavefront-0 tiles whose i_lo lies in
+ * the block (the caller cuts at tile boundaries, so fused rows need no
+ * remote D1) and the wavefront-1 rows j in the block; every D1 row some
+ * wavefront-1 row reads is written to the plan's D1 buffer (global row
+ * indexing) so it can be sent to peers.  D rows this rank computes are
+ * written into d_d at their global positions. */
+tfg_status tfg_plan_create_partition(const tfg_problem *p, const tfg_schedule *s,
+                                     int32_t row_lo, int32_t row_hi,
+                                     void *stream, tfg_plan **out);
+
+/* The plan's D1 scratch (n x c_cols, dtype of the problem): the halo
+ * exchange writes received rows into it between the two stages. */
+tfg_status tfg_plan_d1(const tfg_plan *plan, void **d_d1);
+
+/* Run one half of tfg_plan_execute: stage 0 = wavefront 0 (first op and
+ * fused tiles), stage 1 = wavefront 1 (SpMM over D1).  The kernel boundary
+ * between them is the wavefront barrier (kernels.hpp:118-119). */
+tfg_status tfg_plan_execute_stage(tfg_plan *plan, int32_t stage, void *d_d,
+                                  void *stream);
+
 /* D = A (B C) into the caller's device buffer d_d (n x c_cols row-major,
  * fully overwritten).  Asynchronous on `stream`; no host synchronisation,
  * no allocation, no host<->device traffic. */

@@ -81,6 +81,10 @@ SIGNATURES = [
                                         C.c_size_t]),
     ("tfg_plan_create", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
+    ("tfg_plan_create_partition", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_int32,
+                                            C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("tfg_plan_d1", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("tfg_plan_execute_stage", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     ("tfg_plan_execute", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tfg_plan_stats", C.c_int, [C.c_void_p, i64p, i64p, i64p]),
     ("tfg_plan_info", C.c_int, [C.c_void_p, i64p, i64p, i32p, i64p]),

@@ -1516,12 +1516,14 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   if (w.banded) {
     constexpr int VEC = 16 / sizeof(T);
     const int L = cc / VEC;
-    const int grid = std::min<int>(w.band_blocks, sm_count());
 #define TFG_BAND(LPR, NCH)                                                                   \
   {                                                                                          \
     auto kern = k_spmm_band<T, VEC, LPR, NCH>;                                               \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                   (int)w.band_smem));                                        \
+    int occ = 1;                                                                             \
+    TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, w.band_smem));   \
+    const int grid = (int)std::min<int64_t>(w.band_blocks, (int64_t)sm_count() * std::max(occ, 1)); \
     kern<<<grid, 256, w.band_smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av, \
                                          w.run_begin.p, w.run_start.p, w.run_len.p,          \
                                          w.idx_off.p, w.lidx.p, w.stage_cap, w.idx_cap,      \
@@ -1665,6 +1667,7 @@ struct tfg_plan {
   int64_t spill_rows = 0, fused_rows = 0;
   int64_t first_rows = 0, second_rows = 0, nnz_processed = 0;
   int launches = 0;
+  int row_lo = 0, row_hi = 0;  // row block of a partition plan (multi-GPU)
   // algorithmic (compulsory) HBM bytes per stage: (a) first op, (b) fused
   // tiles, (c) wavefront-1 SpMM -- each input byte read once, each output
   // byte written once (the roofline numerator)
@@ -1689,7 +1692,7 @@ static size_t fused_gemm_smem(const tfg_plan& pl) {
 }
 
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
-                 tfg_plan& pl) {
+                 tfg_plan& pl, int row_lo = 0, int row_hi = -1) {
   // problem.check() -- kernels.hpp:35-42; require_workers is the caller's.
   if (pr.dtype != TFG_F32 && pr.dtype != TFG_F64)
     throw invalid_argument("problem: unknown dtype");
@@ -1706,6 +1709,12 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   pl.elem = pr.dtype == TFG_F64 ? 8 : 4;
   pl.has_sched = s != nullptr;
   const int n = pr.n, cc = pr.c_cols, bc = pr.b_cols;
+  if (row_hi < 0) row_hi = n;
+  if (row_lo < 0 || row_hi > n || row_lo > row_hi)
+    throw invalid_argument("plan: partition rows out of range");
+  const bool partial = row_lo != 0 || row_hi != n;
+  pl.row_lo = row_lo;
+  pl.row_hi = row_hi;
 
   std::vector<int> arp(n + 1), brp;
   d2h(arp.data(), pr.d_a_row_ptr, n + 1, st);
@@ -1735,11 +1744,10 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     if (pl.gemm_kind) pl.gemm_bm = (pl.elem == 4 && pl.gemm_kind == 1) ? 128 : 64;
   }
   if (!s) {
-    fo_rows.resize(n);
-    for (int i = 0; i < n; ++i) fo_rows[i] = i;
+    for (int i = row_lo; i < row_hi; ++i) fo_rows.push_back(i);
     second_rows = fo_rows;
-    pl.first_rows = n;
-    pl.second_rows = n;
+    pl.first_rows = row_hi - row_lo;
+    pl.second_rows = row_hi - row_lo;
     pl.spill_rows = n;
   } else {
     const int64_t nt0 = s->n_tiles[0];
@@ -1752,13 +1760,22 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     second_rows.resize(nj1);
     d2h(second_rows.data(), s->j_rows[1].p, nj1, st);
     TFG_CUDA(cudaStreamSynchronize(st));
+    if (partial) {  // this rank owns the wavefront-1 rows of its row block
+      std::vector<int> mine;
+      for (int j : second_rows)
+        if (j >= row_lo && j < row_hi) mine.push_back(j);
+      second_rows.swap(mine);
+    }
     std::vector<int> jr0(s->n_jrows[0]);
     d2h(jr0.data(), s->j_rows[0].p, jr0.size(), st);
     TFG_CUDA(cudaStreamSynchronize(st));
     std::vector<int> f_ilo, f_ihi, f_rows;
     std::vector<int64_t> f_joff{0};
     int w_max = 0;
+    int64_t fused_here = 0;
     for (int64_t v = 0; v < nt0; ++v) {
+      if (ilo[v] < row_lo || ilo[v] >= row_hi) continue;  // tiles partitioned by i_lo
+      fused_here += joff[v + 1] - joff[v];
       pl.first_rows += ihi[v] - ilo[v];
       // empty fused rows need no D1 (D row = 0): the SpMM stage writes them
       const size_t before = f_rows.size();
@@ -1778,9 +1795,9 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         w_max = std::max(w_max, ihi[v] - ilo[v]);
       }
     }
-    pl.fused_rows = s->n_jrows[0];
-    pl.second_rows = s->n_jrows[0] + s->n_jrows[1];
-    pl.zero_d = pl.second_rows != n;
+    pl.fused_rows = fused_here;
+    pl.second_rows = fused_here + (int64_t)second_rows.size();
+    pl.zero_d = !partial && pl.second_rows != n;
     pl.n_ftiles = (int64_t)f_ilo.size();
     if (pl.n_ftiles) {
       pl.ft_ilo.alloc(pl.n_ftiles);
@@ -2050,11 +2067,13 @@ static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc,
 }
 
 template <class T>
-static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev = nullptr) {
+static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev = nullptr,
+                           int part = -1) {
   const tfg_problem& pr = pl.p;
   const int cc = pr.c_cols, bc = pr.b_cols;
   T* D1 = reinterpret_cast<T*>(pl.d1.p);
   const T* C = static_cast<const T*>(pr.d_c);
+  if (part == 1) goto wave1;
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
   // (a)
@@ -2092,6 +2111,8 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
     TFG_LAUNCH_CHECK();
   }
   if (ev) TFG_CUDA(cudaEventRecord(ev[2], st));
+  if (part == 0) return;
+wave1:
   // (c)
   spmm_run<T>(pl.second, pr.d_a_row_ptr, pr.d_a_col_idx,
               static_cast<const T*>(pr.d_a_val), D1, cc, D, st);
@@ -2103,6 +2124,15 @@ void plan_execute(tfg_plan& pl, void* d, cudaStream_t st, cudaEvent_t* ev = null
     plan_execute_t<double>(pl, static_cast<double*>(d), st, ev);
   else
     plan_execute_t<float>(pl, static_cast<float*>(d), st, ev);
+}
+
+// part 0: wavefront 0 (first op + fused tiles); part 1: wavefront-1 SpMM.
+// The multi-GPU driver runs the D1 halo exchange between the two.
+void plan_execute_part(tfg_plan& pl, void* d, cudaStream_t st, int part) {
+  if (pl.p.dtype == TFG_F64)
+    plan_execute_t<double>(pl, static_cast<double*>(d), st, nullptr, part);
+  else
+    plan_execute_t<float>(pl, static_cast<float*>(d), st, nullptr, part);
 }
 
 void gather_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
@@ -2159,6 +2189,38 @@ tfg_status tfg_plan_create(const tfg_problem* p, const tfg_schedule* s, void* st
       throw;
     }
     *out = pl;
+  });
+}
+
+tfg_status tfg_plan_create_partition(const tfg_problem* p, const tfg_schedule* s,
+                                     int32_t row_lo, int32_t row_hi, void* stream,
+                                     tfg_plan** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!p) throw invalid_argument("plan_create: null problem");
+    auto* pl = new tfg_plan;
+    try {
+      plan_create(*p, s, as_stream(stream), *pl, row_lo, row_hi);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    *out = pl;
+  });
+}
+
+tfg_status tfg_plan_d1(const tfg_plan* pl, void** d1) {
+  return guard([&] {
+    if (!pl) throw invalid_argument("plan_d1: null plan");
+    *d1 = pl->d1.p;
+  });
+}
+
+tfg_status tfg_plan_execute_stage(tfg_plan* pl, int32_t stage, void* d, void* stream) {
+  return guard([&] {
+    if (!pl || !d) throw invalid_argument("plan_execute_stage: null plan or output");
+    if (stage < 0 || stage > 1) throw invalid_argument("plan_execute_stage: stage 0 or 1");
+    plan_execute_part(*pl, d, as_stream(stream), stage);
   });
 }
 
