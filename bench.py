@@ -211,53 +211,116 @@ def run_ours(args, rank, world, dist):
     prob = P.DeviceProblem(w.a, w.b, w.c, w.dtype)
     torch.cuda.synchronize()
     sched = P.build_schedule(prob.a, cfg)  # GPU inspector, outside the timed region
-    plan = P.Plan(prob, sched)
     out = torch.empty((w.n, w.c_cols), dtype=getattr(torch, w.dtype.name), device=dev)
     flush = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+    plan = P.Plan(prob, sched) if rank == 0 else None
+    dplan, bounds, halo = None, None, None
+    if world > 1:
+        # row-block partition of the same global problem (strong scaling)
+        from paper_2407_00243_b200 import distributed as PD
 
-    def step():
-        plan.execute(out, stream)
+        flat = sched.export()
+        bounds = PD.tile_boundaries(flat, w.n, world)
+        halo = PD.halo_plan(w.a.row_ptr, w.a.col_idx, flat, bounds, rank)
+        eng = PD.GpuEngine(prob, sched, *bounds[rank])
+        dplan = PD.DistributedPlan(eng, halo, dist, w.c_cols)
+        launches = eng.launches + 3  # + gather, scatter, NCCL all-to-all
 
-    for _ in range(args.warmup):
-        flush.fill_(1.0)
-        step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.fill_(float(k))
-        evs[k][0].record(stream)
-        step()
-        evs[k][1].record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
-    if dist:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        def step():
+            dplan.execute(out)
+    else:
+        launches = plan.launches
+
+        def step():
+            plan.execute(out, stream)
+
+    def timed_loop(body, flush_between=True):
+        for _ in range(args.warmup):
+            if flush_between:
+                flush.fill_(1.0)
+            body()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for k in range(args.steps):
+            if flush_between:
+                flush.fill_(float(k))
+            evs[k][0].record(stream)
+            body()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tot = float(sum(a.elapsed_time(b) for a, b in evs))
+        if dist:
+            t = torch.tensor([tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+        return tot
+
+    total_ms = timed_loop(step)
+    mean_ms = total_ms / args.steps
+    value = w.flops() * args.steps / (total_ms * 1e-3) / 1e9  # the global problem, all ranks
+
     if args.quick:
         sampler.stop()
         if rank == 0:
-            print(json.dumps({"quick": True, "config": args.config, "ms_per_step": total_ms / args.steps,
-                              "value": world * w.flops() * args.steps / (total_ms * 1e-3) / 1e9}))
+            print(json.dumps({"quick": True, "config": args.config, "n_gpus": world,
+                              "ms_per_step": mean_ms, "value": value}))
         return
-    # a short same-kernel load tail so the clock sampler sees steady clocks
+
+    # end to end: pinned host A,B,C -> HBM, execute, D -> pinned host, every step
+    e2e = None
+    if not args.no_e2e:
+        host_in, dev_in = [], []
+        for t in [prob.a.row_ptr, prob.a.col_idx, prob.a.values, prob.c] + (
+                [prob.b] if prob.b_is_dense else [prob.b.row_ptr, prob.b.col_idx, prob.b.values]):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            host_in.append(h)
+            dev_in.append(t)
+        if world > 1:
+            from paper_2407_00243_b200 import distributed as PD
+
+            own = torch.as_tensor(PD.owned_output_rows(sched.export(), bounds, rank), device=dev)
+        else:
+            own = None
+        nout = w.n if own is None else int(own.numel())
+        host_out = torch.empty((nout, w.c_cols), dtype=out.dtype, pin_memory=True)
+        h2d = int(sum(h.numel() * h.element_size() for h in host_in))
+        d2h = int(host_out.numel() * host_out.element_size())
+
+        def e2e_step():
+            for h, d in zip(host_in, dev_in):
+                d.copy_(h, non_blocking=True)
+            step()
+            host_out.copy_(out if own is None else out.index_select(0, own), non_blocking=True)
+
+        e_ms = timed_loop(e2e_step, flush_between=False)
+        e2e = {"value": w.flops() * args.steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e_ms / args.steps,
+               "path": ("pinned host A,B,C -> HBM (every rank), plan execute, this rank's D rows -> "
+                        "pinned host; max over ranks")}
+
+    if rank != 0:
+        sampler.stop()
+        return
+
+    # a short same-kernel load tail (rank 0, local plan) so the sampler sees steady clocks
     t_end = time.perf_counter() + 1.0
     while time.perf_counter() < t_end:
         for _ in range(20):
-            step()
+            plan.execute(out, stream)
         torch.cuda.synchronize()
     clocks = sampler.stop()
 
-    # roofline of the dominant stage (CUDA events around each stage)
+    # roofline of the dominant stage of the single-GPU plan (CUDA events per stage)
     prof = []
     for _ in range(5):
         flush.fill_(2.0)
@@ -272,43 +335,10 @@ def run_ours(args, rank, world, dist):
     peak, peak_src = peaks()
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
     step_bytes = sum(b for _, b in stage_avg.values())
-    mean_ms = total_ms / args.steps
-
-    # end to end: pinned host inputs -> HBM, execute, D -> pinned host, every step
-    e2e = None
-    if not args.no_e2e:
-        host_in, dev_in = [], []
-        for t in [prob.a.row_ptr, prob.a.col_idx, prob.a.values, prob.c] + (
-                [prob.b] if prob.b_is_dense else [prob.b.row_ptr, prob.b.col_idx, prob.b.values]):
-            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            h.copy_(t)
-            host_in.append(h)
-            dev_in.append(t)
-        host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-        h2d = int(sum(h.numel() * h.element_size() for h in host_in))
-        d2h = int(host_out.numel() * host_out.element_size())
-        for _ in range(max(1, args.warmup)):
-            plan.execute_from_host(host_in, dev_in, out, host_out, stream)
-        torch.cuda.synchronize()
-        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        for k in range(args.steps):
-            ee[k][0].record(stream)
-            plan.execute_from_host(host_in, dev_in, out, host_out, stream)
-            ee[k][1].record(stream)
-        torch.cuda.synchronize()
-        e_ms = float(sum(a.elapsed_time(b) for a, b in ee))
-        if dist:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": world * w.flops() * args.steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e_ms / args.steps,
-               "path": "Plan.execute_from_host: pinned host A,B,C -> HBM, plan execute, D -> pinned host"}
+    single_ms = sum(v[0] for v in stage_avg.values())
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         times, kind, what, sched_s = cpu_reference_time(w, args, cores, 7, 1)
         med = float(np.median(times))
@@ -316,38 +346,40 @@ def run_ours(args, rank, world, dist):
                "sample": what + f"; median of {len(times)} runs after 1 warm-up",
                "ms_per_run": med * 1e3, "scheduler_seconds": sched_s}
 
-    if rank == 0:
-        value = world * w.flops() * args.steps / (total_ms * 1e-3) / 1e9
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64" if w.dtype == np.float64 else "f32",
-            "data": "synthetic (seeded generator with the BASELINE config's shape and distributions; "
-                    "SuiteSparse corpus not available)",
-            "config": {
-                "workload": f"{args.config}: {w.description}", "n": w.n, "nnz_a": w.a.nnz,
-                "b_cols": w.b_cols, "c_cols": w.c_cols, "flops_per_step": w.flops(),
-                "schedule": {**cfg.__dict__, "tile_size": sched.tile_size,
-                             "tiles": list(sched.num_tiles_per_wave),
-                             "fused_ratio": sched.fused_ratio(),
-                             "inspector_seconds_gpu": sched.inspect_seconds},
-                "spill_rows": plan.spill_rows, "bytes_min": w.bytes_min(),
-                "bytes_alg": w.bytes_alg(plan.spill_rows), "bytes_alg_stages": step_bytes,
-                "step_hbm_frac_of_peak": (step_bytes / (mean_ms * 1e-3) / 1e9) / peak,
-                "stages_ms": {k: v[0] for k, v in stage_avg.items()},
-                "l2": f"flushed between timed steps ({args.flush_mib} MiB write, outside the events)",
-                "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                         "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
-                         "peak_source": peak_src},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": plan.launches * args.steps,
-            "clocks": clocks,
-        }
-        print(json.dumps(line), flush=True)
+    parallelism = "single GPU"
+    if world > 1:
+        parallelism = (f"row-block partition x{world} at tile boundaries; D1 halo via one NCCL "
+                       f"all_to_all per step (rank-0 halo rows {dplan.halo_rows})")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if w.dtype == np.float64 else "f32",
+        "data": "synthetic (seeded generator with the BASELINE config's shape and distributions; "
+                "SuiteSparse corpus not available)",
+        "config": {
+            "workload": f"{args.config}: {w.description}", "n": w.n, "nnz_a": w.a.nnz,
+            "b_cols": w.b_cols, "c_cols": w.c_cols, "flops_per_step": w.flops(),
+            "schedule": {**cfg.__dict__, "tile_size": sched.tile_size,
+                         "tiles": list(sched.num_tiles_per_wave),
+                         "fused_ratio": sched.fused_ratio(),
+                         "inspector_seconds_gpu": sched.inspect_seconds},
+            "spill_rows": plan.spill_rows, "bytes_min": w.bytes_min(),
+            "bytes_alg": w.bytes_alg(plan.spill_rows), "bytes_alg_stages": step_bytes,
+            "step_hbm_frac_of_peak": (step_bytes / (single_ms * 1e-3) / 1e9) / peak,
+            "stages_ms": {k: v[0] for k, v in stage_avg.items()},
+            "l2": f"flushed between timed steps ({args.flush_mib} MiB write, outside the events)",
+            "parallelism": parallelism},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                     "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
 
 
 def main():

@@ -1267,7 +1267,7 @@ struct SpmmWork {
     const size_t row_bytes = (size_t)cc * elem;
     static const size_t budget = [] {
       const char* e = getenv("TFG_BAND_KB");
-      return (size_t)(e ? atoi(e) : 24) * 1024;
+      return (size_t)(e ? atoi(e) : 48) * 1024;
     }();
     int64_t nnz_total = (int64_t)rp[row0 + nrows] - rp[row0];
     if (nnz_total <= 0) return;
