@@ -527,6 +527,140 @@ __global__ void __launch_bounds__(256, 1)
   cp_async_wait<0>();
 }
 
+// Warp-specialised band SpMM: warp 8 is the producer (one lane issues the
+// TMA bulk copies of a block's X-row runs and index record, all lanes copy
+// the block's live CSR values into the stage), warps 0-7 consume.  Stages
+// form a ring guarded by full/empty mbarriers, so consumers never meet a
+// CTA-wide barrier and up to STAGES blocks are in flight per CTA.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <class T, int VEC, int LPR, int NCH, int STAGES>
+__global__ void __launch_bounds__(288, 1)
+    k_spmm_band2(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
+                 const T* __restrict__ av, const int* __restrict__ run_begin,
+                 const int* __restrict__ run_start, const int* __restrict__ run_len,
+                 const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
+                 int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
+                 T* __restrict__ out, int ldo) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int cc = ldx;
+  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
+  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
+  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
+  const size_t bufbytes = xbytes + ibytes + vbytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NCONS = 8;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCONS) {
+    // ---------------- producer ----------------
+    int it = 0;
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
+      unsigned char* base = smem_raw + (size_t)s * bufbytes;
+      T* xs = reinterpret_cast<T*>(base);
+      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
+      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
+      const int r_lo = row0 + b * R;
+      const int r_hi = min(r_lo + R, row0 + nrows);
+      const int k0 = __ldg(rp + r_lo), k1 = __ldg(rp + r_hi);
+      for (int k = k0 + lane; k < k1; k += 32) vs[k - k0] = __ldg(av + k);
+      __syncwarp();
+      if (lane == 0) {
+        const int rb = run_begin[b], re = run_begin[b + 1];
+        const int64_t i0 = idx_off[b], i1 = idx_off[b + 1];
+        unsigned total = (unsigned)((i1 - i0) * 2);
+        for (int q = rb; q < re; ++q) total += (unsigned)run_len[q] * cc * sizeof(T);
+        mbar_arrive_expect_tx(&full[s], total);  // also publishes the value stores
+        int off = 0;
+        for (int q = rb; q < re; ++q) {
+          const int len = run_len[q];
+          const char* src = reinterpret_cast<const char*>(X + (size_t)run_start[q] * cc);
+          char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
+          size_t left = (size_t)len * cc * sizeof(T);
+          while (left) {
+            const unsigned chunk = (unsigned)min(left, (size_t)32768);
+            bulk_g2s(dst, src, chunk, &full[s]);
+            dst += chunk;
+            src += chunk;
+            left -= chunk;
+          }
+          off += len;
+        }
+        if (i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &full[s]);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
+  int it = 0;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
+    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
+    const T* xs = reinterpret_cast<const T*>(base);
+    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
+    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
+    const int r_lo = row0 + b * R;
+    const int nr = min(R, row0 + nrows - r_lo);
+    const uint16_t* lrp = is;
+    const uint16_t* lsl = is + nr + 1;
+    for (int r = group; r < nr; r += ngroups) {
+      const int eb = lrp[r], ee = lrp[r + 1];
+      T acc[NCH][VEC];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+      for (int e0 = eb; e0 < ee; e0 += LPR) {
+        int sl = 0;
+        T a = T(0);
+        if (e0 + gl < ee) {
+          sl = lsl[e0 + gl];
+          a = vs[e0 + gl];
+        }
+        const int cnt = min(LPR, ee - e0);
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+          const int su = __shfl_sync(gmask, sl, u, LPR);
+          const T au = __shfl_sync(gmask, a, u, LPR);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            T x[VEC];
+            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+          }
+        }
+      }
+      T* o = out + (size_t)(r_lo + r) * ldo;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 // Generic SpMM (any column count): one warp per row, scalar columns.
 template <class T>
 __global__ void __launch_bounds__(256)
@@ -797,6 +931,30 @@ __device__ __forceinline__ void gemm_compute_chunk(int bc, int kc, int stg, cons
   const T* bs = smem + (size_t)stg * BM * G::B_LD;
   const T* cs = smem + (size_t)STAGES * BM * G::B_LD + (size_t)stg * BK * G::C_LD;
   const int kn = min(BK, bc - kc * BK);
+  if (kn == BK) {  // full chunk: compile-time trip counts, fully unrolled
+#pragma unroll
+    for (int k0 = 0; k0 < BK; k0 += V) {
+      T a[TM][V];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) ldv<T, V>(a[i], bs + (ty * TM + i) * G::B_LD + k0);
+#pragma unroll
+      for (int kk = 0; kk < V; ++kk) {
+        T b[TN];
+#pragma unroll
+        for (int j = 0; j < TN; j += V) {
+          T tmp[V];
+          ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + tx * TN + j);
+#pragma unroll
+          for (int q = 0; q < V; ++q) b[j + q] = tmp[q];
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fops<T>::fma(a[i][kk], b[j], acc[i][j]);
+      }
+    }
+    return;
+  }
   for (int k0 = 0; k0 < kn; k0 += V) {
     T a[TM][V];
 #pragma unroll
@@ -1516,6 +1674,30 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   if (w.banded) {
     constexpr int VEC = 16 / sizeof(T);
     const int L = cc / VEC;
+    static const int ws = [] {
+      const char* e = getenv("TFG_BAND_WS");
+      return e ? atoi(e) : 4;
+    }();
+#define TFG_BAND2(LPR, NCH, S)                                                               \
+  if (ws == S) {                                                                             \
+    auto kern = k_spmm_band2<T, VEC, LPR, NCH, S>;                                           \
+    const size_t smem = w.band_smem / 2 * S;                                                 \
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                  (int)smem));                                               \
+    int occ = 1;                                                                             \
+    TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 288, smem));          \
+    const int grid = (int)std::min<int64_t>(w.band_blocks, (int64_t)sm_count() * std::max(occ, 1)); \
+    kern<<<grid, 288, smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av,   \
+                                  w.run_begin.p, w.run_start.p, w.run_len.p, w.idx_off.p,    \
+                                  w.lidx.p, w.stage_cap, w.idx_cap, w.val_cap, X, cc, out, cc); \
+    TFG_LAUNCH_CHECK();                                                                      \
+    return;                                                                                  \
+  }
+    if (L == 8) { TFG_BAND2(8, 1, 2) TFG_BAND2(8, 1, 3) TFG_BAND2(8, 1, 4) }
+    if (L == 16) { TFG_BAND2(16, 1, 2) TFG_BAND2(16, 1, 3) TFG_BAND2(16, 1, 4) }
+    if (L == 32) { TFG_BAND2(32, 1, 2) TFG_BAND2(32, 1, 3) TFG_BAND2(32, 1, 4) }
+    if (L == 64) { TFG_BAND2(32, 2, 2) TFG_BAND2(32, 2, 3) TFG_BAND2(32, 2, 4) }
+#undef TFG_BAND2
 #define TFG_BAND(LPR, NCH)                                                                   \
   {                                                                                          \
     auto kern = k_spmm_band<T, VEC, LPR, NCH>;                                               \
@@ -1830,7 +2012,10 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         d2h(tc.data(), tcount.p, tc.size(), st);
         TFG_CUDA(cudaStreamSynchronize(st));
         const size_t gsm = fused_gemm_smem(pl);
-        const size_t cap_bytes = kFusedSmemMax > gsm ? kFusedSmemMax - gsm : 0;
+        // stage capacity: two CTAs per SM when the GEMM ring leaves room
+        const size_t per_cta = 2 * gsm + 16 * 1024 <= kFusedSmemMax ? kFusedSmemMax / 2 - 1024
+                                                                   : kFusedSmemMax;
+        const size_t cap_bytes = per_cta > gsm ? per_cta - gsm : 0;
         int max_need = 0;
         for (int c : tc) max_need = std::max(max_need, c);
         const int cap = (int)std::min<size_t>(cap_bytes / ((size_t)BN * pl.elem), (size_t)max_need);

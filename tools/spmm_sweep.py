@@ -30,8 +30,14 @@ def main():
     variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
     for v in variants:
         env = dict(os.environ)
+        if v.startswith("w"):  # w<stages>_<kb>: warp-specialised band kernel
+            st_, kb = v[1:].split("_")
+            env["TFG_BAND_WS"] = st_
+            env["TFG_BAND_KB"] = kb
+            v = "-1"
         if v.startswith("b"):
             env["TFG_BAND_KB"] = v[1:]
+            env["TFG_BAND_WS"] = "0"
             v = "-1"
         if v.startswith("n"):
             env["TFG_SPMM_BAND"] = "0"
