@@ -661,6 +661,177 @@ __global__ void __launch_bounds__(288, 1)
   }
 }
 
+// Band SpMM v3: warp-specialised like v2, but the producer never blocks on
+// data: values are cp.async'ed and tracked by the stage's mbarrier
+// (cp.async.mbarrier.arrive), block metadata is prefetched lane-parallel for
+// 32 blocks at a time, each run's TMA bulk copy is issued by its own lane.
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <class T, int VEC, int LPR, int NCH, int STAGES>
+__global__ void __launch_bounds__(288, 1)
+    k_spmm_band3(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
+                 const T* __restrict__ av, const int* __restrict__ run_begin,
+                 const int* __restrict__ run_start, const int* __restrict__ run_len,
+                 const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
+                 int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
+                 T* __restrict__ out, int ldo) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int cc = ldx;
+  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
+  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
+  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
+  const size_t bufbytes = xbytes + ibytes + vbytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NCONS = 8;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int nmine = blockIdx.x < nblk ? (nblk - 1 - blockIdx.x) / G + 1 : 0;
+  if (warp == NCONS) {
+    // ---------------- producer ----------------
+    int m_k0 = 0, m_k1 = 0, m_rb = 0, m_re = 0;
+    int64_t m_i0 = 0, m_i1 = 0;
+    auto load_meta = [&](int base) {
+      const int itl = base + lane;
+      if (itl < nmine) {
+        const int b = blockIdx.x + itl * G;
+        const int r_lo = row0 + b * R;
+        const int r_hi = min(r_lo + R, row0 + nrows);
+        m_k0 = __ldg(rp + r_lo);
+        m_k1 = __ldg(rp + r_hi);
+        m_rb = __ldg(run_begin + b);
+        m_re = __ldg(run_begin + b + 1);
+        m_i0 = __ldg(idx_off + b);
+        m_i1 = __ldg(idx_off + b + 1);
+      }
+    };
+    load_meta(0);
+    // runs of the current block: lane q holds run q
+    auto load_runs = [&](int it, int& rs, int& rl) {
+      const int rb = __shfl_sync(0xffffffffu, m_rb, it & 31);
+      const int re = __shfl_sync(0xffffffffu, m_re, it & 31);
+      rs = 0;
+      rl = 0;
+      if (rb + lane < re) {
+        rs = __ldg(run_start + rb + lane);
+        rl = __ldg(run_len + rb + lane);
+      }
+    };
+    int rs = 0, rl = 0;
+    if (nmine > 0) load_runs(0, rs, rl);
+    for (int it = 0; it < nmine; ++it) {
+      const int s = it % STAGES;
+      const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
+      const int k1 = __shfl_sync(0xffffffffu, m_k1, it & 31);
+      const int64_t i0 = __shfl_sync(0xffffffffu, m_i0, it & 31);
+      const int64_t i1 = __shfl_sync(0xffffffffu, m_i1, it & 31);
+      // offsets of this block's runs in the stage (exclusive warp scan)
+      int off = rl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += y;
+      }
+      const int total_rows = __shfl_sync(0xffffffffu, off, 31);
+      off -= rl;
+      const int my_rs = rs, my_rl = rl;
+      // prefetch the next block's metadata / runs while this one is issued
+      if (it + 1 < nmine) {
+        if (((it + 1) & 31) == 0) load_meta(it + 1);
+        load_runs(it + 1, rs, rl);
+      }
+      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
+      unsigned char* base = smem_raw + (size_t)s * bufbytes;
+      T* xs = reinterpret_cast<T*>(base);
+      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
+      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
+      for (int k = k0 + lane; k < k1; k += 32) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
+      cp_async_mbar_arrive(&full[s]);
+      __syncwarp();
+      if (lane == 0)
+        mbar_arrive_expect_tx(&full[s], (unsigned)((size_t)total_rows * cc * sizeof(T) +
+                                                   (size_t)(i1 - i0) * 2));
+      __syncwarp();
+      if (my_rl > 0) {
+        const char* src = reinterpret_cast<const char*>(X + (size_t)my_rs * cc);
+        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
+        size_t left = (size_t)my_rl * cc * sizeof(T);
+        while (left) {
+          const unsigned chunk = (unsigned)min(left, (size_t)32768);
+          bulk_g2s(dst, src, chunk, &full[s]);
+          dst += chunk;
+          src += chunk;
+          left -= chunk;
+        }
+      }
+      if (lane == 0 && i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &full[s]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
+  for (int it = 0; it < nmine; ++it) {
+    const int b = blockIdx.x + it * G;
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
+    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
+    const T* xs = reinterpret_cast<const T*>(base);
+    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
+    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
+    const int r_lo = row0 + b * R;
+    const int nr = min(R, row0 + nrows - r_lo);
+    const uint16_t* lrp = is;
+    const uint16_t* lsl = is + nr + 1;
+    for (int r = group; r < nr; r += ngroups) {
+      const int eb = lrp[r], ee = lrp[r + 1];
+      T acc[NCH][VEC];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+      for (int e0 = eb; e0 < ee; e0 += LPR) {
+        int sl = 0;
+        T a = T(0);
+        if (e0 + gl < ee) {
+          sl = lsl[e0 + gl];
+          a = vs[e0 + gl];
+        }
+        const int cnt = min(LPR, ee - e0);
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+          const int su = __shfl_sync(gmask, sl, u, LPR);
+          const T au = __shfl_sync(gmask, a, u, LPR);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            T x[VEC];
+            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+          }
+        }
+      }
+      T* o = out + (size_t)(r_lo + r) * ldo;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 // Generic SpMM (any column count): one warp per row, scalar columns.
 template <class T>
 __global__ void __launch_bounds__(256)
@@ -1678,9 +1849,13 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
       const char* e = getenv("TFG_BAND_WS");
       return e ? atoi(e) : 4;
     }();
+    static const int bv = [] {
+      const char* e = getenv("TFG_BAND_V");
+      return e ? atoi(e) : 3;
+    }();
 #define TFG_BAND2(LPR, NCH, S)                                                               \
   if (ws == S) {                                                                             \
-    auto kern = k_spmm_band2<T, VEC, LPR, NCH, S>;                                           \
+    auto kern = bv == 3 ? k_spmm_band3<T, VEC, LPR, NCH, S> : k_spmm_band2<T, VEC, LPR, NCH, S>; \
     const size_t smem = w.band_smem / 2 * S;                                                 \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                   (int)smem));                                               \

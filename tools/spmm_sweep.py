@@ -30,6 +30,9 @@ def main():
     variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
     for v in variants:
         env = dict(os.environ)
+        if v.startswith("v2"):
+            env["TFG_BAND_V"] = "2"
+            v = v[2:]
         if v.startswith("w"):  # w<stages>_<kb>: warp-specialised band kernel
             st_, kb = v[1:].split("_")
             env["TFG_BAND_WS"] = st_
