@@ -1594,10 +1594,22 @@ struct SpmmWork {
   void build_band(int row0, int64_t nrows, const std::vector<int>& rp,
                   const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st) {
     const size_t row_bytes = (size_t)cc * elem;
-    static const size_t budget = [] {
+    static const int env_kb = [] {
       const char* e = getenv("TFG_BAND_KB");
-      return (size_t)(e ? atoi(e) : 48) * 1024;
+      return e ? atoi(e) : 0;
     }();
+    // smallest stage budget that admits a band layout (more CTAs per SM)
+    for (int kb : {40, 64, 100}) {
+      const int use = env_kb > 0 ? env_kb : kb;
+      build_band_budget(row0, nrows, rp, ci, cc, elem, st, (size_t)use * 1024);
+      if (banded || env_kb > 0) return;
+    }
+  }
+
+  void build_band_budget(int row0, int64_t nrows, const std::vector<int>& rp,
+                         const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st,
+                         size_t budget) {
+    const size_t row_bytes = (size_t)cc * elem;
     int64_t nnz_total = (int64_t)rp[row0 + nrows] - rp[row0];
     if (nnz_total <= 0) return;
     for (int R : {256, 128, 64, 32, 16, 8, 4}) {
