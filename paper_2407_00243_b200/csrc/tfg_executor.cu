@@ -407,6 +407,7 @@ __device__ __forceinline__ void cp_async_small(void* smem, const void* gmem) {
 }
 
 constexpr int kBandRuns = 32;
+constexpr size_t kBandSmemMax = 200 * 1024;
 
 template <class T, int VEC, int LPR, int NCH>
 __global__ void __launch_bounds__(256, 1)
@@ -1671,6 +1672,11 @@ struct SpmmWork {
         io.push_back((int64_t)li.size());
       }
       if (!ok) continue;
+      {
+        const size_t buf = (size_t)scap * row_bytes + ((size_t)icap * 2 + 15) / 16 * 16 +
+                           ((size_t)vcap * elem + 15) / 16 * 16;
+        if (2 * buf > kBandSmemMax) continue;  // two stages must fit one CTA
+      }
       if ((double)staged_total > 0.5 * (double)nnz_total) return;  // not worth it
       banded = true;
       band_R = R;
@@ -1832,6 +1838,12 @@ struct SpmmWork {
     if (band_on && ci && identity && (cc % vec == 0) &&
         (cc / vec == 8 || cc / vec == 16 || cc / vec == 32 || cc / vec == 64))
       build_band(row0, n_short, rp, *ci, cc, elem, st);
+    if (getenv("TFG_DEBUG"))
+      fprintf(stderr,
+              "[tfg] spmm work: short=%lld long=%lld identity=%d skewed=%d banded=%d R=%d "
+              "blocks=%d stage_cap=%d smem=%zu ci=%d\n",
+              (long long)n_short, (long long)n_long, (int)identity, (int)skewed, (int)banded,
+              band_R, band_blocks, stage_cap, band_smem, ci ? 1 : 0);
     static const bool groups_on = [] {
       const char* e = getenv("TFG_SPMM_GROUPS");
       return e && atoi(e) > 0;
@@ -1927,8 +1939,18 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   const int row0 = w.identity ? w.row0 : 0;
   const int64_t n = w.n_short;
   constexpr int VEC = 16 / sizeof(T);
+  static const int skv = [] {
+    const char* e = getenv("TFG_SKEW_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  if (w.skewed)                                                                  \
+  if (w.skewed && skv == 1)                                                      \
+    k_spmm_strip<T, VEC, LPR, NCH, 8, 3, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
+  else if (w.skewed && skv == 2)                                                 \
+    k_spmm_strip<T, VEC, LPR, NCH, 8, 2, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
+  else if (w.skewed)                                                             \
     k_spmm_strip<T, VEC, LPR, NCH, 4, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
         n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
   else                                                                           \
