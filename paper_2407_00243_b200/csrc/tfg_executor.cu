@@ -1871,7 +1871,7 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     const int L = cc / VEC;
     static const int ws = [] {
       const char* e = getenv("TFG_BAND_WS");
-      return e ? atoi(e) : 4;
+      return e ? atoi(e) : 2;
     }();
     static const int bv = [] {
       const char* e = getenv("TFG_BAND_V");
