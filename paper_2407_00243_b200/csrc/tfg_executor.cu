@@ -407,6 +407,7 @@ __device__ __forceinline__ void cp_async_small(void* smem, const void* gmem) {
 }
 
 constexpr int kBandRuns = 32;
+constexpr int kBandMG = 4;  // rows per register-reuse mini-group
 constexpr size_t kBandSmemMax = 200 * 1024;
 
 template <class T, int VEC, int LPR, int NCH>
@@ -827,6 +828,205 @@ __global__ void __launch_bounds__(288, 1)
       T* o = out + (size_t)(r_lo + r) * ldo;
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+template <class T, int VEC, int LPR, int NCH, int STAGES>
+__global__ void __launch_bounds__(288, 1)
+    k_spmm_band4(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
+                 const T* __restrict__ av, const int* __restrict__ run_begin,
+                 const int* __restrict__ run_start, const int* __restrict__ run_len,
+                 const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
+                 int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
+                 T* __restrict__ out, int ldo) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int cc = ldx;
+  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
+  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
+  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
+  const size_t bufbytes = xbytes + ibytes + vbytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NCONS = 8;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int nmine = blockIdx.x < nblk ? (nblk - 1 - blockIdx.x) / G + 1 : 0;
+  if (warp == NCONS) {
+    // ---------------- producer ----------------
+    int m_k0 = 0, m_k1 = 0, m_rb = 0, m_re = 0;
+    int64_t m_i0 = 0, m_i1 = 0;
+    auto load_meta = [&](int base) {
+      const int itl = base + lane;
+      if (itl < nmine) {
+        const int b = blockIdx.x + itl * G;
+        const int r_lo = row0 + b * R;
+        const int r_hi = min(r_lo + R, row0 + nrows);
+        m_k0 = __ldg(rp + r_lo);
+        m_k1 = __ldg(rp + r_hi);
+        m_rb = __ldg(run_begin + b);
+        m_re = __ldg(run_begin + b + 1);
+        m_i0 = __ldg(idx_off + b);
+        m_i1 = __ldg(idx_off + b + 1);
+      }
+    };
+    load_meta(0);
+    // runs of the current block: lane q holds run q
+    auto load_runs = [&](int it, int& rs, int& rl) {
+      const int rb = __shfl_sync(0xffffffffu, m_rb, it & 31);
+      const int re = __shfl_sync(0xffffffffu, m_re, it & 31);
+      rs = 0;
+      rl = 0;
+      if (rb + lane < re) {
+        rs = __ldg(run_start + rb + lane);
+        rl = __ldg(run_len + rb + lane);
+      }
+    };
+    int rs = 0, rl = 0;
+    if (nmine > 0) load_runs(0, rs, rl);
+    for (int it = 0; it < nmine; ++it) {
+      const int s = it % STAGES;
+      const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
+      const int k1 = __shfl_sync(0xffffffffu, m_k1, it & 31);
+      const int64_t i0 = __shfl_sync(0xffffffffu, m_i0, it & 31);
+      const int64_t i1 = __shfl_sync(0xffffffffu, m_i1, it & 31);
+      // offsets of this block's runs in the stage (exclusive warp scan)
+      int off = rl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += y;
+      }
+      const int total_rows = __shfl_sync(0xffffffffu, off, 31);
+      off -= rl;
+      const int my_rs = rs, my_rl = rl;
+      // prefetch the next block's metadata / runs while this one is issued
+      if (it + 1 < nmine) {
+        if (((it + 1) & 31) == 0) load_meta(it + 1);
+        load_runs(it + 1, rs, rl);
+      }
+      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
+      unsigned char* base = smem_raw + (size_t)s * bufbytes;
+      T* xs = reinterpret_cast<T*>(base);
+      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
+      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
+      for (int k = k0 + lane; k < k1; k += 32) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
+      cp_async_mbar_arrive(&full[s]);
+      __syncwarp();
+      if (lane == 0)
+        mbar_arrive_expect_tx(&full[s], (unsigned)((size_t)total_rows * cc * sizeof(T) +
+                                                   (size_t)(i1 - i0) * 2));
+      __syncwarp();
+      if (my_rl > 0) {
+        const char* src = reinterpret_cast<const char*>(X + (size_t)my_rs * cc);
+        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
+        size_t left = (size_t)my_rl * cc * sizeof(T);
+        while (left) {
+          const unsigned chunk = (unsigned)min(left, (size_t)32768);
+          bulk_g2s(dst, src, chunk, &full[s]);
+          dst += chunk;
+          src += chunk;
+          left -= chunk;
+        }
+      }
+      if (lane == 0 && i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &full[s]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+  // ---------------- consumers: mini-groups of kBandMG rows -----------------
+  // Each warp takes a mini-group of consecutive rows and walks the group's
+  // ascending union of stage slots: every staged X row is read from shared
+  // memory once per mini-group and added into the accumulators of the rows
+  // in its mask.  Each row still sums its terms in ascending column order
+  // with its own values in CSR order (bit-identical to the reference).
+  static_assert(LPR == 32, "band4 uses full warps per mini-group");
+  constexpr int MG = kBandMG;
+  for (int it = 0; it < nmine; ++it) {
+    const int b = blockIdx.x + it * G;
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
+    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
+    const T* xs = reinterpret_cast<const T*>(base);
+    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
+    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
+    const int r_lo = row0 + b * R;
+    const int nr = min(R, row0 + nrows - r_lo);
+    const uint16_t* lrp = is;
+    const int nnz_b = lrp[nr];
+    const int nmg = (nr + MG - 1) / MG;
+    const uint16_t* mgoff = is + nr + 1 + nnz_b;
+    const uint16_t* uent = mgoff + nmg + 1;
+    for (int m = warp; m < nmg; m += NCONS) {
+      const int r0 = m * MG;
+      const int nrg = min(MG, nr - r0);
+      const int vb = lrp[r0], ve = lrp[r0 + nrg];
+      T v0 = vb + lane < ve ? vs[vb + lane] : T(0);
+      T v1 = vb + 32 + lane < ve ? vs[vb + 32 + lane] : T(0);
+      T v2 = vb + 64 + lane < ve ? vs[vb + 64 + lane] : T(0);
+      T v3 = vb + 96 + lane < ve ? vs[vb + 96 + lane] : T(0);
+      const bool regs = ve - vb <= 128;
+      int p[MG];
+#pragma unroll
+      for (int r = 0; r < MG; ++r) p[r] = r < nrg ? lrp[r0 + r] - vb : 0;
+      T acc[MG][NCH][VEC];
+#pragma unroll
+      for (int r = 0; r < MG; ++r)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[r][ch][v] = T(0);
+      const int ub = mgoff[m], ue = mgoff[m + 1];
+      for (int u0 = ub; u0 < ue; u0 += 32) {
+        const int ent = u0 + lane < ue ? uent[u0 + lane] : 0;
+        const int cnt = min(32, ue - u0);
+        for (int u = 0; u < cnt; ++u) {
+          const int e = __shfl_sync(0xffffffffu, ent, u);
+          const int slot = e >> 4, mask = e & 15;
+          T x[NCH][VEC];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+            ldv<T, VEC>(x[ch], xs + (size_t)slot * cc + (ch * 32 + lane) * VEC);
+#pragma unroll
+          for (int r = 0; r < MG; ++r) {
+            if (mask & (1 << r)) {
+              const int idx = p[r]++;
+              T a;
+              if (regs) {
+                T src = v0;
+                if (idx >= 32) src = v1;
+                if (idx >= 64) src = v2;
+                if (idx >= 96) src = v3;
+                a = __shfl_sync(0xffffffffu, src, idx & 31);
+              } else {
+                a = vs[vb + idx];
+              }
+#pragma unroll
+              for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v)
+                  acc[r][ch][v] = fops<T>::add(acc[r][ch][v], fops<T>::mul(a, x[ch][v]));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < MG; ++r) {
+        if (r < nrg) {
+          T* o = out + (size_t)(r_lo + r0 + r) * ldo;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * 32 + lane) * VEC, acc[r][ch]);
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -1584,6 +1784,7 @@ struct SpmmWork {
   bool skewed = false;  // row lengths vary a lot: one row per lane group
   // band-staged layout (k_spmm_band)
   bool banded = false;
+  bool band_union = false;  // records carry mini-group unions (k_spmm_band4)
   int band_R = 0, band_blocks = 0, stage_cap = 0, idx_cap = 0, val_cap = 0;
   size_t band_smem = 0;
   dbuf<int> run_begin, run_start, run_len;
@@ -1611,6 +1812,13 @@ struct SpmmWork {
                          const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st,
                          size_t budget) {
     const size_t row_bytes = (size_t)cc * elem;
+    static const bool union_on = [] {
+      const char* e = getenv("TFG_BAND_UNION");
+      return !e || atoi(e) > 0;
+    }();
+    const int L = cc / (16 / (int)elem);
+    const bool use_union = union_on && (L == 32 || L == 64);
+    band_union = use_union;
     int64_t nnz_total = (int64_t)rp[row0 + nrows] - rp[row0];
     if (nnz_total <= 0) return;
     for (int R : {256, 128, 64, 32, 16, 8, 4}) {
@@ -1639,10 +1847,51 @@ struct SpmmWork {
         int staged = 0;
         for (auto& r : runs) staged += r.second;
         const int nr = r_hi - r_lo;
-        const int irec = ((nr + 1 + (k1 - k0)) + 7) / 8 * 8;
+        // slots of every entry (runs are in ascending column order, so slot
+        // order == column order)
+        std::vector<int> run_off;
+        {
+          int off = 0;
+          for (auto& r : runs) {
+            run_off.push_back(off);
+            off += r.second;
+          }
+        }
+        std::vector<int> slots(k1 - k0);
+        for (int k = k0; k < k1; ++k) {
+          const int c = ci[k];
+          size_t q = std::upper_bound(runs.begin(), runs.end(), std::make_pair(c, INT32_MAX)) -
+                     runs.begin() - 1;
+          slots[k - k0] = run_off[q] + (c - runs[q].first);
+        }
+        // mini-groups of kBandMG consecutive rows: ascending union of their
+        // slots with a row mask (the register-reuse consumer)
+        std::vector<int> mgoff{0}, uent;
+        if (use_union) {
+          std::vector<std::pair<int, int>> tmp;
+          for (int m0 = 0; m0 < nr; m0 += kBandMG) {
+            tmp.clear();
+            for (int r = m0; r < std::min(nr, m0 + kBandMG); ++r)
+              for (int k = rp[r_lo + r]; k < rp[r_lo + r + 1]; ++k)
+                tmp.emplace_back(slots[k - k0], r - m0);
+            std::sort(tmp.begin(), tmp.end());
+            for (size_t q = 0; q < tmp.size();) {
+              size_t e = q;
+              int mask = 0;
+              while (e < tmp.size() && tmp[e].first == tmp[q].first) mask |= 1 << tmp[e++].second;
+              uent.push_back((tmp[q].first << 4) | mask);
+              q = e;
+            }
+            mgoff.push_back((int)uent.size());
+          }
+        }
+        const int nmg = (nr + kBandMG - 1) / kBandMG;
+        const int irec = ((nr + 1 + (k1 - k0) + (use_union ? nmg + 1 + (int)uent.size() : 0)) + 7) /
+                         8 * 8;
         const size_t need = (size_t)staged * row_bytes + (size_t)irec * 2 +
                             ((size_t)(k1 - k0) * elem + 15) / 16 * 16;
-        if ((int)runs.size() > kBandRuns || staged > 65535 || need > budget) {
+        if ((int)runs.size() > kBandRuns || staged > (use_union ? 4095 : 65535) || need > budget ||
+            (int)uent.size() > 65535) {
           ok = false;
           break;
         }
@@ -1650,23 +1899,18 @@ struct SpmmWork {
         icap = std::max(icap, irec);
         vcap = std::max(vcap, k1 - k0);
         staged_total += staged;
-        // local index record: row offsets then slots
-        int off = 0;
-        std::vector<int> run_off;
         for (auto& r : runs) {
           rs.push_back(r.first);
           rl.push_back(r.second);
-          run_off.push_back(off);
-          off += r.second;
         }
         rb.push_back((int)rs.size());
+        // index record: row offsets, slots, [mini-group offsets, union entries]
         const size_t rec0 = li.size();
         for (int r = r_lo; r <= r_hi; ++r) li.push_back(rp[r] - k0);
-        for (int k = k0; k < k1; ++k) {
-          const int c = ci[k];
-          size_t q = std::upper_bound(runs.begin(), runs.end(), std::make_pair(c, INT32_MAX)) -
-                     runs.begin() - 1;
-          li.push_back(run_off[q] + (c - runs[q].first));
+        for (int v : slots) li.push_back(v);
+        if (use_union) {
+          for (int v : mgoff) li.push_back(v);
+          for (int v : uent) li.push_back(v);
         }
         while ((li.size() - rec0) % 8) li.push_back(0);
         io.push_back((int64_t)li.size());
@@ -1880,6 +2124,8 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
 #define TFG_BAND2(LPR, NCH, S)                                                               \
   if (ws == S) {                                                                             \
     auto kern = bv == 3 ? k_spmm_band3<T, VEC, LPR, NCH, S> : k_spmm_band2<T, VEC, LPR, NCH, S>; \
+    if constexpr (LPR == 32)                                                                 \
+      if (w.band_union) kern = k_spmm_band4<T, VEC, LPR, NCH, S>;                            \
     const size_t smem = w.band_smem / 2 * S;                                                 \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                   (int)smem));                                               \
