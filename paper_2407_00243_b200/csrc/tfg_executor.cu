@@ -970,11 +970,7 @@ __global__ void __launch_bounds__(288, 1)
       const int r0 = m * MG;
       const int nrg = min(MG, nr - r0);
       const int vb = lrp[r0], ve = lrp[r0 + nrg];
-      T v0 = vb + lane < ve ? vs[vb + lane] : T(0);
-      T v1 = vb + 32 + lane < ve ? vs[vb + 32 + lane] : T(0);
-      T v2 = vb + 64 + lane < ve ? vs[vb + 64 + lane] : T(0);
-      T v3 = vb + 96 + lane < ve ? vs[vb + 96 + lane] : T(0);
-      const bool regs = ve - vb <= 128;
+      (void)ve;
       int p[MG];
 #pragma unroll
       for (int r = 0; r < MG; ++r) p[r] = r < nrg ? lrp[r0 + r] - vb : 0;
@@ -1000,16 +996,7 @@ __global__ void __launch_bounds__(288, 1)
           for (int r = 0; r < MG; ++r) {
             if (mask & (1 << r)) {
               const int idx = p[r]++;
-              T a;
-              if (regs) {
-                T src = v0;
-                if (idx >= 32) src = v1;
-                if (idx >= 64) src = v2;
-                if (idx >= 96) src = v3;
-                a = __shfl_sync(0xffffffffu, src, idx & 31);
-              } else {
-                a = vs[vb + idx];
-              }
+              const T a = vs[vb + idx];  // shared-memory broadcast
 #pragma unroll
               for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
@@ -2125,7 +2112,7 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   if (ws == S) {                                                                             \
     auto kern = bv == 3 ? k_spmm_band3<T, VEC, LPR, NCH, S> : k_spmm_band2<T, VEC, LPR, NCH, S>; \
     if constexpr (LPR == 32)                                                                 \
-      if (w.band_union) kern = k_spmm_band4<T, VEC, LPR, NCH, S>;                            \
+      if (w.band_union && w.band_R >= 8 * kBandMG) kern = k_spmm_band4<T, VEC, LPR, NCH, S>;  \
     const size_t smem = w.band_smem / 2 * S;                                                 \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                   (int)smem));                                               \
