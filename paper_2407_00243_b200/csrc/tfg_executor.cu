@@ -1800,8 +1800,8 @@ struct SpmmWork {
                          size_t budget) {
     const size_t row_bytes = (size_t)cc * elem;
     static const bool union_on = [] {
-      const char* e = getenv("TFG_BAND_UNION");
-      return !e || atoi(e) > 0;
+      const char* e = getenv("TFG_BAND_UNION");  // opt-in: measured slower than band3
+      return e && atoi(e) > 0;
     }();
     const int L = cc / (16 / (int)elem);
     const bool use_union = union_on && (L == 32 || L == 64);

@@ -1,0 +1,116 @@
+"""Edge cases the reference's tests exercise (empty rows, n = 1, dense rows,
+width-1 tiles, schedules imported from the reference inspector) on the GPU."""
+import numpy as np
+import pytest
+
+import paper_2407_00243_b200 as P
+from helpers import TOL, golden_cfg, golden_sched, load, max_rel_err, to_product_cfg
+from oracle.oracle import SchedulerConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reference_schedules_execute_bit_exact(cuda, oracle):
+    """Golden schedules built by the reference inspector, imported into
+    libtfg and executed: SpMM-SpMM bit-identical to the oracle."""
+    z = load("schedules.npz")
+    rng = np.random.default_rng(3)
+    for key in list(z["keys"])[:40]:
+        rp, ci = z[f"{key}/row_ptr"], z[f"{key}/col_idx"]
+        n = rp.size - 1
+        v = rng.uniform(-1, 1, ci.size)
+        c = rng.uniform(-1, 1, (n, 8))
+        flat = golden_sched(z, key)
+        s = P.import_schedule(flat)
+        a = P.Csr(n, n, rp, ci, v)
+        got = P.run(a, a, c, s)
+        want = oracle.run(n, (rp, ci, v), (rp, ci, v, n), c, flat)
+        assert np.array_equal(got, want), key
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_degenerate_shapes(cuda, oracle, dt):
+    size = np.dtype(dt).itemsize
+    # n = 1
+    a = P.Csr(1, 1, [0, 1], [0], [2.0])
+    d = P.fused_gemm_spmm(a, np.array([[3.0]]), np.array([[4.0, 5.0]]), dtype=dt)
+    assert d.tolist() == [[24.0, 30.0]]
+    # all rows empty
+    a = P.Csr(50, 50, np.zeros(51, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    b = np.ones((50, 3))
+    c = np.ones((3, 4))
+    assert not P.fused_gemm_spmm(a, b, c, dtype=dt).any()
+    s = P.build_schedule(a, P.SchedulerConfig(ct_size=8, num_workers=3))
+    assert s.fused_ratio() == 0.5  # every empty row fuses into its own tile
+    # half the rows empty, SpMM-SpMM, odd column count (generic kernels)
+    rng = np.random.default_rng(1)
+    n = 301
+    rows = [np.sort(rng.choice(n, rng.integers(1, 9), replace=False)) if i % 2 else np.zeros(0, int)
+            for i in range(n)]
+    rp = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int32)
+    ci = np.concatenate(rows).astype(np.int32)
+    v = rng.uniform(-1, 1, ci.size)
+    a = P.Csr(n, n, rp, ci, v)
+    c = rng.uniform(-1, 1, (n, 7))
+    cfg = SchedulerConfig(ct_size=16, num_workers=5, cache_size_words=300, b_is_dense=False)
+    osched = oracle.build_schedule(n, n, rp, ci, cfg)
+    want = oracle.run(n, (rp, ci, v), (rp, ci, v, n), c, osched, dt)
+    got = P.run(a.astype(dt), a.astype(dt), c.astype(dt), P.build_schedule(a, to_product_cfg(cfg)), dt)
+    assert np.array_equal(got, want)
+    assert max_rel_err(got, want) <= TOL[size]
+
+
+def test_dense_and_long_rows_spmm_spmm(cuda, oracle):
+    """A dense 6000-wide row (segmented path) next to banded rows, B = A."""
+    n = 6000
+    rng = np.random.default_rng(2)
+    rows = [np.arange(n)] + [np.arange(max(0, i - 2), min(n, i + 3)) for i in range(1, n)]
+    rp = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int32)
+    ci = np.concatenate(rows).astype(np.int32)
+    v = rng.uniform(-1, 1, ci.size)
+    a = P.Csr(n, n, rp, ci, v)
+    c = rng.uniform(-1, 1, (n, 64))
+    for ct, budget in [(2048, 163840), (512, 10 ** 12)]:
+        cfg = SchedulerConfig(ct_size=ct, num_workers=16, cache_size_words=budget, b_is_dense=False,
+                              c_cols=64, b_cols=n)
+        osched = oracle.build_schedule(n, n, rp, ci, cfg)
+        want = oracle.run(n, (rp, ci, v), (rp, ci, v, n), c, osched)
+        got = P.run(a, a, c, P.build_schedule(a, to_product_cfg(cfg)))
+        assert max_rel_err(got, want) <= 1e-12
+        # rows shorter than the segmentation threshold are bit-exact
+        assert np.array_equal(got[1:], want[1:])
+
+
+def test_width_one_tiles_and_tiny_budget(cuda, oracle):
+    rp, ci, v = oracle.gen_random_sparse(400, 0.05, 17)
+    cfg = SchedulerConfig(ct_size=64, num_workers=8, cache_size_words=1, b_cols=4, c_cols=4)
+    osched = oracle.build_schedule(400, 400, rp, ci, cfg)
+    a = P.Csr(400, 400, rp, ci, v)
+    s = P.build_schedule(a, to_product_cfg(cfg))
+    from helpers import schedules_equal
+
+    assert schedules_equal(s.export(), osched)
+    rng = np.random.default_rng(0)
+    b, c = rng.uniform(-1, 1, (400, 4)), rng.uniform(-1, 1, (4, 4))
+    want = oracle.run(400, (rp, ci, v), b, c, osched)
+    assert max_rel_err(P.run(a, b, c, s), want) <= 1e-12
+
+
+def test_plan_reuse_with_new_values(cuda, oracle):
+    """A plan reads the live CSR values: updating A's values in place (same
+    pattern) and re-executing gives the new product."""
+    import torch
+
+    rp, ci, v = oracle.gen_banded(3000, 4)
+    a = P.Csr(3000, 3000, rp, ci, v)
+    rng = np.random.default_rng(5)
+    c = rng.uniform(-1, 1, (3000, 64))
+    prob = P.DeviceProblem(a, a, c)
+    plan = P.Plan(prob, P.build_schedule(a, P.SchedulerConfig(b_is_dense=False, c_cols=64)))
+    d0 = plan.execute().cpu().numpy()
+    v2 = rng.uniform(-1, 1, v.size)
+    prob.a.values.copy_(torch.from_numpy(v2))
+    prob.b.values.copy_(torch.from_numpy(v2))
+    d1 = plan.execute().cpu().numpy()
+    want = oracle.run(3000, (rp, ci, v2), (rp, ci, v2, 3000), c, None)
+    assert np.array_equal(d1, want) and not np.array_equal(d0, d1)
