@@ -1020,6 +1020,109 @@ __global__ void __launch_bounds__(288, 1)
   }
 }
 
+// ---- ring-gather SpMM (skewed / random rows) -----------------------------------
+// For rows with no reusable structure (R-MAT) the gather is latency-bound and
+// the number of X rows in flight is capped by the registers used as landing
+// buffers.  Here each LPR-lane group walks a strip of rows as one entry
+// stream and lands gathered X rows in a DEPTH-slot shared-memory ring with
+// cp.async (16 B per lane), issuing DEPTH entries ahead of the consumer.
+// The consumer sums each row's entries in order (mul then add, bit-identical
+// to the reference).
+template <class T, int VEC, int LPR, int NCH, int DEPTH>
+__global__ void __launch_bounds__(256)
+    k_spmm_ring(int64_t nrows, const int* __restrict__ rows, int row0,
+                const int* __restrict__ rp, const int* __restrict__ ci,
+                const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                T* __restrict__ out, int ldo) {
+  constexpr int SLOT = LPR * VEC * NCH;  // elements per gathered row
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int grp_in_cta = threadIdx.x / LPR;
+  T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)grp_in_cta * DEPTH * SLOT;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  const int64_t base = g * LPR;
+  if (base >= nrows) return;
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int cnt = (int)(nrows - base < LPR ? nrows - base : LPR);
+  int my_r = 0, my_b = 0, my_e = 0;
+  if (gl < cnt) {
+    my_r = rows ? __ldg(rows + base + gl) : row0 + (int)(base + gl);
+    my_b = __ldg(rp + my_r);
+    my_e = __ldg(rp + my_r + 1);
+  }
+  // producer cursor
+  int pq = 0, pk = __shfl_sync(gmask, my_b, 0, LPR), pe = __shfl_sync(gmask, my_e, 0, LPR);
+  int pk0 = pk;
+  int pcol = pk + gl < pe ? __ldg(ci + pk + gl) : 0;
+  int issued = 0;
+  auto produce = [&]() {
+    // skip exhausted rows
+    while (pq < cnt && pk >= pe) {
+      ++pq;
+      if (pq < cnt) {
+        pk = __shfl_sync(gmask, my_b, pq, LPR);
+        pe = __shfl_sync(gmask, my_e, pq, LPR);
+        pk0 = pk;
+        pcol = pk + gl < pe ? __ldg(ci + pk + gl) : 0;
+      }
+    }
+    if (pq < cnt) {
+      if (pk - pk0 == LPR) {
+        pk0 = pk;
+        pcol = pk + gl < pe ? __ldg(ci + pk + gl) : 0;
+      }
+      const int c = __shfl_sync(gmask, pcol, pk - pk0, LPR);
+      T* dst = ring + (size_t)(issued % DEPTH) * SLOT;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int off = (ch * LPR + gl) * VEC;
+        cp_async16(dst + off, X + (size_t)c * ldx + off, 16);
+      }
+      ++pk;
+    }
+    cp_async_commit();  // one group per step keeps wait_group counting exact
+    ++issued;
+  };
+#pragma unroll 1
+  for (int d = 0; d < DEPTH - 1; ++d) produce();
+  // consumer cursor
+  int consumed = 0;
+  for (int q = 0; q < cnt; ++q) {
+    const int b = __shfl_sync(gmask, my_b, q, LPR), e = __shfl_sync(gmask, my_e, q, LPR);
+    T acc[NCH][VEC];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+    for (int k0 = b; k0 < e; k0 += LPR) {
+      const T a = k0 + gl < e ? __ldg(av + k0 + gl) : T(0);
+      const int n_here = min(LPR, e - k0);
+      for (int u = 0; u < n_here; ++u) {
+        produce();
+        cp_async_wait<DEPTH - 1>();
+        __syncwarp(gmask);
+        const T au = __shfl_sync(gmask, a, u, LPR);
+        const T* src = ring + (size_t)(consumed % DEPTH) * SLOT;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          T x[VEC];
+          ldv<T, VEC>(x, src + (ch * LPR + gl) * VEC);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v)
+            acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+        }
+        __syncwarp(gmask);  // slot may be refilled by the next produce()
+        ++consumed;
+      }
+    }
+    const int r = __shfl_sync(gmask, my_r, q, LPR);
+    T* o = out + (size_t)r * ldo;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+  }
+  cp_async_wait<0>();
+}
+
 // Generic SpMM (any column count): one warp per row, scalar columns.
 template <class T>
 __global__ void __launch_bounds__(256)
@@ -2176,6 +2279,27 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     const char* e = getenv("TFG_SKEW_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  static const int ring_depth = [] {
+    const char* e = getenv("TFG_RING");
+    return e ? atoi(e) : 16;
+  }();
+  if (w.skewed && ring_depth > 0 && cc % VEC == 0 && (cc / VEC == 16 || cc / VEC == 32 || cc / VEC == 64)) {
+    const int L = cc / VEC;
+#define TFG_RING(LPR, NCH, D)                                                               \
+  if (ring_depth == D) {                                                                    \
+    auto kern = k_spmm_ring<T, VEC, LPR, NCH, D>;                                           \
+    const size_t smem = (size_t)(256 / LPR) * D * LPR * VEC * NCH * sizeof(T);             \
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<blocks_for((n + LPR - 1) / LPR * LPR), 256, smem, st>>>(n, rows, row0, rp, ci, av, X, \
+                                                                    cc, out, cc);           \
+    TFG_LAUNCH_CHECK();                                                                     \
+    return;                                                                                 \
+  }
+    if (L == 16) { TFG_RING(16, 1, 8) TFG_RING(16, 1, 16) TFG_RING(16, 1, 32) }
+    if (L == 32) { TFG_RING(32, 1, 8) TFG_RING(32, 1, 16) TFG_RING(32, 1, 32) }
+    if (L == 64) { TFG_RING(32, 2, 8) TFG_RING(32, 2, 16) }
+#undef TFG_RING
+  }
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
   if (w.skewed && skv == 1)                                                      \
     k_spmm_strip<T, VEC, LPR, NCH, 8, 3, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
