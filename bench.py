@@ -276,39 +276,14 @@ def run_ours(args, rank, world, dist):
                               "ms_per_step": mean_ms, "value": value}))
         return
 
-    # end to end: pinned host A,B,C -> HBM, execute, D -> pinned host, every step
+    # end to end: pinned host A,B,C -> HBM, execute, D -> pinned host, every step.
+    # Steps are pipelined over two device input/output buffer sets and three
+    # streams (H2D | compute | D2H), so step k+1's upload overlaps step k's
+    # download (PCIe is full duplex); every step still moves all its inputs
+    # and its result across PCIe inside the timed region.
     e2e = None
     if not args.no_e2e:
-        host_in, dev_in = [], []
-        for t in [prob.a.row_ptr, prob.a.col_idx, prob.a.values, prob.c] + (
-                [prob.b] if prob.b_is_dense else [prob.b.row_ptr, prob.b.col_idx, prob.b.values]):
-            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            h.copy_(t)
-            host_in.append(h)
-            dev_in.append(t)
-        if world > 1:
-            from paper_2407_00243_b200 import distributed as PD
-
-            own = torch.as_tensor(PD.owned_output_rows(sched.export(), bounds, rank), device=dev)
-        else:
-            own = None
-        nout = w.n if own is None else int(own.numel())
-        host_out = torch.empty((nout, w.c_cols), dtype=out.dtype, pin_memory=True)
-        h2d = int(sum(h.numel() * h.element_size() for h in host_in))
-        d2h = int(host_out.numel() * host_out.element_size())
-
-        def e2e_step():
-            for h, d in zip(host_in, dev_in):
-                d.copy_(h, non_blocking=True)
-            step()
-            host_out.copy_(out if own is None else out.index_select(0, own), non_blocking=True)
-
-        e_ms = timed_loop(e2e_step, flush_between=False)
-        e2e = {"value": w.flops() * args.steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e_ms / args.steps,
-               "path": ("pinned host A,B,C -> HBM (every rank), plan execute, this rank's D rows -> "
-                        "pinned host; max over ranks")}
+        e2e = _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan)
 
     if rank != 0:
         sampler.stop()
@@ -389,6 +364,79 @@ def run_ours(args, rank, world, dist):
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan):
+    import torch
+
+    import paper_2407_00243_b200 as P
+
+    sets = [prob, prob.clone()]
+    host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in prob.device_inputs()]
+    if world > 1:
+        from paper_2407_00243_b200 import distributed as PD
+
+        own = torch.as_tensor(PD.owned_output_rows(sched.export(), bounds, rank), device=dev)
+        flat = sched.export()
+        engines = [dplan.engine, PD.GpuEngine(sets[1], sched, *bounds[rank])]
+        dplans = [dplan, PD.DistributedPlan(engines[1], dplan.halo, dist, w.c_cols)]
+        execs = [lambda o, i=i: dplans[i].execute(o) for i in range(2)]
+        del flat
+    else:
+        own = None
+        plans = [plan, P.Plan(sets[1], sched)]
+        execs = [lambda o, i=i: plans[i].execute(o, torch.cuda.current_stream()) for i in range(2)]
+    outs = [out, torch.empty_like(out)]
+    nout = w.n if own is None else int(own.numel())
+    host_out = [torch.empty((nout, w.c_cols), dtype=out.dtype, pin_memory=True) for _ in range(2)]
+    h2d = int(sum(h.numel() * h.element_size() for h in host_in))
+    d2h = int(host_out[0].numel() * host_out[0].element_size())
+    s_h, s_c, s_d = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev_h = [torch.cuda.Event() for _ in range(2)]
+    ev_c = [torch.cuda.Event() for _ in range(2)]
+    ev_d = [torch.cuda.Event() for _ in range(2)]
+
+    def run(nsteps):
+        for k in range(nsteps):
+            b = k & 1
+            with torch.cuda.stream(s_h):
+                if k >= 2:
+                    s_h.wait_event(ev_c[b])  # inputs of step k-2 consumed
+                for hsrc, ddst in zip(host_in, sets[b].device_inputs()):
+                    ddst.copy_(hsrc, non_blocking=True)
+                ev_h[b].record(s_h)
+            with torch.cuda.stream(s_c):
+                s_c.wait_event(ev_h[b])
+                if k >= 2:
+                    s_c.wait_event(ev_d[b])  # output buffer of step k-2 drained
+                execs[b](outs[b])
+                ev_c[b].record(s_c)
+            with torch.cuda.stream(s_d):
+                s_d.wait_event(ev_c[b])
+                src = outs[b] if own is None else outs[b].index_select(0, own)
+                host_out[b].copy_(src, non_blocking=True)
+                ev_d[b].record(s_d)
+
+    run(max(2, args.warmup))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(s_h)
+    run(args.steps)
+    s_h.wait_stream(s_d)
+    t1.record(s_h)
+    torch.cuda.synchronize()
+    e_ms = t0.elapsed_time(t1)
+    if dist:
+        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    return {"value": w.flops() * args.steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / args.steps,
+            "path": ("pinned host A, B (aliased when B is A), C -> HBM, plan execute, D -> pinned host, "
+                     "every step; steps pipelined over two buffer sets and H2D/compute/D2H streams; "
+                     "max over ranks")}
 
 
 def main():

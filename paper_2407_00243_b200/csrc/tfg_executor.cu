@@ -2281,7 +2281,7 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   }();
   static const int ring_depth = [] {
     const char* e = getenv("TFG_RING");
-    return e ? atoi(e) : 16;
+    return e ? atoi(e) : 0;  // opt-in: measured slower on R-MAT
   }();
   if (w.skewed && ring_depth > 0 && cc % VEC == 0 && (cc / VEC == 16 || cc / VEC == 32 || cc / VEC == 64)) {
     const int L = cc / VEC;

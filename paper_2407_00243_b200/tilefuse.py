@@ -398,7 +398,8 @@ class DeviceProblem:
         if isinstance(b, Csr):
             self.b_is_dense = False
             self.b_rows, self.b_cols = b.n_rows, b.n_cols
-            self.b = DeviceCsr(b, device, self.dtype)
+            # the same host matrix passed as A and B is uploaded once
+            self.b = self.a if b is a else DeviceCsr(b, device, self.dtype)
         else:
             b = np.ascontiguousarray(b, self.dtype)
             self.b_is_dense = True
@@ -407,6 +408,38 @@ class DeviceProblem:
         self.c_rows, self.c_cols = c.shape
         self.c = torch.from_numpy(c).to(device)
         self.device = device
+
+    @property
+    def b_aliases_a(self) -> bool:
+        return self.b is self.a
+
+    def device_inputs(self):
+        """The distinct device tensors holding this problem's inputs."""
+        ts = [self.a.row_ptr, self.a.col_idx, self.a.values, self.c]
+        if self.b_is_dense:
+            ts.append(self.b)
+        elif not self.b_aliases_a:
+            ts += [self.b.row_ptr, self.b.col_idx, self.b.values]
+        return ts
+
+    def clone(self):
+        """A second device copy of the inputs (for double-buffered streaming)."""
+        import copy
+
+        other = copy.copy(self)
+        other.a = copy.copy(self.a)
+        for name in ("row_ptr", "col_idx", "values"):
+            setattr(other.a, name, getattr(self.a, name).clone())
+        other.c = self.c.clone()
+        if self.b_is_dense:
+            other.b = self.b.clone()
+        elif self.b_aliases_a:
+            other.b = other.a
+        else:
+            other.b = copy.copy(self.b)
+            for name in ("row_ptr", "col_idx", "values"):
+                setattr(other.b, name, getattr(self.b, name).clone())
+        return other
 
     def c_struct(self) -> TfgProblem:
         p = TfgProblem()
