@@ -803,41 +803,26 @@ __global__ void __launch_bounds__(288, 1)
       for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-      // (slot, value) per entry by broadcast 16-byte shared loads: 8 slots
-      // and 16/sizeof(T) values per load instead of two shuffles per entry
-      constexpr int VPL = 16 / (int)sizeof(T);
-      uintptr_t s_base = ~(uintptr_t)0, v_base = ~(uintptr_t)0;
-      uint4 s8 = make_uint4(0, 0, 0, 0);
-      T vv[VPL];
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) vv[q] = T(0);
-#pragma unroll 2
-      for (int e = eb; e < ee; ++e) {
-        const uintptr_t sp = reinterpret_cast<uintptr_t>(lsl + e);
-        if ((sp & ~(uintptr_t)15) != s_base) {
-          s_base = sp & ~(uintptr_t)15;
-          s8 = *reinterpret_cast<const uint4*>(s_base);
+      for (int e0 = eb; e0 < ee; e0 += LPR) {
+        int sl = 0;
+        T a = T(0);
+        if (e0 + gl < ee) {
+          sl = lsl[e0 + gl];
+          a = vs[e0 + gl];
         }
-        const int si = (int)((sp & 15) >> 1);
-        const unsigned wd = si < 2 ? s8.x : si < 4 ? s8.y : si < 6 ? s8.z : s8.w;
-        const int su = (si & 1) ? (int)(wd >> 16) : (int)(wd & 0xffffu);
-        const uintptr_t vp = reinterpret_cast<uintptr_t>(vs + e);
-        if ((vp & ~(uintptr_t)15) != v_base) {
-          v_base = vp & ~(uintptr_t)15;
-          ldv<T, VPL>(vv, reinterpret_cast<const T*>(v_base));
-        }
-        const int vi = (int)((vp & 15) / sizeof(T));
-        T au = vv[0];
+        const int cnt = min(LPR, ee - e0);
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+          const int su = __shfl_sync(gmask, sl, u, LPR);
+          const T au = __shfl_sync(gmask, a, u, LPR);
 #pragma unroll
-        for (int q = 1; q < VPL; ++q)
-          if (vi == q) au = vv[q];
+          for (int ch = 0; ch < NCH; ++ch) {
+            T x[VEC];
+            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          T x[VEC];
-          ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v)
-            acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+          }
         }
       }
       T* o = out + (size_t)(r_lo + r) * ldo;
