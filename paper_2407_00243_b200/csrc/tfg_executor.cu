@@ -804,17 +804,12 @@ __global__ void __launch_bounds__(288, 1)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
       for (int e0 = eb; e0 < ee; e0 += LPR) {
-        int sl = 0;
-        T a = T(0);
-        if (e0 + gl < ee) {
-          sl = lsl[e0 + gl];
-          a = vs[e0 + gl];
-        }
+        const int sl = e0 + gl < ee ? lsl[e0 + gl] : 0;
         const int cnt = min(LPR, ee - e0);
 #pragma unroll 4
         for (int u = 0; u < cnt; ++u) {
           const int su = __shfl_sync(gmask, sl, u, LPR);
-          const T au = __shfl_sync(gmask, a, u, LPR);
+          const T au = vs[e0 + u];  // broadcast load: 1 wavefront vs 2 for a 64-bit shuffle
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
             T x[VEC];
