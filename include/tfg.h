@@ -225,6 +225,21 @@ void tfg_plan_destroy(tfg_plan *plan);
 tfg_status tfg_run_host(const tfg_problem *host_problem,
                         const tfg_schedule *s, void *h_d);
 
+/* Row-range helpers (kernels.hpp:159-180) on host operands, computed by the
+ * GPU kernels.  gemm: rows [row_lo, row_hi) of D1 = B*C written into h_d1
+ * (b_rows x c_cols; other rows untouched); EINVAL if b_cols != c_rows or the
+ * range is out of bounds.  spmm: rows h_rows[] of D = A*X written into h_d
+ * (a_rows x x_cols; other rows untouched); EINVAL if a_cols != x_rows. */
+tfg_status tfg_gemm_rows_host(int32_t dtype, const void *h_b, int32_t b_rows,
+                              int32_t b_cols, const void *h_c, int32_t c_rows,
+                              int32_t c_cols, int32_t row_lo, int32_t row_hi,
+                              void *h_d1);
+tfg_status tfg_spmm_rows_host(int32_t dtype, int32_t a_rows, int32_t a_cols,
+                              const int32_t *h_row_ptr, const int32_t *h_col_idx,
+                              const void *h_values, const void *h_x,
+                              int32_t x_rows, int32_t x_cols,
+                              const int32_t *h_rows, int64_t n_rows, void *h_d);
+
 /* ---------------------------------------------------------------------
  * Multi-GPU row-block partition helpers: halo pack / unpack of
  * D1 rows around the NCCL exchange.  rows: device int32 list.

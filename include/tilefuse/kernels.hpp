@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <span>
 #include <stdexcept>
 #include <type_traits>
 #include <variant>
@@ -114,6 +115,32 @@ DenseMatrix<T> run_on_device(const FusedProblem<T>& p, const FusedSchedule* sche
 }
 
 }  // namespace detail
+
+// Rows [row_lo, row_hi) of D1 = B*C (kernels.hpp:159-169), on the GPU.
+template <class T>
+void gemm(const DenseMatrix<T>& b, const DenseMatrix<T>& c, index_t row_lo, index_t row_hi,
+          DenseMatrix<T>& d1) {
+  if (b.n_cols != c.n_rows) throw std::invalid_argument("gemm: inner dimensions disagree");
+  if (d1.n_rows != b.n_rows || d1.n_cols != c.n_cols)
+    throw std::invalid_argument("gemm: output shape mismatch");
+  detail::tfg_check(tfg_gemm_rows_host(std::is_same_v<T, double> ? TFG_F64 : TFG_F32,
+                                       b.data.data(), b.n_rows, b.n_cols, c.data.data(), c.n_rows,
+                                       c.n_cols, row_lo, row_hi, d1.data.data()));
+}
+
+// Rows j_list of D = A*X (kernels.hpp:171-180), on the GPU.
+template <class T>
+void spmm(const CsrMatrix<T>& a, const DenseMatrix<T>& x, std::span<const index_t> j_list,
+          DenseMatrix<T>& d) {
+  if (a.n_cols != x.n_rows) throw std::invalid_argument("spmm: inner dimensions disagree");
+  if (d.n_rows != a.n_rows || d.n_cols != x.n_cols)
+    throw std::invalid_argument("spmm: output shape mismatch");
+  const index_t dummy = 0;
+  detail::tfg_check(tfg_spmm_rows_host(
+      std::is_same_v<T, double> ? TFG_F64 : TFG_F32, a.n_rows, a.n_cols, a.row_ptr.data(),
+      a.col_idx.empty() ? &dummy : a.col_idx.data(), a.values.data(), x.data.data(), x.n_rows,
+      x.n_cols, j_list.empty() ? &dummy : j_list.data(), (int64_t)j_list.size(), d.data.data()));
+}
 
 template <class T>
 DenseMatrix<T> fused_gemm_spmm(const FusedProblem<T>& problem, const FusedSchedule& sched,

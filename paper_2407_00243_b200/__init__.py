@@ -21,6 +21,8 @@ from .tilefuse import (  # noqa: F401
     fused_spmm_spmm,
     gen_banded,
     gen_random_sparse,
+    gemm,
+    spmm,
     import_schedule,
     run,
     schedule_from_json,

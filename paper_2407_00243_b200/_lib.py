@@ -91,6 +91,10 @@ SIGNATURES = [
     ("tfg_plan_profile", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, f64p, i64p]),
     ("tfg_plan_destroy", None, [C.c_void_p]),
     ("tfg_run_host", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p]),
+    ("tfg_gemm_rows_host", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                     C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+    ("tfg_spmm_rows_host", C.c_int, [C.c_int32, C.c_int32, C.c_int32, i32p, i32p, C.c_void_p,
+                                     C.c_void_p, C.c_int32, C.c_int32, i32p, C.c_int64, C.c_void_p]),
     ("tfg_gather_rows", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
                                   C.c_void_p, C.c_void_p]),
     ("tfg_scatter_rows", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,

@@ -3079,3 +3079,93 @@ tfg_status tfg_scatter_rows(int32_t dtype, const void* src, int32_t cols, const 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Row-range helpers (kernels.hpp:159-180): host operands, GPU kernels.
+// ---------------------------------------------------------------------------
+extern "C" {
+
+tfg_status tfg_gemm_rows_host(int32_t dtype, const void* h_b, int32_t b_rows, int32_t b_cols,
+                              const void* h_c, int32_t c_rows, int32_t c_cols, int32_t row_lo,
+                              int32_t row_hi, void* h_d1) {
+  return guard([&] {
+    if (b_cols != c_rows) throw invalid_argument("gemm: inner dimensions disagree");
+    if (row_lo < 0 || row_hi > b_rows || row_lo > row_hi)
+      throw invalid_argument("gemm: row range out of bounds");
+    if (row_hi == row_lo) return;
+    const size_t el = dtype == TFG_F64 ? 8 : 4;
+    cudaStream_t st = nullptr;
+    const int nr = row_hi - row_lo;
+    dbuf<unsigned char> b((size_t)nr * b_cols * el), c((size_t)c_rows * c_cols * el),
+        d((size_t)nr * c_cols * el);
+    h2d(b.p, static_cast<const unsigned char*>(h_b) + (size_t)row_lo * b_cols * el,
+        (size_t)nr * b_cols * el, st);
+    h2d(c.p, static_cast<const unsigned char*>(h_c), (size_t)c_rows * c_cols * el, st);
+    std::vector<int> r0, cnt;
+    for (int r = 0; r < nr; r += kGemmBM) {
+      r0.push_back(r);
+      cnt.push_back(std::min(kGemmBM, nr - r));
+    }
+    dbuf<int> dr0(r0.size()), dcnt(cnt.size());
+    h2d(dr0.p, r0.data(), r0.size(), st);
+    h2d(dcnt.p, cnt.data(), cnt.size(), st);
+    const int gy = (c_cols + kGemmBN - 1) / kGemmBN;
+    const int gx = (int)std::min<size_t>(r0.size(), (size_t)sm_count() * 16);
+    if (dtype == TFG_F64)
+      k_gemm_blocks<double, kGemmBM, kGemmBN, kGemmBK, kGemmTM, kGemmTN>
+          <<<dim3(gx, gy), 256, 0, st>>>((int64_t)r0.size(), dr0.p, dcnt.p,
+                                         reinterpret_cast<const double*>(b.p), b_cols,
+                                         reinterpret_cast<const double*>(c.p), c_cols,
+                                         reinterpret_cast<double*>(d.p), c_cols);
+    else
+      k_gemm_blocks<float, kGemmBM, kGemmBN, kGemmBK, kGemmTM, kGemmTN>
+          <<<dim3(gx, gy), 256, 0, st>>>((int64_t)r0.size(), dr0.p, dcnt.p,
+                                         reinterpret_cast<const float*>(b.p), b_cols,
+                                         reinterpret_cast<const float*>(c.p), c_cols,
+                                         reinterpret_cast<float*>(d.p), c_cols);
+    TFG_LAUNCH_CHECK();
+    d2h(static_cast<unsigned char*>(h_d1) + (size_t)row_lo * c_cols * el, d.p,
+        (size_t)nr * c_cols * el, st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+tfg_status tfg_spmm_rows_host(int32_t dtype, int32_t a_rows, int32_t a_cols,
+                              const int32_t* h_rp, const int32_t* h_ci, const void* h_av,
+                              const void* h_x, int32_t x_rows, int32_t x_cols,
+                              const int32_t* h_rows, int64_t n_list, void* h_d) {
+  return guard([&] {
+    if (a_cols != x_rows) throw invalid_argument("spmm: inner dimensions disagree");
+    for (int64_t q = 0; q < n_list; ++q)
+      if (h_rows[q] < 0 || h_rows[q] >= a_rows) throw invalid_argument("spmm: row out of range");
+    if (n_list == 0) return;
+    const size_t el = dtype == TFG_F64 ? 8 : 4;
+    cudaStream_t st = nullptr;
+    const int64_t nnz = h_rp[a_rows];
+    dbuf<int32_t> rp(a_rows + 1), ci(std::max<int64_t>(nnz, 1));
+    dbuf<unsigned char> av(std::max<int64_t>(nnz, 1) * el), x((size_t)x_rows * x_cols * el),
+        d((size_t)a_rows * x_cols * el);
+    h2d(rp.p, h_rp, a_rows + 1, st);
+    h2d(ci.p, h_ci, nnz, st);
+    h2d(av.p, static_cast<const unsigned char*>(h_av), nnz * el, st);
+    h2d(x.p, static_cast<const unsigned char*>(h_x), (size_t)x_rows * x_cols * el, st);
+    // rows not in the list keep the caller's values
+    h2d(d.p, static_cast<const unsigned char*>(h_d), (size_t)a_rows * x_cols * el, st);
+    std::vector<int> rows(h_rows, h_rows + n_list);
+    std::vector<int> rph(h_rp, h_rp + a_rows + 1);
+    SpmmWork w;
+    w.build(rows, rph, x_cols, el, st);
+    if (dtype == TFG_F64)
+      spmm_run<double>(w, rp.p, ci.p, reinterpret_cast<const double*>(av.p),
+                       reinterpret_cast<const double*>(x.p), x_cols,
+                       reinterpret_cast<double*>(d.p), st);
+    else
+      spmm_run<float>(w, rp.p, ci.p, reinterpret_cast<const float*>(av.p),
+                      reinterpret_cast<const float*>(x.p), x_cols, reinterpret_cast<float*>(d.p),
+                      st);
+    d2h(static_cast<unsigned char*>(h_d), d.p, (size_t)a_rows * x_cols * el, st);
+    TFG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

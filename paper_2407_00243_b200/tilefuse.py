@@ -667,6 +667,43 @@ def unfused_spmm_spmm(a: Csr, b: Csr, c, workers: int = 1, dtype=np.float64) -> 
     return run(a, b, c, None, dtype)
 
 
+def gemm(b, c, row_lo: int, row_hi: int, d1: np.ndarray) -> np.ndarray:
+    """kernels.hpp:159-169: rows [row_lo, row_hi) of D1 = B*C into d1 (in place), on the GPU."""
+    b = np.asarray(b)
+    c = np.asarray(c)
+    if b.shape[1] != c.shape[0]:
+        raise ValueError("gemm: inner dimensions disagree")
+    if d1.shape != (b.shape[0], c.shape[1]):
+        raise ValueError("gemm: output shape mismatch")
+    dt = d1.dtype
+    bb = np.ascontiguousarray(b, dt)
+    cc = np.ascontiguousarray(c, dt)
+    assert d1.flags.c_contiguous
+    check(lib().tfg_gemm_rows_host(_dt_code(dt), bb.ctypes.data, b.shape[0], b.shape[1], cc.ctypes.data,
+                                   c.shape[0], c.shape[1], int(row_lo), int(row_hi), d1.ctypes.data))
+    return d1
+
+
+def spmm(a: Csr, x, j_list, d: np.ndarray) -> np.ndarray:
+    """kernels.hpp:171-180: rows j_list of D = A*X into d (in place), on the GPU."""
+    x = np.asarray(x)
+    if a.n_cols != x.shape[0]:
+        raise ValueError("spmm: inner dimensions disagree")
+    if d.shape != (a.n_rows, x.shape[1]):
+        raise ValueError("spmm: output shape mismatch")
+    dt = d.dtype
+    rows = np.ascontiguousarray(j_list, np.int32)
+    rr = rows if rows.size else np.zeros(1, np.int32)
+    ci = a.col_idx if a.nnz else np.zeros(1, np.int32)
+    av = np.ascontiguousarray(a.values, dt) if a.nnz else np.zeros(1, dt)
+    xx = np.ascontiguousarray(x, dt)
+    assert d.flags.c_contiguous
+    check(lib().tfg_spmm_rows_host(_dt_code(dt), a.n_rows, a.n_cols, a.row_ptr.ctypes.data_as(i32p),
+                                   ci.ctypes.data_as(i32p), av.ctypes.data, xx.ctypes.data, x.shape[0],
+                                   x.shape[1], rr.ctypes.data_as(i32p), rows.size, d.ctypes.data))
+    return d
+
+
 def fused_ratio(a: Csr, tile_size: int) -> float:
     """bindings.cpp:132-141: step-1 fused fraction at a given tile size
     (inspector with p=1 and an unbounded budget, so nothing is split)."""

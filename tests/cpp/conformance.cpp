@@ -123,6 +123,31 @@ int main() {
     CHECK((unfused_spmm_spmm(q, 1).data == std::vector<double>{6, 8, 3, 6}));
   }
 
+  // gemm / spmm row-range helpers (test_kernels.cpp:26-64)
+  {
+    DenseMatrix<double> b(2, 2), c(2, 2), d1(2, 2);
+    b.data = {1, 2, 3, 4};
+    c.data = {5, 6, 7, 8};
+    gemm(b, c, 0, 2, d1);
+    CHECK((d1.data == std::vector<double>{19, 22, 43, 50}));
+    DenseMatrix<double> part(2, 2);
+    gemm(b, c, 1, 2, part);
+    CHECK((part.data == std::vector<double>{0, 0, 43, 50}));
+    DenseMatrix<double> wrong(3, 2);
+    CHECK_THROWS_AS(gemm(b, c, 0, 2, wrong), std::invalid_argument);
+    const auto a = csr_from_triplets<double>(2, 2, {{0, 1, 2.0}, {1, 0, 3.0}});
+    DenseMatrix<double> x(2, 2), d(2, 2);
+    x.data = {1, 2, 3, 4};
+    const std::vector<index_t> all{0, 1}, one{1};
+    spmm(a, x, all, d);
+    CHECK((d.data == std::vector<double>{6, 8, 3, 6}));
+    DenseMatrix<double> pd(2, 2);
+    spmm(a, x, one, pd);
+    CHECK((pd.data == std::vector<double>{0, 0, 3, 6}));
+    DenseMatrix<double> xbad(3, 2);
+    CHECK_THROWS_AS(spmm(a, xbad, all, d), std::invalid_argument);
+  }
+
   // fused vs dense oracle, fused == unfused bitwise, stats, errors
   // (test_kernels.cpp:66-229)
   {

@@ -51,6 +51,31 @@ def test_known_answers(cuda):  # test_kernels.cpp:26-64
     assert d.ravel().tolist() == [6, 8, 3, 6]
 
 
+def test_row_range_helpers(cuda, oracle):  # test_kernels.cpp:26-64, kernels.hpp:159-180
+    b = np.array([[1., 2.], [3., 4.]])
+    c = np.array([[5., 6.], [7., 8.]])
+    d1 = np.zeros((2, 2))
+    assert P.gemm(b, c, 0, 2, d1).ravel().tolist() == [19, 22, 43, 50]
+    part = np.zeros((2, 2))
+    assert P.gemm(b, c, 1, 2, part).ravel().tolist() == [0, 0, 43, 50]
+    with pytest.raises(ValueError):
+        P.gemm(b, c, 0, 2, np.zeros((3, 2)))
+    a = P.Csr(2, 2, [0, 1, 2], [1, 0], [2.0, 3.0])
+    x = np.array([[1., 2.], [3., 4.]])
+    assert P.spmm(a, x, [0, 1], np.zeros((2, 2))).ravel().tolist() == [6, 8, 3, 6]
+    assert P.spmm(a, x, [1], np.zeros((2, 2))).ravel().tolist() == [0, 0, 3, 6]
+    with pytest.raises(ValueError):
+        P.spmm(a, np.zeros((3, 2)), [0], np.zeros((2, 2)))
+    # a larger random row subset is bit-exact against the reference order
+    rp, ci, v = oracle.gen_random_sparse(500, 0.02, 8)
+    a = P.Csr(500, 500, rp, ci, v)
+    xx = np.random.default_rng(0).uniform(-1, 1, (500, 64))
+    rows = np.sort(np.random.default_rng(1).choice(500, 200, replace=False))
+    got = P.spmm(a, xx, rows, np.zeros((500, 64)))
+    want = oracle.run(500, (rp, ci, v), np.eye(500), xx, None)  # D = A (I X)
+    assert np.array_equal(got[rows], want[rows]) and not got[np.setdiff1d(np.arange(500), rows)].any()
+
+
 def test_matches_numpy_like_reference_smoke(cuda):  # tests/python/test_smoke.py:60-90
     rng = np.random.default_rng(3)
     a = P.gen_random_sparse(80, 0.08, seed=3)
