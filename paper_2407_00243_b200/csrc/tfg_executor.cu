@@ -1198,6 +1198,54 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Vectorised long-row segments: LPR lanes per segment (16-byte gathers),
+// partial rows to scratch, then an ordered combine per long row.
+template <class T, int VEC, int LPR, int NCH>
+__global__ void __launch_bounds__(256)
+    k_spmm_segments_vec(int64_t nseg, const int* __restrict__ seg_k0,
+                        const int* __restrict__ seg_k1, const int* __restrict__ ci,
+                        const T* __restrict__ av, const T* __restrict__ X, int ldx,
+                        T* __restrict__ partial) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  if (g >= nseg) return;
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  auto xl = [&](int c, int ch, T(&x)[VEC]) {
+    ldv<T, VEC>(x, X + (size_t)c * ldx + (ch * LPR + gl) * VEC);
+  };
+  T acc[NCH][VEC];
+  spmm_row<T, VEC, LPR, NCH>(seg_k0[g], seg_k1[g], ci, av, gl, gmask, xl, acc);
+  T* o = partial + (size_t)g * ldx;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+}
+
+template <class T, int VEC, int LPR, int NCH>
+__global__ void __launch_bounds__(256)
+    k_segment_combine_vec(int64_t nlong, const int* __restrict__ long_rows,
+                          const int64_t* __restrict__ long_seg_off,
+                          const T* __restrict__ partial, int cc, T* __restrict__ out,
+                          int ldo) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  if (g >= nlong) return;
+  const int gl = threadIdx.x & (LPR - 1);
+  const int r = long_rows[g];
+  const int64_t s0 = long_seg_off[g], s1 = long_seg_off[g + 1];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int col = (ch * LPR + gl) * VEC;
+    T acc[VEC];
+    ldv<T, VEC>(acc, partial + (size_t)s0 * cc + col);
+    for (int64_t sg = s0 + 1; sg < s1; ++sg) {
+      T x[VEC];
+      ldv<T, VEC>(x, partial + (size_t)sg * cc + col);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[v] = fops<T>::add(acc[v], x[v]);
+    }
+    stv<T, VEC>(out + (size_t)r * ldo + col, acc);
+  }
+}
+
 // ---- dense first op: D1[rows, :] = B[rows, :] C, register tiled ----------
 // Per element: acc = fma(B[i,j], C[j,k], acc) for j ascending from 0, the
 // same sequence the fused kernel uses, so fused and unfused agree bitwise.
@@ -2109,15 +2157,33 @@ struct SpmmWork {
     std::vector<int> sh, lg, k0, k1;
     std::vector<int64_t> off{0};
     sh.reserve(rows.size());
+    // Power-law rows: one lane group would walk a row of thousands of
+    // nonzeros alone while the rest of the GPU idles, so skewed lists split
+    // every row longer than ~8x the mean into segments of that length.
+    int long_thr = kLongRow, seg_len = kSegLen;
+    if (!rows.empty()) {
+      int64_t tot = 0;
+      int mx = 0;
+      for (int r : rows) {
+        tot += rp[r + 1] - rp[r];
+        mx = std::max(mx, rp[r + 1] - rp[r]);
+      }
+      const double mean = (double)tot / (double)rows.size();
+      const int thr = std::max(256, (int)(8.0 * mean));
+      if (mx > thr && thr < kLongRow) {
+        long_thr = thr;
+        seg_len = thr;
+      }
+    }
     for (int r : rows) {
       const int b = rp[r], e = rp[r + 1];
-      if (e - b <= kLongRow) {
+      if (e - b <= long_thr) {
         sh.push_back(r);
       } else {
         lg.push_back(r);
-        for (int k = b; k < e; k += kSegLen) {
+        for (int k = b; k < e; k += seg_len) {
           k0.push_back(k);
-          k1.push_back(std::min(e, k + kSegLen));
+          k1.push_back(std::min(e, k + seg_len));
         }
         off.push_back((int64_t)k0.size());
       }
@@ -2365,6 +2431,23 @@ static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
   spmm_dispatch_short<T>(w, rp, ci, av, X, cc, out, st);
   if (w.n_long) {
     T* partial = reinterpret_cast<T*>(w.partial.p);
+    constexpr int VEC = 16 / sizeof(T);
+    const int L = cc % VEC == 0 ? cc / VEC : 0;
+#define TFG_SEG(LPR, NCH)                                                                     \
+  {                                                                                           \
+    k_spmm_segments_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(         \
+        w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                             \
+    TFG_LAUNCH_CHECK();                                                                       \
+    k_segment_combine_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_long * LPR), 256, 0, st>>>(      \
+        w.n_long, w.long_rows.p, w.long_seg_off.p, partial, cc, out, cc);                     \
+    TFG_LAUNCH_CHECK();                                                                       \
+    return;                                                                                   \
+  }
+    if (L == 8) TFG_SEG(8, 1)
+    if (L == 16) TFG_SEG(16, 1)
+    if (L == 32) TFG_SEG(32, 1)
+    if (L == 64) TFG_SEG(32, 2)
+#undef TFG_SEG
     k_spmm_segments<T><<<blocks_for(w.n_seg * 32), 256, 0, st>>>(
         w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, cc, partial);
     TFG_LAUNCH_CHECK();
