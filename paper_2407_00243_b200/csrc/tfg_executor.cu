@@ -803,40 +803,21 @@ __global__ void __launch_bounds__(288, 1)
       for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-      auto fma_row = [&](int su, T au) {
+      for (int e0 = eb; e0 < ee; e0 += LPR) {
+        const int sl = e0 + gl < ee ? lsl[e0 + gl] : 0;
+        const int cnt = min(LPR, ee - e0);
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+          const int su = __shfl_sync(gmask, sl, u, LPR);
+          const T au = vs[e0 + u];  // broadcast load: 1 wavefront vs 2 for a 64-bit shuffle
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          T x[VEC];
-          ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
+          for (int ch = 0; ch < NCH; ++ch) {
+            T x[VEC];
+            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
 #pragma unroll
-          for (int v = 0; v < VEC; ++v)
-            acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
-        }
-      };
-      int e = eb;
-      if (e < ee && (e & 1)) {  // leading odd entry: keeps value pairs 2-aligned
-        fma_row(lsl[e], vs[e]);
-        ++e;
-      }
-      // entry pairs: one 32-bit shuffle carries two slots, one broadcast
-      // 2-element load carries two values (in-order accumulation kept)
-      for (int e0 = e; e0 < ee; e0 += 2 * LPR) {
-        const int i0 = e0 + 2 * gl;
-        const unsigned sl0 = i0 < ee ? lsl[i0] : 0u;
-        const unsigned sl1 = i0 + 1 < ee ? lsl[i0 + 1] : 0u;
-        const unsigned pk = sl0 | (sl1 << 16);
-        const int cnt = min(2 * LPR, ee - e0);
-#pragma unroll 2
-        for (int u = 0; u + 1 < cnt; u += 2) {
-          const unsigned w2 = __shfl_sync(gmask, pk, u >> 1, LPR);
-          T a2[2];
-          ldv<T, 2>(a2, vs + e0 + u);
-          fma_row((int)(w2 & 0xffffu), a2[0]);
-          fma_row((int)(w2 >> 16), a2[1]);
-        }
-        if (cnt & 1) {
-          const unsigned w2 = __shfl_sync(gmask, pk, (cnt - 1) >> 1, LPR);
-          fma_row((int)(w2 & 0xffffu), vs[e0 + cnt - 1]);
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+          }
         }
       }
       T* o = out + (size_t)(r_lo + r) * ldo;
