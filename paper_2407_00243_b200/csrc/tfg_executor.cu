@@ -1320,7 +1320,7 @@ struct GemmCfg {
   static constexpr int C_LD = BN + PAD;
   static constexpr size_t SMEM =
       (size_t)STAGES * ((size_t)BM * B_LD + (size_t)BK * C_LD) * sizeof(T);
-  static_assert(THREADS == 256, "256 threads per CTA");
+  static_assert(THREADS == 256 || THREADS == 128, "128 or 256 threads per CTA");
   static_assert(BK % V == 0 && TN % V == 0, "vector widths");
 };
 
@@ -1489,7 +1489,7 @@ __device__ __forceinline__ void gemm_compute_chunk(int bc, int kc, int stg, cons
 // flattened with their K chunks into one cp.async ring, so loads of the next
 // block overlap the current block's FMAs and epilogue.
 template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
     k_gemm_stream(int64_t nblk, const int* __restrict__ blk_r0, const int* __restrict__ blk_cnt,
                   const T* __restrict__ B, int bc, const T* __restrict__ C, int cc,
                   T* __restrict__ D1, int ldd) {
@@ -2840,9 +2840,9 @@ static void launch_gemm_v2_cfg(tfg_plan& pl, const T* B, int bc, const T* C, int
     attr = true;
   }
   int per_sm = 1;
-  TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, G::SMEM));
+  TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, G::SMEM));
   const int64_t gx = std::min<int64_t>(pl.n_fo_blocks, (int64_t)sm_count() * std::max(per_sm, 1));
-  kern<<<dim3((unsigned)gx, cc / BN), 256, G::SMEM, st>>>(pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p,
+  kern<<<dim3((unsigned)gx, cc / BN), G::THREADS, G::SMEM, st>>>(pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p,
                                                           B, bc, C, cc, D1, cc);
   TFG_LAUNCH_CHECK();
 }
@@ -2882,9 +2882,15 @@ static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
 template <class T>
 static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
                            cudaStream_t st) {
+  static const int gv = [] {
+    const char* e = getenv("TFG_GEMM_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
   if constexpr (sizeof(T) == 4) {
     if (pl.gemm_kind == 2)
       launch_gemm_v2_cfg<T, 64, 128, 32, 4, 8>(pl, B, bc, C, cc, D1, st);
+    else if (gv == 1)  // 8x8 thread tiles, 128 threads (blocks of 128 rows)
+      launch_gemm_v2_cfg<T, 128, 64, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
     else
       launch_gemm_v2_cfg<T, 128, 64, 32, 8, 4>(pl, B, bc, C, cc, D1, st);
   } else {

@@ -30,6 +30,9 @@ def main():
     variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
     for v in variants:
         env = dict(os.environ)
+        if v.startswith("G"):  # GEMM variant
+            env["TFG_GEMM_VARIANT"] = v[1:]
+            v = "-1"
         if v.startswith("u0"):  # band without the mini-group union consumer
             env["TFG_BAND_UNION"] = "0"
             v = v[2:] or "-1"
