@@ -2508,11 +2508,21 @@ static constexpr size_t kFusedSmemCap = 200 * 1024;
 static constexpr int64_t kGroupMaxNnz = 96ll << 20;
 static constexpr size_t kFusedSmemMax = 227 * 1024;  // sm_100 opt-in max per CTA
 
+static int gemm_variant() {
+  static const int gv = [] {
+    const char* e = getenv("TFG_GEMM_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return gv;
+}
+
 // shared memory of the pipelined GEMM configuration a plan uses
 static size_t fused_gemm_smem(const tfg_plan& pl) {
-  if (pl.elem == 4)
+  if (pl.elem == 4) {
+    if (pl.gemm_kind == 2 && gemm_variant() == 2) return GemmCfg<float, 128, 128, 32, 8, 8, 3>::SMEM;
     return pl.gemm_kind == 2 ? GemmCfg<float, 64, 128, 32, 4, 8, 3>::SMEM
                              : GemmCfg<float, 128, 64, 32, 8, 4, 3>::SMEM;
+  }
   return pl.gemm_kind == 2 ? GemmCfg<double, 64, 128, 16, 4, 8, 3>::SMEM
                            : GemmCfg<double, 64, 64, 16, 4, 4, 3>::SMEM;
 }
@@ -2567,7 +2577,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       pl.gemm_kind = 2;  // BN = 128
     else if (aligned && cc % 64 == 0)
       pl.gemm_kind = 1;  // BN = 64
-    if (pl.gemm_kind) pl.gemm_bm = (pl.elem == 4 && pl.gemm_kind == 1) ? 128 : 64;
+    if (pl.gemm_kind)
+      pl.gemm_bm = (pl.elem == 4 && (pl.gemm_kind == 1 || gemm_variant() == 2)) ? 128 : 64;
   }
   if (!s) {
     for (int i = row_lo; i < row_hi; ++i) fo_rows.push_back(i);
@@ -2867,7 +2878,9 @@ static void launch_fused_v2_cfg(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
 template <class T>
 static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
-    if (pl.gemm_kind == 2)
+    if (pl.gemm_kind == 2 && gemm_variant() == 2)
+      launch_fused_v2_cfg<T, 128, 128, 32, 8, 8, 32>(pl, D1, D, st);
+    else if (pl.gemm_kind == 2)
       launch_fused_v2_cfg<T, 64, 128, 32, 4, 8, 32>(pl, D1, D, st);
     else
       launch_fused_v2_cfg<T, 128, 64, 32, 8, 4, 16>(pl, D1, D, st);
@@ -2882,12 +2895,11 @@ static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
 template <class T>
 static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
                            cudaStream_t st) {
-  static const int gv = [] {
-    const char* e = getenv("TFG_GEMM_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
+  const int gv = gemm_variant();
   if constexpr (sizeof(T) == 4) {
-    if (pl.gemm_kind == 2)
+    if (pl.gemm_kind == 2 && gv == 2)
+      launch_gemm_v2_cfg<T, 128, 128, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
+    else if (pl.gemm_kind == 2)
       launch_gemm_v2_cfg<T, 64, 128, 32, 4, 8>(pl, B, bc, C, cc, D1, st);
     else if (gv == 1)  // 8x8 thread tiles, 128 threads (blocks of 128 rows)
       launch_gemm_v2_cfg<T, 128, 64, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
