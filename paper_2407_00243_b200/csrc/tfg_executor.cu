@@ -2224,7 +2224,10 @@ struct SpmmWork {
         mx = std::max(mx, rp[r + 1] - rp[r]);
       }
       const double mean = (double)tot / (double)sh.size();
-      skewed = mx > 8.0 * std::max(mean, 1.0);
+      // one row per lane group when rows are skewed, or when strips of 32
+      // rows would leave the GPU with too few warps (small row lists)
+      skewed = mx > 8.0 * std::max(mean, 1.0) ||
+               (int64_t)sh.size() < (int64_t)sm_count() * 32 * 32;
     }
     static const bool band_on = [] {
       const char* e = getenv("TFG_SPMM_BAND");
