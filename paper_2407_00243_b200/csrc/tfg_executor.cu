@@ -1023,7 +1023,7 @@ __global__ void __launch_bounds__(288, 1)
 // cp.async (16 B per lane), issuing DEPTH entries ahead of the consumer.
 // The consumer sums each row's entries in order (mul then add, bit-identical
 // to the reference).
-template <class T, int VEC, int LPR, int NCH, int DEPTH>
+template <class T, int VEC, int LPR, int NCH, int DEPTH, int STRIP = LPR>
 __global__ void __launch_bounds__(256)
     k_spmm_ring(int64_t nrows, const int* __restrict__ rows, int row0,
                 const int* __restrict__ rp, const int* __restrict__ ci,
@@ -1034,11 +1034,11 @@ __global__ void __launch_bounds__(256)
   const int grp_in_cta = threadIdx.x / LPR;
   T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)grp_in_cta * DEPTH * SLOT;
   const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
-  const int64_t base = g * LPR;
+  const int64_t base = g * STRIP;
   if (base >= nrows) return;
   const int gl = threadIdx.x & (LPR - 1);
   const unsigned gmask = group_mask(LPR);
-  const int cnt = (int)(nrows - base < LPR ? nrows - base : LPR);
+  const int cnt = (int)(nrows - base < STRIP ? nrows - base : STRIP);
   int my_r = 0, my_b = 0, my_e = 0;
   if (gl < cnt) {
     my_r = rows ? __ldg(rows + base + gl) : row0 + (int)(base + gl);
@@ -2351,11 +2351,10 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     const int L = cc / VEC;
 #define TFG_RING(LPR, NCH, D)                                                               \
   if (ring_depth == D) {                                                                    \
-    auto kern = k_spmm_ring<T, VEC, LPR, NCH, D>;                                           \
+    auto kern = k_spmm_ring<T, VEC, LPR, NCH, D, 1>;                                        \
     const size_t smem = (size_t)(256 / LPR) * D * LPR * VEC * NCH * sizeof(T);             \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<blocks_for((n + LPR - 1) / LPR * LPR), 256, smem, st>>>(n, rows, row0, rp, ci, av, X, \
-                                                                    cc, out, cc);           \
+    kern<<<blocks_for(n * LPR), 256, smem, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
     TFG_LAUNCH_CHECK();                                                                     \
     return;                                                                                 \
   }
