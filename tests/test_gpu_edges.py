@@ -137,3 +137,35 @@ def test_skewed_rows_spmm_spmm_bit_exact(cuda, oracle, cc):
     assert max_rel_err(got, want) <= 1e-12
     if not long_rows.any():
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name,scale", [("cfg1", 1 / 16), ("cfg2", 1 / 16), ("cfg3", 1 / 64),
+                                        ("cfg4", 1 / 8), ("cfg5", 1 / 512)])
+def test_poisoned_scratch_and_output(cuda, name, scale):
+    """Stand-in for a memory checker: the plan's D1 scratch and D are filled
+    with NaN bytes before executing, so any read of a D1 row the step did not
+    write first, or any D row the step forgets, shows up as NaN or as a
+    difference from an unpoisoned run."""
+    import ctypes as C
+
+    import torch
+    from cuda.bindings import runtime as rt
+
+    from paper_2407_00243_b200 import workloads as W
+    from paper_2407_00243_b200._lib import check, lib
+
+    w = W.make(name, scale=scale)
+    s = P.build_schedule(w.a, w.scheduler_config())
+    prob = P.DeviceProblem(w.a, w.b, w.c, w.dtype)
+    want = P.Plan(prob, s).execute().cpu().numpy()
+    plan = P.Plan(prob, s)
+    d1 = C.c_void_p()
+    check(lib().tfg_plan_d1(plan._h, C.byref(d1)))
+    tdt = getattr(torch, w.dtype.name)
+    if d1.value:
+        (err,) = rt.cudaMemset(d1.value, 0xFF, w.n * w.c_cols * np.dtype(w.dtype).itemsize)
+        assert err == rt.cudaError_t.cudaSuccess
+    out = torch.full((w.n, w.c_cols), float("nan"), dtype=tdt, device="cuda")
+    got = plan.execute(out).cpu().numpy()
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, want)
