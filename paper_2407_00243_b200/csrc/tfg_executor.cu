@@ -2685,6 +2685,24 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         h2d(pl.ft_wide.p, wide.data(), wide.size(), st);
         pl.stage_cap = cap;
         pl.fused_smem = gsm + (size_t)cap * BN * pl.elem;
+        if (getenv("TFG_DEBUG")) {
+          int64_t rows = 0, pad128 = 0, slots = 0, small = 0;
+          int wmax = 0;
+          for (int64_t v = 0; v < pl.n_ftiles; ++v) {
+            const int w = f_ihi[v] - f_ilo[v];
+            rows += w;
+            pad128 += (w + 127) / 128 * 128;
+            slots += tc[v];
+            small += w < 128;
+            wmax = std::max(wmax, w);
+          }
+          fprintf(stderr,
+                  "[tfg] fused tiles %lld rows %lld (pad128 %lld) wmax %d small %lld slots %lld "
+                  "fused_rows %lld cap %d wide %lld first_rows(unfused) %zu\n",
+                  (long long)pl.n_ftiles, (long long)rows, (long long)pad128, wmax,
+                  (long long)small, (long long)slots, (long long)f_rows.size(), cap,
+                  (long long)pl.n_wide, fo_rows.size());
+        }
       } else {
         // generic fused kernel: column slice = whole cc when the widest tile fits
         int cs = std::min(cc, 128);
