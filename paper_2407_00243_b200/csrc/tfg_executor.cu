@@ -32,6 +32,8 @@
 #include <vector>
 
 #include "tfg_common.cuh"
+#include "tfg_device.cuh"
+#include "tfg_tc.cuh"
 
 namespace tfg {
 namespace {
@@ -39,115 +41,7 @@ namespace {
 constexpr int kLongRow = 4096;  // rows with more nonzeros are segmented
 constexpr int kSegLen = 2048;   // nonzeros per segment
 
-template <class T>
-struct fops;
-template <>
-struct fops<double> {
-  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-  static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
-};
-template <>
-struct fops<float> {
-  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
-  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
-  static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-};
-
-template <class T, int VEC>
-struct VT;
-template <> struct VT<double, 1> { using type = double; };
-template <> struct VT<double, 2> { using type = double2; };
-template <> struct VT<float, 1> { using type = float; };
-template <> struct VT<float, 2> { using type = float2; };
-template <> struct VT<float, 4> { using type = float4; };
-
-template <class T, int VEC>
-__device__ __forceinline__ void ldv(T (&r)[VEC], const T* p) {
-  using V = typename VT<T, VEC>::type;
-  const V x = *reinterpret_cast<const V*>(p);
-  memcpy(r, &x, sizeof(V));
-}
-template <class T, int VEC>
-__device__ __forceinline__ void stv(T* p, const T (&r)[VEC]) {
-  using V = typename VT<T, VEC>::type;
-  V x;
-  memcpy(&x, r, sizeof(V));
-  *reinterpret_cast<V*>(p) = x;
-}
-// streaming store for D (written once, never re-read by this launch)
-template <class T, int VEC>
-__device__ __forceinline__ void stv_cs(T* p, const T (&r)[VEC]) {
-  using V = typename VT<T, VEC>::type;
-  V x;
-  memcpy(&x, r, sizeof(V));
-  __stcs(reinterpret_cast<V*>(p), x);
-}
-
-__device__ __forceinline__ unsigned group_mask(int lpr) {
-  if (lpr == 32) return 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  return ((1u << lpr) - 1u) << (lane & ~(lpr - 1));
-}
-
-// One CSR row times X, LPR lanes per row, each lane NCH x VEC columns.
-// Per-element order = ascending nonzeros, separate mul and add
-// (kernels.hpp:75-79).  XL(c, ch, out[VEC]) loads X row c, chunk ch.
-template <class T, int VEC, int LPR, int NCH, class XL>
-__device__ __forceinline__ void spmm_row(int kb, int ke,
-                                         const int* __restrict__ ci,
-                                         const T* __restrict__ av, int gl,
-                                         unsigned gmask, XL xl,
-                                         T (&acc)[NCH][VEC]) {
-#pragma unroll
-  for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[ch][e] = T(0);
-  for (int k0 = kb; k0 < ke; k0 += LPR) {
-    const int kk = k0 + gl;
-    int c = 0;
-    T a = T(0);
-    if (kk < ke) {
-      c = __ldg(ci + kk);
-      a = __ldg(av + kk);
-    }
-    const int cnt = min(LPR, ke - k0);
-    int u = 0;
-    for (; u + 4 <= cnt; u += 4) {
-      int cu[4];
-      T au[4];
-      T x[4][NCH][VEC];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        cu[q] = __shfl_sync(gmask, c, u + q, LPR);
-        au[q] = __shfl_sync(gmask, a, u + q, LPR);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) xl(cu[q], ch, x[q][ch]);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-          for (int e = 0; e < VEC; ++e)
-            acc[ch][e] = fops<T>::add(acc[ch][e], fops<T>::mul(au[q], x[q][ch][e]));
-    }
-    for (; u < cnt; ++u) {
-      const int cu = __shfl_sync(gmask, c, u, LPR);
-      const T au = __shfl_sync(gmask, a, u, LPR);
-      T x[NCH][VEC];
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) xl(cu, ch, x[ch]);
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int e = 0; e < VEC; ++e)
-          acc[ch][e] = fops<T>::add(acc[ch][e], fops<T>::mul(au, x[ch][e]));
-    }
-  }
-}
+using namespace dev;
 
 // ---- SpMM over a row list (short rows) ------------------------------------
 // A group of LPR lanes walks a strip of STRIP rows (STRIP <= LPR) in order.
@@ -2474,6 +2368,8 @@ struct tfg_plan {
   int gemm_kind = 0;             // 0 generic k_gemm_blocks, else k_gemm_v2 config id
   int gemm_bm = 64;
   tfg::dbuf<int> fo_r0, fo_cnt;  // dense B: GEMM row blocks
+  tfg::dbuf<int> fo_ihi;         // r0 + cnt (tensor-core first op)
+  tfg::TcPlan tc;                // fp32 dense B: tcgen05 3xTF32 first op (tfg_tc.cu)
   tfg::SpmmWork fo_sparse;       // sparse B: SpMM rows with X = C
   // (b) fused tiles
   int64_t n_ftiles = 0;
@@ -2581,6 +2477,9 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       pl.gemm_kind = 1;  // BN = 64
     if (pl.gemm_kind)
       pl.gemm_bm = (pl.elem == 4 && (pl.gemm_kind == 1 || gemm_variant() == 2)) ? 128 : 64;
+    if (pl.gemm_kind && pl.elem == 4 &&
+        tc_prepare(pl.tc, static_cast<const float*>(pr.d_b_dense), n, bc, cc))
+      pl.gemm_bm = 128;
   }
   if (!s) {
     for (int i = row_lo; i < row_hi; ++i) fo_rows.push_back(i);
@@ -2672,10 +2571,17 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         // stage capacity: two CTAs per SM when the GEMM ring leaves room
         const size_t per_cta = 2 * gsm + 16 * 1024 <= kFusedSmemMax ? kFusedSmemMax / 2 - 1024
                                                                    : kFusedSmemMax;
-        const size_t cap_bytes = per_cta > gsm ? per_cta - gsm : 0;
+        size_t cap_bytes = per_cta > gsm ? per_cta - gsm : 0;
         int max_need = 0;
         for (int c : tc) max_need = std::max(max_need, c);
-        const int cap = (int)std::min<size_t>(cap_bytes / ((size_t)BN * pl.elem), (size_t)max_need);
+        size_t row_bytes = (size_t)BN * pl.elem;
+        if (pl.tc.on) {  // tensor-core tiles: one CTA per SM, stage after ring + C
+          cap_bytes = tc_stage_bytes(pl.tc);
+          row_bytes = (size_t)pl.tc.bn * 4;
+          pl.cs = pl.tc.bn;
+          pl.n_slices = pl.tc.slices;
+        }
+        const int cap = (int)std::min<size_t>(cap_bytes / row_bytes, (size_t)max_need);
         std::vector<uint8_t> wide(pl.n_ftiles);
         for (int64_t v = 0; v < pl.n_ftiles; ++v) {
           wide[v] = tc[v] > cap;
@@ -2685,6 +2591,10 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         h2d(pl.ft_wide.p, wide.data(), wide.size(), st);
         pl.stage_cap = cap;
         pl.fused_smem = gsm + (size_t)cap * BN * pl.elem;
+        if (pl.tc.on) {
+          tc_finalize(pl.tc, cap);
+          pl.fused_smem = pl.tc.smem;
+        }
         if (getenv("TFG_DEBUG")) {
           int64_t rows = 0, pad128 = 0, slots = 0, small = 0;
           int wmax = 0;
@@ -2758,6 +2668,12 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     pl.fo_cnt.alloc(cnt.size());
     h2d(pl.fo_r0.p, r0.data(), r0.size(), st);
     h2d(pl.fo_cnt.p, cnt.data(), cnt.size(), st);
+    if (pl.tc.on) {
+      std::vector<int> ihi(r0.size());
+      for (size_t k = 0; k < r0.size(); ++k) ihi[k] = r0[k] + cnt[k];
+      pl.fo_ihi.alloc(ihi.size());
+      h2d(pl.fo_ihi.p, ihi.data(), ihi.size(), st);
+    }
   } else {
     std::vector<int> bci;
     if (pr.b_nnz > 0 && pr.b_nnz <= kGroupMaxNnz) {
@@ -2851,6 +2767,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   }
 
   pl.launches = 0;
+  if (pl.tc.on && (pl.n_fo_blocks > 0 || pl.n_ftiles > 0)) pl.launches += 1;  // C split
   if (pr.b_is_dense)
     pl.launches += pl.n_fo_blocks > 0;
   else
@@ -2944,8 +2861,17 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
   // (a)
+  if constexpr (sizeof(T) == 4) {
+    if (pl.tc.on && (pl.n_fo_blocks || pl.n_ftiles))
+      tc_prep_c(pl.tc, reinterpret_cast<const float*>(C), bc, cc, st);
+  }
   if (pr.b_is_dense) {
-    if (pl.n_fo_blocks && pl.gemm_kind) {
+    if (pl.n_fo_blocks && pl.tc.on) {
+      if constexpr (sizeof(T) == 4)
+        tc_run(pl.tc, pr.n, bc, cc, pl.n_fo_blocks, pl.fo_r0.p, pl.fo_ihi.p, nullptr, nullptr,
+               nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+               reinterpret_cast<float*>(D1), nullptr, st);
+    } else if (pl.n_fo_blocks && pl.gemm_kind) {
       launch_gemm_v2<T>(pl, static_cast<const T*>(pr.d_b_dense), bc, C, cc, D1, st);
     } else if (pl.n_fo_blocks) {
       const int gy = (cc + kGemmBN - 1) / kGemmBN;
@@ -2962,7 +2888,13 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   }
   if (ev) TFG_CUDA(cudaEventRecord(ev[1], st));
   // (b)
-  if (pl.n_ftiles && pl.fused_v2) {
+  if (pl.n_ftiles && pl.fused_v2 && pl.tc.on) {
+    if constexpr (sizeof(T) == 4)
+      tc_run(pl.tc, pr.n, bc, cc, pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, pl.ft_joff.p,
+             pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p, pl.spill.p, pr.d_a_row_ptr, pr.d_a_col_idx,
+             static_cast<const float*>(pr.d_a_val), reinterpret_cast<float*>(D1),
+             reinterpret_cast<float*>(D), st);
+  } else if (pl.n_ftiles && pl.fused_v2) {
     launch_fused_v2<T>(pl, D1, D, st);
   } else if (pl.n_ftiles) {
     if (pl.fused_smem > 48 * 1024)

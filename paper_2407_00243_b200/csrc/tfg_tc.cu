@@ -1,0 +1,470 @@
+// tfg_tc.cu -- FP32 first op on tcgen05 tensor cores (3xTF32), optionally
+// fused with the wavefront-0 tile's SpMM rows.  See tfg_tc.cuh.
+//
+// Per CTA (one per SM, 320 threads, persistent over tiles):
+//   warp 0      TMA producer: 128-row x 32-column fp32 blocks of B land in a
+//               4-stage ring with the 128-byte swizzle the MMA descriptors use;
+//               the CTA's C slice (pre-split image) is bulk-copied once.
+//   warps 1-4   split each landed block in place into tf32 hi and a tf32 lo
+//               plane (x = hi + lo + O(2^-22 x)), then release it to the MMA.
+//   warp 5      one lane issues tcgen05.mma kind::tf32, M=128, N=BN, K=8:
+//               D += B_lo C_hi + B_hi C_lo + B_hi C_hi per K step into one of
+//               two TMEM accumulators; tcgen05.commit frees ring slots and
+//               hands finished accumulators to the epilogue.
+//   warps 6-9   epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
+//               wavefront 1 reads (spill) or that no stage holds (wide tile),
+//               stage rows the tile's fused rows read, then compute those
+//               fused rows (spmm_row, reference order) into D.
+// The algorithm is the reference's (kernels.hpp:88-126: first-op rows of a
+// tile, then its fused rows); only the arithmetic of the dense product is the
+// tensor cores' (error ~1e-6 relative, inside the 1e-5 fp32 tolerance).
+#include "tfg_tc.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "tfg_device.cuh"
+
+namespace tfg {
+namespace {
+
+using namespace dev;
+
+constexpr int kStages = 4;
+constexpr int kBM = 128;                      // rows per MMA block (M)
+constexpr int kKC = 32;                       // K per ring chunk (one 128-byte swizzle row)
+constexpr int kChunkBytes = kBM * kKC * 4;    // 16 KB
+constexpr int kThreads = 320;
+constexpr size_t kCMax = 64 * 1024;           // resident C slice image (hi + lo)
+constexpr size_t kSmemMax = 227 * 1024;
+constexpr size_t kBarBytes = 256;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n TC_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TC_WAIT_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// K-major operand, 128-byte swizzle: 8-row atoms of 128 B, atoms 1 KB apart
+// (SBO), version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          su32(bar))
+      : "memory");
+}
+// 32 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split4(const float4& x, float4& h, float4& l) {
+  h.x = tf32_rna(x.x);
+  h.y = tf32_rna(x.y);
+  h.z = tf32_rna(x.z);
+  h.w = tf32_rna(x.w);
+  l.x = tf32_rna(x.x - h.x);
+  l.y = tf32_rna(x.y - h.y);
+  l.z = tf32_rna(x.z - h.z);
+  l.w = tf32_rna(x.w - h.w);
+}
+
+// C (bc x cc, row-major) -> per column slice y and K chunk kc: [hi | lo] planes
+// of BN rows (output columns) x 32 K values, 128-byte swizzled (16-byte unit
+// u of row r stored at u ^ (r % 8)), i.e. the K-major operand image.
+__global__ void k_tc_prep_c(const float* __restrict__ C, int bc, int cc, int bn,
+                            float* __restrict__ img) {
+  const int64_t total = (int64_t)bc * cc;
+  const int kchunks = bc / kKC;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / cc), col = (int)(e % cc);
+    const float x = C[e];
+    const float h = tf32_rna(x), l = tf32_rna(x - h);
+    const int y = col / bn, nl = col % bn, kc = k / kKC, kk = k % kKC;
+    const size_t base = (size_t)(y * kchunks + kc) * 2 * bn * kKC;
+    const size_t w = (size_t)(nl / 8) * 256 + (nl % 8) * 32 + (((kk / 4) ^ (nl % 8)) * 4) + kk % 4;
+    img[base + w] = h;
+    img[base + (size_t)bn * kKC + w] = l;
+  }
+}
+
+template <int BN, int LPR>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_tiles(const __grid_constant__ CUtensorMap bmap, int kchunks,
+               const float* __restrict__ cimg, int64_t ntiles, const int* __restrict__ t_ilo,
+               const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
+               const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
+               const int* __restrict__ slot, const uint8_t* __restrict__ spill, int stage_cap,
+               int cc, const int* __restrict__ arp, const int* __restrict__ aci,
+               const float* __restrict__ av, float* D1, float* __restrict__ D) {
+  constexpr int VEC = 4;
+  constexpr int NCH = BN / (LPR * VEC);
+  static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
+  constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
+  static_assert(kTmemCols >= 32 && (kTmemCols & (kTmemCols - 1)) == 0, "TMEM columns");
+  constexpr uint32_t kIdesc = (1u << 4)                       // D format f32
+                              | (2u << 7) | (2u << 10)        // A, B format tf32
+                              | ((uint32_t)(BN >> 3) << 17)   // N
+                              | ((uint32_t)(kBM >> 4) << 24); // M
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  const size_t cbytes = (size_t)kchunks * 2 * BN * kKC * 4;
+  float* sc = reinterpret_cast<float*>(base);
+  unsigned char* ring = base + cbytes;
+  float* stage = reinterpret_cast<float*>(ring + (size_t)kStages * 2 * kChunkBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + (size_t)stage_cap * BN);
+  uint64_t* raw_full = bars;
+  uint64_t* conv_full = bars + kStages;
+  uint64_t* slot_empty = bars + 2 * kStages;
+  uint64_t* acc_full = bars + 3 * kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* c_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.y * BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      bar_init(&raw_full[s], 1);
+      bar_init(&conv_full[s], 128);
+      bar_init(&slot_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&acc_full[a], 1);
+      bar_init(&acc_empty[a], 128);
+    }
+    bar_init(c_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const float* csrc = cimg + (size_t)blockIdx.y * kchunks * 2 * BN * kKC;
+      bar_expect(c_full, (uint32_t)cbytes);
+      for (size_t off = 0; off < cbytes; off += 16384)
+        bulk_1d(reinterpret_cast<unsigned char*>(sc) + off,
+                reinterpret_cast<const unsigned char*>(csrc) + off,
+                (uint32_t)(cbytes - off < 16384 ? cbytes - off : 16384), c_full);
+      uint32_t t = 0;
+      for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+        const int ilo = t_ilo[v], ihi = t_ihi[v];
+        for (int r0 = ilo; r0 < ihi; r0 += kBM)
+          for (int kc = 0; kc < kchunks; ++kc, ++t) {
+            const int s = t % kStages;
+            if (t >= kStages) bar_wait(&slot_empty[s], ((t / kStages) - 1) & 1);
+            bar_expect(&raw_full[s], kChunkBytes);
+            tma_2d(ring + (size_t)s * 2 * kChunkBytes, &bmap, kc * kKC, r0, &raw_full[s]);
+          }
+      }
+    }
+  } else if (warp <= 4) {
+    const int ct = threadIdx.x - 32;
+    uint32_t t = 0;
+    for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+      const int ilo = t_ilo[v], ihi = t_ihi[v];
+      for (int r0 = ilo; r0 < ihi; r0 += kBM)
+        for (int kc = 0; kc < kchunks; ++kc, ++t) {
+          const int s = t % kStages;
+          bar_wait(&raw_full[s], (t / kStages) & 1);
+          float4* hi = reinterpret_cast<float4*>(ring + (size_t)s * 2 * kChunkBytes);
+          float4* lo = hi + kChunkBytes / 16;
+#pragma unroll
+          for (int i = 0; i < kChunkBytes / 16 / 128; ++i) {
+            const int e = ct + i * 128;
+            float4 h, l;
+            split4(hi[e], h, l);
+            hi[e] = h;
+            lo[e] = l;
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          bar_arrive(&conv_full[s]);
+        }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      bar_wait(c_full, 0);
+      const uint32_t sc_addr = su32(sc);
+      const uint32_t ring_addr = su32(ring);
+      uint32_t t = 0, b = 0;
+      for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+        const int ilo = t_ilo[v], ihi = t_ihi[v];
+        for (int r0 = ilo; r0 < ihi; r0 += kBM, ++b) {
+          const int a = b & 1;
+          if (b >= 2) bar_wait(&acc_empty[a], ((b / 2) - 1) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(a * BN);
+          for (int kc = 0; kc < kchunks; ++kc, ++t) {
+            const int s = t % kStages;
+            bar_wait(&conv_full[s], (t / kStages) & 1);
+            tc_fence_after();
+            const uint32_t ah = ring_addr + (uint32_t)(s * 2 * kChunkBytes), al = ah + kChunkBytes;
+            const uint32_t ch = sc_addr + (uint32_t)(kc * 2 * BN * kKC * 4),
+                           cl = ch + (uint32_t)(BN * kKC * 4);
+#pragma unroll
+            for (int ks = 0; ks < kKC / 8; ++ks) {
+              const uint32_t o = (uint32_t)ks * 32;
+              mma_tf32(d, sw128_desc(al + o), sw128_desc(ch + o), kIdesc, (kc | ks) != 0);
+              mma_tf32(d, sw128_desc(ah + o), sw128_desc(cl + o), kIdesc, 1);
+              mma_tf32(d, sw128_desc(ah + o), sw128_desc(ch + o), kIdesc, 1);
+            }
+            mma_commit(&slot_empty[s]);
+          }
+          mma_commit(&acc_full[a]);
+        }
+      }
+    }
+  } else {
+    // epilogue warps 6..9: TMEM lane quarter = warp % 4
+    const int et = threadIdx.x - 192;
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    const bool first_op = t_joff == nullptr;
+    const int gl = et & (LPR - 1);
+    const unsigned gmask = group_mask(LPR);
+    const int group = et / LPR, ngroups = 128 / LPR;
+    uint32_t b = 0;
+    for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+      const int ilo = t_ilo[v], ihi = t_ihi[v];
+      const bool wide = first_op || t_wide[v] != 0;
+      for (int r0 = ilo; r0 < ihi; r0 += kBM, ++b) {
+        const int a = b & 1;
+        bar_wait(&acc_full[a], (b / 2) & 1);
+        tc_fence_after();
+        const int row = r0 + m;
+        const bool valid = row < ihi;
+        const bool sp = valid && (wide || spill[row]);
+        const int sl = (valid && !wide) ? slot[row] : -1;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float x[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
+          if (sp) {
+            float4* o = reinterpret_cast<float4*>(D1 + (size_t)row * cc + n0 + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          }
+          if (sl >= 0) {
+            float4* o = reinterpret_cast<float4*>(stage + (size_t)sl * BN + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          }
+        }
+        tc_fence_before();
+        bar_arrive(&acc_empty[a]);
+      }
+      if (first_op) continue;
+      const int64_t jb = t_joff[v], je = t_joff[v + 1];
+      if (je == jb) continue;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // staged / spilled rows visible
+      for (int64_t qq = jb + group; qq < je; qq += ngroups) {
+        const int j = jrows[qq];
+        const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
+        float acc2[NCH][VEC];
+        if (wide) {
+          auto xl = [&](int c, int chn, float(&xx)[VEC]) {
+            ldv<float, VEC>(xx, D1 + (size_t)c * cc + n0 + (chn * LPR + gl) * VEC);
+          };
+          spmm_row<float, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc2);
+        } else {
+          auto xl = [&](int c, int chn, float(&xx)[VEC]) {
+            ldv<float, VEC>(xx, stage + (size_t)__ldg(slot + c) * BN + (chn * LPR + gl) * VEC);
+          };
+          spmm_row<float, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc2);
+        }
+        float* o = D + (size_t)j * cc + n0;
+#pragma unroll
+        for (int chn = 0; chn < NCH; ++chn) stv<float, VEC>(o + (chn * LPR + gl) * VEC, acc2[chn]);
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // stage free for the next tile
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(kTmemCols));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+size_t fixed_bytes(const TcPlan& tc) {
+  return 1024 + (size_t)tc.kchunks * 2 * tc.bn * kKC * 4 + (size_t)kStages * 2 * kChunkBytes +
+         kBarBytes;
+}
+
+}  // namespace
+
+int tc_env_enabled() {
+  const char* e = getenv("TFG_TC");
+  return e ? atoi(e) : 1;
+}
+
+bool tc_prepare(TcPlan& tc, const float* B, int n, int bc, int cc) {
+  tc.on = false;
+  if (!tc_env_enabled()) return false;
+  if (bc < kKC || bc % kKC != 0 || (uintptr_t)B % 16 != 0) return false;
+  int bn = 0;
+  for (int c : {128, 64, 32})
+    if (cc % c == 0 && (size_t)bc * c * 8 <= kCMax) {
+      bn = c;
+      break;
+    }
+  if (!bn) return false;
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)bc, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)bc * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kBM};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(&tc.bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides, box,
+          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  tc.bn = bn;
+  tc.slices = cc / bn;
+  tc.kchunks = bc / kKC;
+  tc.cimg.alloc((size_t)bc * cc * 2);
+  tc.stage_cap = 0;
+  tc.smem = fixed_bytes(tc);
+  tc.on = true;
+  return true;
+}
+
+size_t tc_stage_bytes(const TcPlan& tc) {
+  const size_t f = fixed_bytes(tc);
+  return f < kSmemMax ? kSmemMax - f : 0;
+}
+
+void tc_finalize(TcPlan& tc, int stage_cap) {
+  tc.stage_cap = stage_cap;
+  tc.smem = fixed_bytes(tc) + (size_t)stage_cap * tc.bn * 4;
+}
+
+void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st) {
+  const int64_t total = (int64_t)bc * cc;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
+  k_tc_prep_c<<<blocks, 256, 0, st>>>(C, bc, cc, tc.bn, tc.cimg.p);
+  TFG_LAUNCH_CHECK();
+}
+
+void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* ilo,
+            const int* ihi, const int64_t* joff, const int* jrows, const uint8_t* wide,
+            const int* slot, const uint8_t* spill, const int* arp, const int* aci,
+            const float* av, float* D1, float* D, cudaStream_t st) {
+  (void)n;
+  (void)bc;
+  if (!ntiles) return;
+  auto launch = [&](auto kern) {
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.smem));
+    // all column slices of a tile run concurrently so B blocks are read from
+    // HBM once and hit L2 for the other slices
+    const int64_t gx =
+        std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
+    kern<<<dim3((unsigned)gx, (unsigned)tc.slices), kThreads, tc.smem, st>>>(
+        tc.bmap, tc.kchunks, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
+        tc.stage_cap, cc, arp, aci, av, D1, D);
+  };
+  if (tc.bn == 128)
+    launch(k_tc_tiles<128, 32>);
+  else if (tc.bn == 64)
+    launch(k_tc_tiles<64, 16>);
+  else
+    launch(k_tc_tiles<32, 8>);
+  TFG_LAUNCH_CHECK();
+}
+
+}  // namespace tfg
