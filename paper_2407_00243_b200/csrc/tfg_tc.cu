@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
                const int* __restrict__ slot, const uint8_t* __restrict__ spill, int stage_cap,
                int cc, const int* __restrict__ arp, const int* __restrict__ aci,
-               const float* __restrict__ av, float* D1, float* __restrict__ D) {
+               const float* __restrict__ av, float* D1, float* __restrict__ D, int dbg) {
   constexpr int VEC = 4;
   constexpr int NCH = BN / (LPR * VEC);
   static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4* lo = hi + kChunkBytes / 16;
 #pragma unroll
           for (int i = 0; i < kChunkBytes / 16 / 128; ++i) {
+            if (dbg & 1) break;
             const int e = ct + i * 128;
             float4 h, l;
             split4(hi[e], h, l);
@@ -280,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            cl = ch + (uint32_t)(BN * kKC * 4);
 #pragma unroll
             for (int ks = 0; ks < kKC / 8; ++ks) {
+              if ((dbg & 2) && (kc | ks)) break;
               const uint32_t o = (uint32_t)ks * 32;
               mma_tf32(d, sw128_desc(al + o), sw128_desc(ch + o), kIdesc, (kc | ks) != 0);
               mma_tf32(d, sw128_desc(ah + o), sw128_desc(cl + o), kIdesc, 1);
@@ -316,13 +318,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float x[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
-          if (sp) {
+          if (sp && !(dbg & 8)) {
             float4* o = reinterpret_cast<float4*>(D1 + (size_t)row * cc + n0 + c0);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
           }
-          if (sl >= 0) {
+          if (sl >= 0 && !(dbg & 8)) {
             float4* o = reinterpret_cast<float4*>(stage + (size_t)sl * BN + c0);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (first_op) continue;
       const int64_t jb = t_joff[v], je = t_joff[v + 1];
-      if (je == jb) continue;
+      if (je == jb || (dbg & 4)) continue;
       asm volatile("bar.sync 1, 128;\n" ::: "memory");  // staged / spilled rows visible
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
@@ -448,6 +450,10 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
   (void)n;
   (void)bc;
   if (!ntiles) return;
+  static const int dbg = [] {
+    const char* e = getenv("TFG_TC_DBG");  // timing experiments only: skips work
+    return e ? atoi(e) : 0;
+  }();
   auto launch = [&](auto kern) {
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.smem));
     // all column slices of a tile run concurrently so B blocks are read from
@@ -456,7 +462,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), kThreads, tc.smem, st>>>(
         tc.bmap, tc.kchunks, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
-        tc.stage_cap, cc, arp, aci, av, D1, D);
+        tc.stage_cap, cc, arp, aci, av, D1, D, dbg);
   };
   if (tc.bn == 128)
     launch(k_tc_tiles<128, 32>);
