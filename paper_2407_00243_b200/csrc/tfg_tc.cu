@@ -1,20 +1,26 @@
 // tfg_tc.cu -- FP32 first op on tcgen05 tensor cores (3xTF32), optionally
 // fused with the wavefront-0 tile's SpMM rows.  See tfg_tc.cuh.
 //
-// Per CTA (one per SM, 320 threads, persistent over tiles):
+// Per CTA (one per SM, 448 threads, persistent over tiles):
 //   warp 0      TMA producer: 128-row x 32-column fp32 blocks of B land in a
-//               4-stage ring with the 128-byte swizzle the MMA descriptors use;
-//               the CTA's C slice (pre-split image) is bulk-copied once.
-//   warps 1-4   split each landed block in place into tf32 hi and a tf32 lo
-//               plane (x = hi + lo + O(2^-22 x)), then release it to the MMA.
-//   warp 5      one lane issues tcgen05.mma kind::tf32, M=128, N=BN, K=8:
-//               D += B_lo C_hi + B_hi C_lo + B_hi C_hi per K step into one of
-//               two TMEM accumulators; tcgen05.commit frees ring slots and
-//               hands finished accumulators to the epilogue.
-//   warps 6-9   epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
+//               ring of raw shared-memory slots (128-byte swizzle); the CTA's
+//               C slice (pre-split tf32 hi/lo image, K-major) is bulk-copied
+//               once and stays resident.
+//   warps 1-4   converters, one block row per thread: read the row's 32
+//               values, free the raw slot, split x = hi + lo (tf32 each,
+//               error O(2^-22 x)) and tcgen05.st both planes into a TMEM
+//               operand stage.
+//   warp 5      one lane issues tcgen05.mma kind::tf32 with A from TMEM and
+//               B (C) from shared memory, M=128, N=BN, K=8:
+//               D += B_lo C_hi + B_hi C_lo + B_hi C_hi into one of two TMEM
+//               accumulators; tcgen05.commit frees operand stages and hands
+//               finished accumulators to the epilogue.
+//   warps 6-13  epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
 //               wavefront 1 reads (spill) or that no stage holds (wide tile),
 //               stage rows the tile's fused rows read, then compute those
 //               fused rows (spmm_row, reference order) into D.
+// Shared memory carries only the raw B blocks and C: the split operand lives
+// in TMEM, so the MMAs do not compete with the converters for SMEM bandwidth.
 // The algorithm is the reference's (kernels.hpp:88-126: first-op rows of a
 // tile, then its fused rows); only the arithmetic of the dense product is the
 // tensor cores' (error ~1e-6 relative, inside the 1e-5 fp32 tolerance).
@@ -37,8 +43,8 @@ constexpr int kStages = 4;
 constexpr int kBM = 128;                      // rows per MMA block (M)
 constexpr int kKC = 32;                       // K per ring chunk (one 128-byte swizzle row)
 constexpr int kChunkBytes = kBM * kKC * 4;    // 16 KB
-constexpr int kThreads = 320;
-constexpr size_t kCMax = 64 * 1024;           // resident C slice image (hi + lo)
+constexpr int kThreads = 448;  // 1 TMA + 4 convert + 1 MMA + 8 epilogue warps
+constexpr size_t kCMax = 128 * 1024;          // resident C slice image (hi + lo)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kBarBytes = 256;
 
@@ -91,51 +97,17 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
          ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
           su32(bar))
       : "memory");
 }
-// 32 consecutive fp32 columns of this thread's TMEM lane.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-__device__ __forceinline__ void split4(const float4& x, float4& h, float4& l) {
-  h.x = tf32_rna(x.x);
-  h.y = tf32_rna(x.y);
-  h.z = tf32_rna(x.z);
-  h.w = tf32_rna(x.w);
-  l.x = tf32_rna(x.x - h.x);
-  l.y = tf32_rna(x.y - h.y);
-  l.z = tf32_rna(x.z - h.z);
-  l.w = tf32_rna(x.w - h.w);
-}
-
 // C (bc x cc, row-major) -> per column slice y and K chunk kc: [hi | lo] planes
 // of BN rows (output columns) x 32 K values, 128-byte swizzled (16-byte unit
 // u of row r stored at u ^ (r % 8)), i.e. the K-major operand image.
@@ -156,9 +128,56 @@ __global__ void k_tc_prep_c(const float* __restrict__ C, int bc, int cc, int bn,
   }
 }
 
+// 16 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 32 consecutive fp32 columns into this thread's TMEM lane.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem desc]^T
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// TMEM columns: [0, 2*BN) two accumulators, then kOpStages x 64 operand
+// columns (32 tf32 hi + 32 tf32 lo per row of the 128-row block).
+constexpr int kOpStages = 4;
+constexpr uint32_t kTmemCols = 512;
+
 template <int BN, int LPR>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_tc_tiles(const __grid_constant__ CUtensorMap bmap, int kchunks,
+    k_tc_tiles(const __grid_constant__ CUtensorMap bmap, int kchunks, int raw_stages,
                const float* __restrict__ cimg, int64_t ntiles, const int* __restrict__ t_ilo,
                const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
                const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
@@ -168,8 +187,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int VEC = 4;
   constexpr int NCH = BN / (LPR * VEC);
   static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
-  constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
-  static_assert(kTmemCols >= 32 && (kTmemCols & (kTmemCols - 1)) == 0, "TMEM columns");
+  static_assert(2 * BN + kOpStages * 64 <= (int)kTmemCols, "TMEM budget");
+  constexpr int kHalf = BN / 2;  // columns per epilogue warp
+  static_assert(kHalf % 16 == 0, "epilogue column split");
   constexpr uint32_t kIdesc = (1u << 4)                       // D format f32
                               | (2u << 7) | (2u << 10)        // A, B format tf32
                               | ((uint32_t)(BN >> 3) << 17)   // N
@@ -178,28 +198,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const size_t cbytes = (size_t)kchunks * 2 * BN * kKC * 4;
   float* sc = reinterpret_cast<float*>(base);
-  unsigned char* ring = base + cbytes;
-  float* stage = reinterpret_cast<float*>(ring + (size_t)kStages * 2 * kChunkBytes);
+  unsigned char* ring = base + cbytes;  // raw_stages x 16 KB of fp32 B blocks (swizzled)
+  float* stage = reinterpret_cast<float*>(ring + (size_t)raw_stages * kChunkBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage + (size_t)stage_cap * BN);
-  uint64_t* raw_full = bars;
-  uint64_t* conv_full = bars + kStages;
-  uint64_t* slot_empty = bars + 2 * kStages;
-  uint64_t* acc_full = bars + 3 * kStages;
-  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* raw_full = bars;                   // [raw_stages] TMA landed
+  uint64_t* raw_empty = bars + raw_stages;     // [raw_stages] converters read it
+  uint64_t* op_full = raw_empty + raw_stages;  // [kOpStages] hi/lo in TMEM
+  uint64_t* op_empty = op_full + kOpStages;    // [kOpStages] MMAs done with it
+  uint64_t* acc_full = op_empty + kOpStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;          // [2]
   uint64_t* c_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.y * BN;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < raw_stages; ++s) {
       bar_init(&raw_full[s], 1);
-      bar_init(&conv_full[s], 128);
-      bar_init(&slot_empty[s], 1);
+      bar_init(&raw_empty[s], 128);
+    }
+    for (int s = 0; s < kOpStages; ++s) {
+      bar_init(&op_full[s], 128);
+      bar_init(&op_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&acc_full[a], 1);
-      bar_init(&acc_empty[a], 128);
+      bar_init(&acc_empty[a], 256);
     }
     bar_init(c_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -214,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t op_col0 = 2 * BN;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -228,42 +253,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ilo = t_ilo[v], ihi = t_ihi[v];
         for (int r0 = ilo; r0 < ihi; r0 += kBM)
           for (int kc = 0; kc < kchunks; ++kc, ++t) {
-            const int s = t % kStages;
-            if (t >= kStages) bar_wait(&slot_empty[s], ((t / kStages) - 1) & 1);
+            const int s = t % raw_stages;
+            if (t >= (uint32_t)raw_stages) bar_wait(&raw_empty[s], ((t / raw_stages) - 1) & 1);
             bar_expect(&raw_full[s], kChunkBytes);
-            tma_2d(ring + (size_t)s * 2 * kChunkBytes, &bmap, kc * kKC, r0, &raw_full[s]);
+            tma_2d(ring + (size_t)s * kChunkBytes, &bmap, kc * kKC, r0, &raw_full[s]);
           }
       }
     }
   } else if (warp <= 4) {
-    const int ct = threadIdx.x - 32;
+    // converters: one row of the 128-row block per thread, TMEM lane quarter
+    // = warp % 4 (the lanes a warp may access)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_bits = (uint32_t)(q * 32) << 16;
     uint32_t t = 0;
     for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
       const int ilo = t_ilo[v], ihi = t_ihi[v];
       for (int r0 = ilo; r0 < ihi; r0 += kBM)
         for (int kc = 0; kc < kchunks; ++kc, ++t) {
-          const int s = t % kStages;
-          bar_wait(&raw_full[s], (t / kStages) & 1);
-          float4* hi = reinterpret_cast<float4*>(ring + (size_t)s * 2 * kChunkBytes);
-          float4* lo = hi + kChunkBytes / 16;
+          const int s = t % raw_stages, so = t % kOpStages;
+          bar_wait(&raw_full[s], (t / raw_stages) & 1);
+          const float4* src = reinterpret_cast<const float4*>(ring + (size_t)s * kChunkBytes +
+                                                              (size_t)r * 128);
+          float x[32];
 #pragma unroll
-          for (int i = 0; i < kChunkBytes / 16 / 128; ++i) {
-            if (dbg & 1) break;
-            const int e = ct + i * 128;
-            float4 h, l;
-            split4(hi[e], h, l);
-            hi[e] = h;
-            lo[e] = l;
+          for (int u = 0; u < 8; ++u) {
+            const float4 f = src[u ^ (r & 7)];
+            x[4 * u] = f.x;
+            x[4 * u + 1] = f.y;
+            x[4 * u + 2] = f.z;
+            x[4 * u + 3] = f.w;
           }
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          bar_arrive(&conv_full[s]);
+          bar_arrive(&raw_empty[s]);  // values are in registers: slot may be refilled
+          float h[32], l[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            h[i] = (dbg & 1) ? x[i] : tf32_rna(x[i]);
+            l[i] = (dbg & 1) ? x[i] : tf32_rna(x[i] - h[i]);
+          }
+          if (t >= (uint32_t)kOpStages) bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
+          tc_fence_after();
+          const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64;
+          tmem_st32(col, h);
+          tmem_st32(col + 32, l);
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          tc_fence_before();
+          bar_arrive(&op_full[so]);
         }
     }
   } else if (warp == 5) {
     if (lane == 0) {
       bar_wait(c_full, 0);
       const uint32_t sc_addr = su32(sc);
-      const uint32_t ring_addr = su32(ring);
       uint32_t t = 0, b = 0;
       for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
         const int ilo = t_ilo[v], ihi = t_ihi[v];
@@ -273,35 +314,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(a * BN);
           for (int kc = 0; kc < kchunks; ++kc, ++t) {
-            const int s = t % kStages;
-            bar_wait(&conv_full[s], (t / kStages) & 1);
+            const int so = t % kOpStages;
+            bar_wait(&op_full[so], (t / kOpStages) & 1);
             tc_fence_after();
-            const uint32_t ah = ring_addr + (uint32_t)(s * 2 * kChunkBytes), al = ah + kChunkBytes;
+            const uint32_t ah = tmem + op_col0 + (uint32_t)so * 64, al = ah + 32;
             const uint32_t ch = sc_addr + (uint32_t)(kc * 2 * BN * kKC * 4),
                            cl = ch + (uint32_t)(BN * kKC * 4);
 #pragma unroll
             for (int ks = 0; ks < kKC / 8; ++ks) {
               if ((dbg & 2) && (kc | ks)) break;
-              const uint32_t o = (uint32_t)ks * 32;
-              mma_tf32(d, sw128_desc(al + o), sw128_desc(ch + o), kIdesc, (kc | ks) != 0);
-              mma_tf32(d, sw128_desc(ah + o), sw128_desc(cl + o), kIdesc, 1);
-              mma_tf32(d, sw128_desc(ah + o), sw128_desc(ch + o), kIdesc, 1);
+              const uint32_t o = (uint32_t)ks * 32;  // 8 tf32 = 32 bytes of the swizzled row
+              mma_tf32_ts(d, al + ks * 8, sw128_desc(ch + o), kIdesc, (kc | ks) != 0);
+              mma_tf32_ts(d, ah + ks * 8, sw128_desc(cl + o), kIdesc, 1);
+              mma_tf32_ts(d, ah + ks * 8, sw128_desc(ch + o), kIdesc, 1);
             }
-            mma_commit(&slot_empty[s]);
+            mma_commit(&op_empty[so]);
           }
           mma_commit(&acc_full[a]);
         }
       }
     }
   } else {
-    // epilogue warps 6..9: TMEM lane quarter = warp % 4
+    // epilogue warps 6..13: TMEM lane quarter = warp % 4, column half h
     const int et = threadIdx.x - 192;
-    const int q = warp & 3;
+    const int q = warp & 3, h = (warp - 6) >> 2;
     const int m = q * 32 + lane;
     const bool first_op = t_joff == nullptr;
     const int gl = et & (LPR - 1);
     const unsigned gmask = group_mask(LPR);
-    const int group = et / LPR, ngroups = 128 / LPR;
+    const int group = et / LPR, ngroups = 256 / LPR;
     uint32_t b = 0;
     for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
       const int ilo = t_ilo[v], ihi = t_ihi[v];
@@ -315,19 +356,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool sp = valid && (wide || spill[row]);
         const int sl = (valid && !wide) ? slot[row] : -1;
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float x[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
+        for (int c0 = h * kHalf; c0 < (h + 1) * kHalf; c0 += 16) {
+          float x[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
           if (sp && !(dbg & 8)) {
             float4* o = reinterpret_cast<float4*>(D1 + (size_t)row * cc + n0 + c0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 4; ++j)
               o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
           }
           if (sl >= 0 && !(dbg & 8)) {
             float4* o = reinterpret_cast<float4*>(stage + (size_t)sl * BN + c0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 4; ++j)
               o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
           }
         }
@@ -337,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (first_op) continue;
       const int64_t jb = t_joff[v], je = t_joff[v + 1];
       if (je == jb || (dbg & 4)) continue;
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // staged / spilled rows visible
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");  // staged / spilled rows visible
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
         const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
@@ -357,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int chn = 0; chn < NCH; ++chn) stv<float, VEC>(o + (chn * LPR + gl) * VEC, acc2[chn]);
       }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // stage free for the next tile
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");  // stage free for the next tile
     }
   }
   tc_fence_before();
@@ -383,8 +424,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+int raw_stages() {
+  static const int r = [] {
+    const char* e = getenv("TFG_TC_RING");
+    const int v = e ? atoi(e) : kStages;
+    return v < 2 ? 2 : (v > 8 ? 8 : v);
+  }();
+  return r;
+}
+
 size_t fixed_bytes(const TcPlan& tc) {
-  return 1024 + (size_t)tc.kchunks * 2 * tc.bn * kKC * 4 + (size_t)kStages * 2 * kChunkBytes +
+  return 1024 + (size_t)tc.kchunks * 2 * tc.bn * kKC * 4 + (size_t)raw_stages() * kChunkBytes +
          kBarBytes;
 }
 
@@ -400,7 +450,7 @@ bool tc_prepare(TcPlan& tc, const float* B, int n, int bc, int cc) {
   if (!tc_env_enabled()) return false;
   if (bc < kKC || bc % kKC != 0 || (uintptr_t)B % 16 != 0) return false;
   int bn = 0;
-  for (int c : {128, 64, 32})
+  for (int c : {128, 64, 32})  // widest slice whose split C fits (TMEM: 2*BN + 256 <= 512)
     if (cc % c == 0 && (size_t)bc * c * 8 <= kCMax) {
       bn = c;
       break;
@@ -461,7 +511,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
     const int64_t gx =
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), kThreads, tc.smem, st>>>(
-        tc.bmap, tc.kchunks, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
+        tc.bmap, tc.kchunks, raw_stages(), tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
         tc.stage_cap, cc, arp, aci, av, D1, D, dbg);
   };
   if (tc.bn == 128)
