@@ -284,13 +284,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * u + 2] = f.z;
             x[4 * u + 3] = f.w;
           }
-          bar_arrive(&raw_empty[s]);  // values are in registers: slot may be refilled
           float h[32], l[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             h[i] = (dbg & 1) ? x[i] : tf32_rna(x[i]);
             l[i] = (dbg & 1) ? x[i] : tf32_rna(x[i] - h[i]);
           }
+          // the split consumed every loaded value, so the loads are complete:
+          // the slot may be refilled by the next TMA
+          bar_arrive(&raw_empty[s]);
           if (t >= (uint32_t)kOpStages) bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
           tc_fence_after();
           const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64;
