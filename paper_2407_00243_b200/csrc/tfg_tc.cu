@@ -290,8 +290,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             h[i] = (dbg & 1) ? x[i] : tf32_rna(x[i]);
             l[i] = (dbg & 1) ? x[i] : tf32_rna(x[i] - h[i]);
           }
-          // the split consumed every loaded value, so the loads are complete:
-          // the slot may be refilled by the next TMA
+          // the slot is refilled by the TMA (async proxy): order these generic
+          // reads before that write, then release the slot
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           bar_arrive(&raw_empty[s]);
           if (t >= (uint32_t)kOpStages) bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
           tc_fence_after();
