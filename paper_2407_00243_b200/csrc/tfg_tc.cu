@@ -427,17 +427,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int raw_stages() {
-  static const int r = [] {
-    const char* e = getenv("TFG_TC_RING");
-    const int v = e ? atoi(e) : kStages;
-    return v < 2 ? 2 : (v > 8 ? 8 : v);
-  }();
-  return r;
+int env_raw_stages() {  // TFG_TC_RING: raw ring depth (tests stress 2)
+  const char* e = getenv("TFG_TC_RING");
+  const int v = e ? atoi(e) : kStages;
+  return v < 2 ? 2 : (v > 8 ? 8 : v);
 }
 
 size_t fixed_bytes(const TcPlan& tc) {
-  return 1024 + (size_t)tc.kchunks * 2 * tc.bn * kKC * 4 + (size_t)raw_stages() * kChunkBytes +
+  return 1024 + (size_t)tc.kchunks * 2 * tc.bn * kKC * 4 + (size_t)tc.raw * kChunkBytes +
          kBarBytes;
 }
 
@@ -470,6 +467,8 @@ bool tc_prepare(TcPlan& tc, const float* B, int n, int bc, int cc) {
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   tc.bn = bn;
+  tc.raw = env_raw_stages();
+  if (fixed_bytes(tc) > kSmemMax) return false;
   tc.slices = cc / bn;
   tc.kchunks = bc / kKC;
   tc.cimg.alloc((size_t)bc * cc * 2);
@@ -514,7 +513,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
     const int64_t gx =
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), kThreads, tc.smem, st>>>(
-        tc.bmap, tc.kchunks, raw_stages(), tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
+        tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
         tc.stage_cap, cc, arp, aci, av, D1, D, dbg);
   };
   if (tc.bn == 128)

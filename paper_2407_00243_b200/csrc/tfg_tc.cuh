@@ -22,6 +22,7 @@ struct TcPlan {
   int bn = 0;         // column slice (MMA N)
   int slices = 0;     // cc / bn (gridDim.y)
   int kchunks = 0;    // bc / 32
+  int raw = 4;        // raw B slots in the shared-memory ring
   int stage_cap = 0;  // staged D1 rows per fused tile
   size_t smem = 0;    // dynamic shared memory per CTA
   alignas(64) CUtensorMap bmap;  // B: n x bc fp32, box 32 x 128, 128B swizzle

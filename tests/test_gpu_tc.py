@@ -92,3 +92,22 @@ def test_tc_dense_rows_exact_inputs(cuda, monkeypatch):
     want = dense_a @ (b.astype(np.float64) @ c.astype(np.float64))
     got = P.fused_gemm_spmm(a, b, c, dtype=np.float32, ct_size=128)
     assert np.array_equal(got.astype(np.float64), want)
+
+
+@pytest.mark.parametrize("ring", ["2", "3"])
+def test_tc_shallow_ring_many_blocks(cuda, oracle, monkeypatch, ring):
+    """Many 128-row blocks per CTA through a 2-3 slot TMA ring: every slot is
+    refilled many times, so a missing ordering between the converters'
+    reads and the next TMA write shows up as wrong rows."""
+    monkeypatch.setenv("TFG_TC", "1")
+    monkeypatch.setenv("TFG_TC_RING", ring)
+    n, bc, cc = 150000, 128, 64
+    rng = np.random.default_rng(17)
+    rp, ci, v = oracle.gen_banded(n, 1)
+    b = rng.standard_normal((n, bc)).astype(np.float32)
+    c = (rng.standard_normal((bc, cc)) / 11).astype(np.float32)
+    a = P.Csr(n, n, rp, ci, v)
+    prob = P.DeviceProblem(a, b, c, np.float32)
+    got = P.Plan(prob, None).execute().cpu().numpy()
+    want = oracle.run(n, (rp, ci, v), b, c, None, np.float32, workers=8)
+    assert max_rel_err(got, want) <= TOL[4]
