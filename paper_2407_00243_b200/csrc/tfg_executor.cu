@@ -2576,6 +2576,33 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         for (int c : tc) max_need = std::max(max_need, c);
         size_t row_bytes = (size_t)BN * pl.elem;
         if (pl.tc.on) {  // tensor-core tiles: one CTA per SM, stage after ring + C
+          // column slice: wider slices read B fewer times, narrower ones leave
+          // more shared memory for staged D1 rows; fused rows of tiles that do
+          // not fit gather D1 from L2 (weighted 2x: random 4-16 B-per-lane
+          // gathers against streamed TMA blocks)
+          std::vector<int64_t> tnnz(pl.n_ftiles, 0);
+          int64_t ft_rows = 0;
+          for (int64_t v = 0; v < pl.n_ftiles; ++v) {
+            ft_rows += f_ihi[v] - f_ilo[v];
+            for (int64_t q = f_joff[v]; q < f_joff[v + 1]; ++q)
+              tnnz[v] += arp[f_rows[q] + 1] - arp[f_rows[q]];
+          }
+          int best_bn = pl.tc.bn;
+          double best = 1e300;
+          const char* env_bn = getenv("TFG_TC_BN");
+          for (int bnc = pl.tc.bn; bnc >= 32 && cc % bnc == 0; bnc /= 2) {
+            const int capc = (int)std::min<size_t>(tc_stage_bytes_bn(pl.tc, bnc) / ((size_t)bnc * 4),
+                                                   (size_t)max_need);
+            int64_t wide_nnz = 0;
+            for (int64_t v = 0; v < pl.n_ftiles; ++v)
+              if (tc[v] > capc) wide_nnz += tnnz[v];
+            const double cost = (double)(cc / bnc) * ft_rows * bc * 4 + 2.0 * wide_nnz * cc * 4;
+            if (env_bn ? bnc == atoi(env_bn) : cost < best) {
+              best = env_bn ? -1.0 : cost;
+              best_bn = bnc;
+            }
+          }
+          if (best_bn != pl.tc.bn) tc_set_bn(pl.tc, best_bn);
           cap_bytes = tc_stage_bytes(pl.tc);
           row_bytes = (size_t)pl.tc.bn * 4;
           pl.cs = pl.tc.bn;

@@ -1,21 +1,20 @@
 // tfg_tc.cu -- FP32 first op on tcgen05 tensor cores (3xTF32), optionally
 // fused with the wavefront-0 tile's SpMM rows.  See tfg_tc.cuh.
 //
-// Per CTA (one per SM, 448 threads, persistent over tiles):
+// Per CTA (one per SM, 576 threads, persistent over tiles):
 //   warp 0      TMA producer: 128-row x 32-column fp32 blocks of B land in a
 //               ring of raw shared-memory slots (128-byte swizzle); the CTA's
 //               C slice (pre-split tf32 hi/lo image, K-major) is bulk-copied
 //               once and stays resident.
-//   warps 1-4   converters, one block row per thread: read the row's 32
-//               values, free the raw slot, split x = hi + lo (tf32 each,
-//               error O(2^-22 x)) and tcgen05.st both planes into a TMEM
-//               operand stage.
-//   warp 5      one lane issues tcgen05.mma kind::tf32 with A from TMEM and
+//   warps 1-8   converters, half a block row per thread: read 16 values,
+//               split x = hi + lo (tf32 each, error < 2^-20 x), free the raw
+//               slot and tcgen05.st both planes into a TMEM operand stage.
+//   warp 9      one lane issues tcgen05.mma kind::tf32 with A from TMEM and
 //               B (C) from shared memory, M=128, N=BN, K=8:
 //               D += B_lo C_hi + B_hi C_lo + B_hi C_hi into one of two TMEM
 //               accumulators; tcgen05.commit frees operand stages and hands
 //               finished accumulators to the epilogue.
-//   warps 6-13  epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
+//   warps 10-17 epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
 //               wavefront 1 reads (spill) or that no stage holds (wide tile),
 //               stage rows the tile's fused rows read, then compute those
 //               fused rows (spmm_row, reference order) into D.
@@ -43,7 +42,7 @@ constexpr int kStages = 4;
 constexpr int kBM = 128;                      // rows per MMA block (M)
 constexpr int kKC = 32;                       // K per ring chunk (one 128-byte swizzle row)
 constexpr int kChunkBytes = kBM * kKC * 4;    // 16 KB
-constexpr int kThreads = 448;  // 1 TMA + 4 convert + 1 MMA + 8 epilogue warps
+constexpr int kThreads = 576;  // 1 TMA + 8 convert + 1 MMA + 8 epilogue warps
 constexpr size_t kCMax = 128 * 1024;          // resident C slice image (hi + lo)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kBarBytes = 256;
@@ -65,7 +64,7 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n TC_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       " @!p bra TC_WAIT_%=;\n}\n" ::"r"(su32(b)),
       "r"(parity)
       : "memory");
@@ -142,24 +141,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-// 32 consecutive fp32 columns into this thread's TMEM lane.
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+// 16 consecutive fp32 columns into this thread's TMEM lane.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(
-          taddr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};\n" ::"r"(taddr),
       "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
       "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
       "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
       "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
-      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
-      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
-      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
-      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
-      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      "r"(__float_as_uint(v[15]))
       : "memory");
+}
+// x = hi + lo with hi = x truncated to tf32 (exact) and lo = x - hi (exact in
+// fp32, |lo| < 2^-10 |x|); the tensor core reads lo at tf32 precision, so the
+// split represents x to 2^-20 relative.  Non-finite x: hi = x, lo = 0.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = hi == x ? 0.f : x - hi;
 }
 // D[tmem] (+)= A[tmem] . B[smem desc]^T
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < raw_stages; ++s) {
       bar_init(&raw_full[s], 1);
-      bar_init(&raw_empty[s], 128);
+      bar_init(&raw_empty[s], 256);
     }
     for (int s = 0; s < kOpStages; ++s) {
-      bar_init(&op_full[s], 128);
+      bar_init(&op_full[s], 256);
       bar_init(&op_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bar_init(c_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      su32(tmem_slot)),
                  "n"(kTmemCols));
@@ -260,10 +260,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       }
     }
-  } else if (warp <= 4) {
-    // converters: one row of the 128-row block per thread, TMEM lane quarter
-    // = warp % 4 (the lanes a warp may access)
-    const int q = warp & 3;
+  } else if (warp <= 8) {
+    // converters: half a row (16 K values) of the 128-row block per thread,
+    // TMEM lane quarter = warp % 4 (the lanes a warp may access)
+    const int q = warp & 3, hh = (warp - 1) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_bits = (uint32_t)(q * 32) << 16;
     uint32_t t = 0;
@@ -275,20 +275,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           bar_wait(&raw_full[s], (t / raw_stages) & 1);
           const float4* src = reinterpret_cast<const float4*>(ring + (size_t)s * kChunkBytes +
                                                               (size_t)r * 128);
-          float x[32];
+          float x[16];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float4 f = src[u ^ (r & 7)];
+          for (int u = 0; u < 4; ++u) {
+            const float4 f = src[(hh * 4 + u) ^ (r & 7)];
             x[4 * u] = f.x;
             x[4 * u + 1] = f.y;
             x[4 * u + 2] = f.z;
             x[4 * u + 3] = f.w;
           }
-          float h[32], l[32];
+          float h[16], l[16];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            h[i] = (dbg & 1) ? x[i] : tf32_rna(x[i]);
-            l[i] = (dbg & 1) ? x[i] : tf32_rna(x[i] - h[i]);
+          for (int i = 0; i < 16; ++i) {
+            if (dbg & 1) {
+              h[i] = l[i] = x[i];
+            } else {
+              split_tf32(x[i], h[i], l[i]);
+            }
           }
           // the slot is refilled by the TMA (async proxy): order these generic
           // reads before that write, then release the slot
@@ -296,15 +299,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           bar_arrive(&raw_empty[s]);
           if (t >= (uint32_t)kOpStages) bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
           tc_fence_after();
-          const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64;
-          tmem_st32(col, h);
-          tmem_st32(col + 32, l);
+          const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64 + hh * 16;
+          tmem_st16(col, h);
+          tmem_st16(col + 32, l);
           asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
           tc_fence_before();
           bar_arrive(&op_full[so]);
         }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       bar_wait(c_full, 0);
       const uint32_t sc_addr = su32(sc);
@@ -338,9 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue warps 6..13: TMEM lane quarter = warp % 4, column half h
-    const int et = threadIdx.x - 192;
-    const int q = warp & 3, h = (warp - 6) >> 2;
+    // epilogue warps 10..17: TMEM lane quarter = warp % 4, column half h
+    const int et = threadIdx.x - 320;
+    const int q = warp & 3, h = (warp - 10) >> 2;
     const int m = q * 32 + lane;
     const bool first_op = t_joff == nullptr;
     const int gl = et & (LPR - 1);
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "n"(kTmemCols));
@@ -433,10 +436,10 @@ int env_raw_stages() {  // TFG_TC_RING: raw ring depth (tests stress 2)
   return v < 2 ? 2 : (v > 8 ? 8 : v);
 }
 
-size_t fixed_bytes(const TcPlan& tc) {
-  return 1024 + (size_t)tc.kchunks * 2 * tc.bn * kKC * 4 + (size_t)tc.raw * kChunkBytes +
-         kBarBytes;
+size_t fixed_bytes_bn(const TcPlan& tc, int bn) {
+  return 1024 + (size_t)tc.kchunks * 2 * bn * kKC * 4 + (size_t)tc.raw * kChunkBytes + kBarBytes;
 }
+size_t fixed_bytes(const TcPlan& tc) { return fixed_bytes_bn(tc, tc.bn); }
 
 }  // namespace
 
@@ -478,9 +481,19 @@ bool tc_prepare(TcPlan& tc, const float* B, int n, int bc, int cc) {
   return true;
 }
 
-size_t tc_stage_bytes(const TcPlan& tc) {
-  const size_t f = fixed_bytes(tc);
+size_t tc_stage_bytes(const TcPlan& tc) { return tc_stage_bytes_bn(tc, tc.bn); }
+
+size_t tc_stage_bytes_bn(const TcPlan& tc, int bn) {
+  const size_t f = fixed_bytes_bn(tc, bn);
   return f < kSmemMax ? kSmemMax - f : 0;
+}
+
+void tc_set_bn(TcPlan& tc, int bn) {
+  if (bn < 32 || bn % 32 != 0 || (tc.slices * tc.bn) % bn != 0)
+    throw invalid_argument("tc: bad column slice");
+  tc.slices = tc.slices * tc.bn / bn;
+  tc.bn = bn;
+  tc.smem = fixed_bytes(tc) + (size_t)tc.stage_cap * bn * 4;
 }
 
 void tc_finalize(TcPlan& tc, int stage_cap) {

@@ -33,6 +33,9 @@ struct TcPlan {
 bool tc_prepare(TcPlan& tc, const float* B, int n, int bc, int cc);
 // Shared memory left for the fused stage (bytes) once the ring and C fit.
 size_t tc_stage_bytes(const TcPlan& tc);
+size_t tc_stage_bytes_bn(const TcPlan& tc, int bn);
+// Narrow the column slice (more slices, more room for the fused stage).
+void tc_set_bn(TcPlan& tc, int bn);
 void tc_finalize(TcPlan& tc, int stage_cap);
 // Split + swizzle C into the image (one tiny kernel per execution).
 void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st);
