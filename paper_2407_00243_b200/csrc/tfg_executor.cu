@@ -2603,6 +2603,17 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
             }
           }
           if (best_bn != pl.tc.bn) tc_set_bn(pl.tc, best_bn);
+          if (getenv("TFG_DEBUG")) {
+            const int capc = (int)std::min<size_t>(
+                tc_stage_bytes(pl.tc) / ((size_t)pl.tc.bn * 4), (size_t)max_need);
+            int64_t wn = 0, an = 0;
+            for (int64_t v = 0; v < pl.n_ftiles; ++v) {
+              an += tnnz[v];
+              if (tc[v] > capc) wn += tnnz[v];
+            }
+            fprintf(stderr, "[tfg] tc bn %d slices %d cap %d wide-nnz %.3f of %lld\n", pl.tc.bn,
+                    pl.tc.slices, capc, an ? (double)wn / an : 0.0, (long long)an);
+          }
           cap_bytes = tc_stage_bytes(pl.tc);
           row_bytes = (size_t)pl.tc.bn * 4;
           pl.cs = pl.tc.bn;

@@ -45,7 +45,7 @@ constexpr int kChunkBytes = kBM * kKC * 4;    // 16 KB
 constexpr int kThreads = 576;  // 1 TMA + 8 convert + 1 MMA + 8 epilogue warps
 constexpr size_t kCMax = 128 * 1024;          // resident C slice image (hi + lo)
 constexpr size_t kSmemMax = 227 * 1024;
-constexpr size_t kBarBytes = 256;
+constexpr size_t kBarBytes = 384;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -170,10 +170,16 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-// TMEM columns: [0, 2*BN) two accumulators, then kOpStages x 64 operand
-// columns (32 tf32 hi + 32 tf32 lo per row of the 128-row block).
-constexpr int kOpStages = 4;
+// TMEM columns: [0, NACC*BN) accumulators, then kOpStages x 64 operand
+// columns (32 tf32 hi + 32 tf32 lo per row of the 128-row block).  Narrow
+// slices get more accumulators: the MMAs then run up to NACC blocks ahead
+// of the epilogue, which also computes the fused rows of finished tiles.
+constexpr int kOpStages = 2;
 constexpr uint32_t kTmemCols = 512;
+template <int BN>
+__host__ __device__ constexpr int nacc() {
+  return ((int)kTmemCols - kOpStages * 64) / BN > 8 ? 8 : ((int)kTmemCols - kOpStages * 64) / BN;
+}
 
 template <int BN, int LPR>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -187,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int VEC = 4;
   constexpr int NCH = BN / (LPR * VEC);
   static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
-  static_assert(2 * BN + kOpStages * 64 <= (int)kTmemCols, "TMEM budget");
+  constexpr int NACC = nacc<BN>();
+  static_assert(NACC >= 2 && NACC * BN + kOpStages * 64 <= (int)kTmemCols, "TMEM budget");
   constexpr int kHalf = BN / 2;  // columns per epilogue warp
   static_assert(kHalf % 16 == 0, "epilogue column split");
   constexpr uint32_t kIdesc = (1u << 4)                       // D format f32
@@ -205,8 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* raw_empty = bars + raw_stages;     // [raw_stages] converters read it
   uint64_t* op_full = raw_empty + raw_stages;  // [kOpStages] hi/lo in TMEM
   uint64_t* op_empty = op_full + kOpStages;    // [kOpStages] MMAs done with it
-  uint64_t* acc_full = op_empty + kOpStages;   // [2]
-  uint64_t* acc_empty = acc_full + 2;          // [2]
+  uint64_t* acc_full = op_empty + kOpStages;   // [NACC]
+  uint64_t* acc_empty = acc_full + NACC;       // [NACC]
   uint64_t* c_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_init(&op_full[s], 256);
       bar_init(&op_empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       bar_init(&acc_full[a], 1);
       bar_init(&acc_empty[a], 256);
     }
@@ -238,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t op_col0 = 2 * BN;
+  const uint32_t op_col0 = NACC * BN;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -315,8 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
         const int ilo = t_ilo[v], ihi = t_ihi[v];
         for (int r0 = ilo; r0 < ihi; r0 += kBM, ++b) {
-          const int a = b & 1;
-          if (b >= 2) bar_wait(&acc_empty[a], ((b / 2) - 1) & 1);
+          const int a = b % NACC;
+          if (b >= (uint32_t)NACC) bar_wait(&acc_empty[a], ((b / NACC) - 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(a * BN);
           for (int kc = 0; kc < kchunks; ++kc, ++t) {
@@ -354,8 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ilo = t_ilo[v], ihi = t_ihi[v];
       const bool wide = first_op || t_wide[v] != 0;
       for (int r0 = ilo; r0 < ihi; r0 += kBM, ++b) {
-        const int a = b & 1;
-        bar_wait(&acc_full[a], (b / 2) & 1);
+        const int a = b % NACC;
+        bar_wait(&acc_full[a], (b / NACC) & 1);
         tc_fence_after();
         const int row = r0 + m;
         const bool valid = row < ihi;
