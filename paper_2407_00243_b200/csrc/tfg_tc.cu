@@ -174,11 +174,19 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
 // columns (32 tf32 hi + 32 tf32 lo per row of the 128-row block).  Narrow
 // slices get more accumulators: the MMAs then run up to NACC blocks ahead
 // of the epilogue, which also computes the fused rows of finished tiles.
-constexpr int kOpStages = 2;
+#ifndef TFG_TC_OPS
+#define TFG_TC_OPS 2
+#endif
+#ifndef TFG_TC_NACC_MAX
+#define TFG_TC_NACC_MAX 8
+#endif
+constexpr int kOpStages = TFG_TC_OPS;
 constexpr uint32_t kTmemCols = 512;
 template <int BN>
 __host__ __device__ constexpr int nacc() {
-  return ((int)kTmemCols - kOpStages * 64) / BN > 8 ? 8 : ((int)kTmemCols - kOpStages * 64) / BN;
+  return ((int)kTmemCols - kOpStages * 64) / BN > TFG_TC_NACC_MAX
+             ? TFG_TC_NACC_MAX
+             : ((int)kTmemCols - kOpStages * 64) / BN;
 }
 
 template <int BN, int LPR>
