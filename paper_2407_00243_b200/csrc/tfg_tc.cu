@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* op_empty = op_full + kOpStages;    // [kOpStages] MMAs done with it
   uint64_t* acc_full = op_empty + kOpStages;   // [NACC]
   uint64_t* acc_empty = acc_full + NACC;       // [NACC]
-  uint64_t* c_full = acc_empty + 2;
+  uint64_t* c_full = acc_empty + NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.y * BN;
