@@ -1717,6 +1717,25 @@ __global__ void __launch_bounds__(256)
   cp_async_wait<0>();
 }
 
+// Fused-row index stream of the tensor-core tiles: per nonzero, the stage
+// slot of its column (staged tile) or the column itself (wide tile).
+__global__ void k_fused_xidx(int64_t nrows, const int* __restrict__ jrows,
+                             const int64_t* __restrict__ off, const uint8_t* __restrict__ rwide,
+                             const int* __restrict__ arp, const int* __restrict__ aci,
+                             const int* __restrict__ slot, int* __restrict__ xidx) {
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= nrows) return;
+  const int lane = threadIdx.x & 31;
+  const int j = jrows[q];
+  const int kb = arp[j], ke = arp[j + 1];
+  const bool w = rwide[q] != 0;
+  int* o = xidx + off[q] - kb;
+  for (int k = kb + lane; k < ke; k += 32) {
+    const int c = aci[k];
+    o[k] = w ? c : slot[c];
+  }
+}
+
 // slot[i] = position of D1 row i in its tile's stage (-1: not read by the
 // tile's fused rows).  One warp per fused tile, rows ascending.
 __global__ void k_assign_slots(int64_t ntiles, const int* __restrict__ t_ilo,
@@ -2370,6 +2389,8 @@ struct tfg_plan {
   tfg::dbuf<int> fo_r0, fo_cnt;  // dense B: GEMM row blocks
   tfg::dbuf<int> fo_ihi;         // r0 + cnt (tensor-core first op)
   tfg::TcPlan tc;                // fp32 dense B: tcgen05 3xTF32 first op (tfg_tc.cu)
+  tfg::dbuf<int64_t> fx_off;     // tc fused rows: offsets into fx_idx (ft_jrows order)
+  tfg::dbuf<int> fx_idx;         // per fused nonzero: stage slot (staged tile) or D1 row (wide)
   tfg::SpmmWork fo_sparse;       // sparse B: SpMM rows with X = C
   // (b) fused tiles
   int64_t n_ftiles = 0;
@@ -2632,6 +2653,25 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         if (pl.tc.on) {
           tc_finalize(pl.tc, cap);
           pl.fused_smem = pl.tc.smem;
+          // fused rows address the stage (or D1) directly: no slot lookup per
+          // nonzero in the kernel
+          std::vector<int64_t> off(f_rows.size() + 1, 0);
+          std::vector<uint8_t> rwide(f_rows.size());
+          for (int64_t v = 0; v < pl.n_ftiles; ++v)
+            for (int64_t q = f_joff[v]; q < f_joff[v + 1]; ++q) {
+              rwide[q] = wide[v];
+              off[q + 1] = off[q] + (arp[f_rows[q] + 1] - arp[f_rows[q]]);
+            }
+          pl.fx_off.alloc(off.size());
+          h2d(pl.fx_off.p, off.data(), off.size(), st);
+          pl.fx_idx.alloc(std::max<int64_t>(off.back(), 1));
+          dbuf<uint8_t> drw(rwide.size());
+          h2d(drw.p, rwide.data(), rwide.size(), st);
+          k_fused_xidx<<<blocks_for((int64_t)f_rows.size() * 32), 256, 0, st>>>(
+              (int64_t)f_rows.size(), pl.ft_jrows.p, pl.fx_off.p, drw.p, pr.d_a_row_ptr,
+              pr.d_a_col_idx, pl.slot.p, pl.fx_idx.p);
+          TFG_LAUNCH_CHECK();
+          TFG_CUDA(cudaStreamSynchronize(st));
         }
         if (getenv("TFG_DEBUG")) {
           int64_t rows = 0, pad128 = 0, slots = 0, small = 0;
@@ -2907,7 +2947,7 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
     if (pl.n_fo_blocks && pl.tc.on) {
       if constexpr (sizeof(T) == 4)
         tc_run(pl.tc, pr.n, bc, cc, pl.n_fo_blocks, pl.fo_r0.p, pl.fo_ihi.p, nullptr, nullptr,
-               nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+               nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                reinterpret_cast<float*>(D1), nullptr, st);
     } else if (pl.n_fo_blocks && pl.gemm_kind) {
       launch_gemm_v2<T>(pl, static_cast<const T*>(pr.d_b_dense), bc, C, cc, D1, st);
@@ -2929,8 +2969,8 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (pl.n_ftiles && pl.fused_v2 && pl.tc.on) {
     if constexpr (sizeof(T) == 4)
       tc_run(pl.tc, pr.n, bc, cc, pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, pl.ft_joff.p,
-             pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p, pl.spill.p, pr.d_a_row_ptr, pr.d_a_col_idx,
-             static_cast<const float*>(pr.d_a_val), reinterpret_cast<float*>(D1),
+             pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p, pl.spill.p, pr.d_a_row_ptr, pl.fx_off.p,
+             pl.fx_idx.p, static_cast<const float*>(pr.d_a_val), reinterpret_cast<float*>(D1),
              reinterpret_cast<float*>(D), st);
   } else if (pl.n_ftiles && pl.fused_v2) {
     launch_fused_v2<T>(pl, D1, D, st);

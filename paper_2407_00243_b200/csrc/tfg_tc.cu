@@ -196,8 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
                const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
                const int* __restrict__ slot, const uint8_t* __restrict__ spill, int stage_cap,
-               int cc, const int* __restrict__ arp, const int* __restrict__ aci,
-               const float* __restrict__ av, float* D1, float* __restrict__ D, int dbg) {
+               int cc, const int* __restrict__ arp, const int64_t* __restrict__ fx_off,
+               const int* __restrict__ fx_idx, const float* __restrict__ av, float* D1,
+               float* __restrict__ D, int dbg) {
   constexpr int VEC = 4;
   constexpr int NCH = BN / (LPR * VEC);
   static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
@@ -402,18 +403,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 256;\n" ::: "memory");  // staged / spilled rows visible
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
-        const int kb = __ldg(arp + j), ke = __ldg(arp + j + 1);
+        const int xb = (int)fx_off[qq], xe = (int)fx_off[qq + 1];
+        const float* avj = av + (__ldg(arp + j) - xb);  // value of fused nonzero k: avj[k]
         float acc2[NCH][VEC];
         if (wide) {
           auto xl = [&](int c, int chn, float(&xx)[VEC]) {
             ldv<float, VEC>(xx, D1 + (size_t)c * cc + n0 + (chn * LPR + gl) * VEC);
           };
-          spmm_row<float, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc2);
+          spmm_row<float, VEC, LPR, NCH>(xb, xe, fx_idx, avj, gl, gmask, xl, acc2);
         } else {
           auto xl = [&](int c, int chn, float(&xx)[VEC]) {
-            ldv<float, VEC>(xx, stage + (size_t)__ldg(slot + c) * BN + (chn * LPR + gl) * VEC);
+            ldv<float, VEC>(xx, stage + (size_t)c * BN + (chn * LPR + gl) * VEC);
           };
-          spmm_row<float, VEC, LPR, NCH>(kb, ke, aci, av, gl, gmask, xl, acc2);
+          spmm_row<float, VEC, LPR, NCH>(xb, xe, fx_idx, avj, gl, gmask, xl, acc2);
         }
         float* o = D + (size_t)j * cc + n0;
 #pragma unroll
@@ -525,8 +527,8 @@ void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st
 
 void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* ilo,
             const int* ihi, const int64_t* joff, const int* jrows, const uint8_t* wide,
-            const int* slot, const uint8_t* spill, const int* arp, const int* aci,
-            const float* av, float* D1, float* D, cudaStream_t st) {
+            const int* slot, const uint8_t* spill, const int* arp, const int64_t* fx_off,
+            const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st) {
   (void)n;
   (void)bc;
   if (!ntiles) return;
@@ -542,7 +544,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), kThreads, tc.smem, st>>>(
         tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
-        tc.stage_cap, cc, arp, aci, av, D1, D, dbg);
+        tc.stage_cap, cc, arp, fx_off, fx_idx, av, D1, D, dbg);
   };
   if (tc.bn == 128)
     launch(k_tc_tiles<128, 32>);
