@@ -1,20 +1,20 @@
 // tfg_tc.cu -- FP32 first op on tcgen05 tensor cores (3xTF32), optionally
 // fused with the wavefront-0 tile's SpMM rows.  See tfg_tc.cuh.
 //
-// Per CTA (one per SM, 576 threads, persistent over tiles):
+// Per CTA (one per SM, 704 threads, persistent over tiles):
 //   warp 0      TMA producer: 128-row x 32-column fp32 blocks of B land in a
 //               ring of raw shared-memory slots (128-byte swizzle); the CTA's
 //               C slice (pre-split tf32 hi/lo image, K-major) is bulk-copied
 //               once and stays resident.
-//   warps 1-8   converters, half a block row per thread: read 16 values,
+//   warps 1-4   converters, one block row per thread: read its 32 values,
 //               split x = hi + lo (tf32 each, error < 2^-20 x), free the raw
 //               slot and tcgen05.st both planes into a TMEM operand stage.
-//   warp 9      one lane issues tcgen05.mma kind::tf32 with A from TMEM and
+//   warp 5      one lane issues tcgen05.mma kind::tf32 with A from TMEM and
 //               B (C) from shared memory, M=128, N=BN, K=8:
 //               D += B_lo C_hi + B_hi C_lo + B_hi C_hi into one of two TMEM
 //               accumulators; tcgen05.commit frees operand stages and hands
 //               finished accumulators to the epilogue.
-//   warps 10-17 epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
+//   warps 6-21  epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
 //               wavefront 1 reads (spill) or that no stage holds (wide tile),
 //               stage rows the tile's fused rows read, then compute those
 //               fused rows (spmm_row, reference order) into D.
@@ -42,7 +42,21 @@ constexpr int kStages = 4;
 constexpr int kBM = 128;                      // rows per MMA block (M)
 constexpr int kKC = 32;                       // K per ring chunk (one 128-byte swizzle row)
 constexpr int kChunkBytes = kBM * kKC * 4;    // 16 KB
-constexpr int kThreads = 576;  // 1 TMA + 8 convert + 1 MMA + 8 epilogue warps
+#ifndef TFG_TC_CONV
+#define TFG_TC_CONV 4
+#endif
+#ifndef TFG_TC_EPI
+#define TFG_TC_EPI 16
+#endif
+// warp roles: 0 TMA producer, 1..kConv converters, kMmaWarp MMA issuer, then
+// kEpi epilogue / fused-row warps
+constexpr int kConv = TFG_TC_CONV;  // 4 or 8
+constexpr int kEpi = TFG_TC_EPI;    // multiple of 4
+constexpr int kMmaWarp = 1 + kConv;
+constexpr int kEpi0 = kMmaWarp + 1;
+constexpr int kThreads = 32 * (kEpi0 + kEpi);
+static_assert(kConv == 4 || kConv == 8, "converter warps");
+static_assert(kEpi % 4 == 0 && kEpi >= 4, "epilogue warps");
 constexpr size_t kCMax = 128 * 1024;          // resident C slice image (hi + lo)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kBarBytes = 384;
@@ -175,7 +189,7 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
 // slices get more accumulators: the MMAs then run up to NACC blocks ahead
 // of the epilogue, which also computes the fused rows of finished tiles.
 #ifndef TFG_TC_OPS
-#define TFG_TC_OPS 2
+#define TFG_TC_OPS 4
 #endif
 #ifndef TFG_TC_NACC_MAX
 #define TFG_TC_NACC_MAX 8
@@ -204,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
   constexpr int NACC = nacc<BN>();
   static_assert(NACC >= 2 && NACC * BN + kOpStages * 64 <= (int)kTmemCols, "TMEM budget");
-  constexpr int kHalf = BN / 2;  // columns per epilogue warp
-  static_assert(kHalf % 16 == 0, "epilogue column split");
+  constexpr int kEpiGroups = kEpi / 4;  // epilogue warps per TMEM lane quarter
+  static_assert(BN % 16 == 0, "epilogue column chunks");
   constexpr uint32_t kIdesc = (1u << 4)                       // D format f32
                               | (2u << 7) | (2u << 10)        // A, B format tf32
                               | ((uint32_t)(BN >> 3) << 17)   // N
@@ -231,20 +245,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < raw_stages; ++s) {
       bar_init(&raw_full[s], 1);
-      bar_init(&raw_empty[s], 256);
+      bar_init(&raw_empty[s], kConv * 32);
     }
     for (int s = 0; s < kOpStages; ++s) {
-      bar_init(&op_full[s], 256);
+      bar_init(&op_full[s], kConv * 32);
       bar_init(&op_empty[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
       bar_init(&acc_full[a], 1);
-      bar_init(&acc_empty[a], 256);
+      bar_init(&acc_empty[a], kEpi * 32);
     }
     bar_init(c_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      su32(tmem_slot)),
                  "n"(kTmemCols));
@@ -276,10 +290,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       }
     }
-  } else if (warp <= 8) {
-    // converters: half a row (16 K values) of the 128-row block per thread,
-    // TMEM lane quarter = warp % 4 (the lanes a warp may access)
-    const int q = warp & 3, hh = (warp - 1) >> 2;
+  } else if (warp <= kConv) {
+    // converters: one row of the 128-row block per thread (kConv = 4: both
+    // 16-value halves in turn; kConv = 8: one half), TMEM lane quarter =
+    // warp % 4 (the lanes a warp may access)
+    const int q = warp & 3, hpart = (warp - 1) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_bits = (uint32_t)(q * 32) << 16;
     uint32_t t = 0;
@@ -291,22 +306,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           bar_wait(&raw_full[s], (t / raw_stages) & 1);
           const float4* src = reinterpret_cast<const float4*>(ring + (size_t)s * kChunkBytes +
                                                               (size_t)r * 128);
-          float x[16];
+          constexpr int kHalves = kConv == 4 ? 2 : 1;
+          float h[kHalves][16], l[kHalves][16];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 f = src[(hh * 4 + u) ^ (r & 7)];
-            x[4 * u] = f.x;
-            x[4 * u + 1] = f.y;
-            x[4 * u + 2] = f.z;
-            x[4 * u + 3] = f.w;
-          }
-          float h[16], l[16];
+          for (int hv = 0; hv < kHalves; ++hv) {
+            const int hh = kHalves == 2 ? hv : hpart;
+            float x[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (dbg & 1) {
-              h[i] = l[i] = x[i];
-            } else {
-              split_tf32(x[i], h[i], l[i]);
+            for (int u = 0; u < 4; ++u) {
+              const float4 f = src[(hh * 4 + u) ^ (r & 7)];
+              x[4 * u] = f.x;
+              x[4 * u + 1] = f.y;
+              x[4 * u + 2] = f.z;
+              x[4 * u + 3] = f.w;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (dbg & 1) {
+                h[hv][i] = l[hv][i] = x[i];
+              } else {
+                split_tf32(x[i], h[hv][i], l[hv][i]);
+              }
             }
           }
           // the slot is refilled by the TMA (async proxy): order these generic
@@ -315,15 +335,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           bar_arrive(&raw_empty[s]);
           if (t >= (uint32_t)kOpStages) bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
           tc_fence_after();
-          const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64 + hh * 16;
-          tmem_st16(col, h);
-          tmem_st16(col + 32, l);
+#pragma unroll
+          for (int hv = 0; hv < kHalves; ++hv) {
+            const int hh = kHalves == 2 ? hv : hpart;
+            const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64 + hh * 16;
+            tmem_st16(col, h[hv]);
+            tmem_st16(col + 32, l[hv]);
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
           tc_fence_before();
           bar_arrive(&op_full[so]);
         }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0) {
       bar_wait(c_full, 0);
       const uint32_t sc_addr = su32(sc);
@@ -357,14 +381,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue warps 10..17: TMEM lane quarter = warp % 4, column half h
-    const int et = threadIdx.x - 320;
-    const int q = warp & 3, h = (warp - 10) >> 2;
+    // epilogue warps: TMEM lane quarter = warp % 4, column chunks of 16
+    // interleaved over the kEpiGroups warps of a quarter
+    const int et = threadIdx.x - kEpi0 * 32;
+    const int q = warp & 3, g = (warp - kEpi0) >> 2;
     const int m = q * 32 + lane;
     const bool first_op = t_joff == nullptr;
+    auto named_sync = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(kEpi * 32) : "memory"); };
     const int gl = et & (LPR - 1);
     const unsigned gmask = group_mask(LPR);
-    const int group = et / LPR, ngroups = 256 / LPR;
+    const int group = et / LPR, ngroups = kEpi * 32 / LPR;
     uint32_t b = 0;
     for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
       const int ilo = t_ilo[v], ihi = t_ihi[v];
@@ -378,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool sp = valid && (wide || spill[row]);
         const int sl = (valid && !wide) ? slot[row] : -1;
 #pragma unroll
-        for (int c0 = h * kHalf; c0 < (h + 1) * kHalf; c0 += 16) {
+        for (int c0 = g * 16; c0 < BN; c0 += 16 * kEpiGroups) {
           float x[16];
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
           if (sp && !(dbg & 8)) {
@@ -400,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (first_op) continue;
       const int64_t jb = t_joff[v], je = t_joff[v + 1];
       if (je == jb || (dbg & 4)) continue;
-      asm volatile("bar.sync 1, 256;\n" ::: "memory");  // staged / spilled rows visible
+      named_sync();  // staged / spilled rows visible
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
         const int xb = (int)fx_off[qq], xe = (int)fx_off[qq + 1];
@@ -421,12 +447,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int chn = 0; chn < NCH; ++chn) stv<float, VEC>(o + (chn * LPR + gl) * VEC, acc2[chn]);
       }
-      asm volatile("bar.sync 1, 256;\n" ::: "memory");  // stage free for the next tile
+      named_sync();  // stage free for the next tile
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "n"(kTmemCols));
