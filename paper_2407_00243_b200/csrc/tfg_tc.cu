@@ -1,20 +1,20 @@
 // tfg_tc.cu -- FP32 first op on tcgen05 tensor cores (3xTF32), optionally
 // fused with the wavefront-0 tile's SpMM rows.  See tfg_tc.cuh.
 //
-// Per CTA (one per SM, 704 threads, persistent over tiles):
+// Per CTA (one per SM, 576-704 threads, persistent over tiles):
 //   warp 0      TMA producer: 128-row x 32-column fp32 blocks of B land in a
 //               ring of raw shared-memory slots (128-byte swizzle); the CTA's
 //               C slice (pre-split tf32 hi/lo image, K-major) is bulk-copied
 //               once and stays resident.
-//   warps 1-4   converters, one block row per thread: read its 32 values,
+//   warps 1-C   converters (C = 4 or 8), a block row per 4 warps: read values,
 //               split x = hi + lo (tf32 each, error < 2^-20 x), free the raw
 //               slot and tcgen05.st both planes into a TMEM operand stage.
-//   warp 5      one lane issues tcgen05.mma kind::tf32 with A from TMEM and
+//   warp C+1    one lane issues tcgen05.mma kind::tf32 with A from TMEM and
 //               B (C) from shared memory, M=128, N=BN, K=8:
 //               D += B_lo C_hi + B_hi C_lo + B_hi C_hi into one of two TMEM
 //               accumulators; tcgen05.commit frees operand stages and hands
 //               finished accumulators to the epilogue.
-//   warps 6-21  epilogue: tcgen05.ld rows out of TMEM, write D1 rows that
+//   last E      epilogue (E = 16 or 8): tcgen05.ld rows out of TMEM, write D1 rows that
 //               wavefront 1 reads (spill) or that no stage holds (wide tile),
 //               stage rows the tile's fused rows read, then compute those
 //               fused rows (spmm_row, reference order) into D.
@@ -42,21 +42,20 @@ constexpr int kStages = 4;
 constexpr int kBM = 128;                      // rows per MMA block (M)
 constexpr int kKC = 32;                       // K per ring chunk (one 128-byte swizzle row)
 constexpr int kChunkBytes = kBM * kKC * 4;    // 16 KB
-#ifndef TFG_TC_CONV
-#define TFG_TC_CONV 4
-#endif
-#ifndef TFG_TC_EPI
-#define TFG_TC_EPI 16
-#endif
-// warp roles: 0 TMA producer, 1..kConv converters, kMmaWarp MMA issuer, then
-// kEpi epilogue / fused-row warps
-constexpr int kConv = TFG_TC_CONV;  // 4 or 8
-constexpr int kEpi = TFG_TC_EPI;    // multiple of 4
-constexpr int kMmaWarp = 1 + kConv;
-constexpr int kEpi0 = kMmaWarp + 1;
-constexpr int kThreads = 32 * (kEpi0 + kEpi);
-static_assert(kConv == 4 || kConv == 8, "converter warps");
-static_assert(kEpi % 4 == 0 && kEpi >= 4, "epilogue warps");
+// warp roles: 0 TMA producer, 1..CONV converters, CONV+1 MMA issuer, then
+// EPI epilogue / fused-row warps.  First-op launches (no fused rows) use
+// 8 + 8; fused tiles 4 + 16 (the fused rows need the warps, the 4-op split
+// does not).
+template <int CONV, int EPI>
+struct Roles {
+  static constexpr int kConv = CONV;
+  static constexpr int kEpi = EPI;
+  static constexpr int kMmaWarp = 1 + CONV;
+  static constexpr int kEpi0 = kMmaWarp + 1;
+  static constexpr int kThreads = 32 * (kEpi0 + EPI);
+  static_assert(CONV == 4 || CONV == 8, "converter warps");
+  static_assert(EPI % 4 == 0 && EPI >= 4, "epilogue warps");
+};
 constexpr size_t kCMax = 128 * 1024;          // resident C slice image (hi + lo)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kBarBytes = 384;
@@ -203,8 +202,8 @@ __host__ __device__ constexpr int nacc() {
              : ((int)kTmemCols - kOpStages * 64) / BN;
 }
 
-template <int BN, int LPR>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int LPR, int CONV, int EPI>
+__global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
     k_tc_tiles(const __grid_constant__ CUtensorMap bmap, int kchunks, int raw_stages,
                const float* __restrict__ cimg, int64_t ntiles, const int* __restrict__ t_ilo,
                const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
@@ -213,6 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                int cc, const int* __restrict__ arp, const int64_t* __restrict__ fx_off,
                const int* __restrict__ fx_idx, const float* __restrict__ av, float* D1,
                float* __restrict__ D, int dbg) {
+  using R = Roles<CONV, EPI>;
+  constexpr int kConv = R::kConv, kEpi = R::kEpi, kMmaWarp = R::kMmaWarp, kEpi0 = R::kEpi0;
   constexpr int VEC = 4;
   constexpr int NCH = BN / (LPR * VEC);
   static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
@@ -562,22 +563,25 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
     const char* e = getenv("TFG_TC_DBG");  // timing experiments only: skips work
     return e ? atoi(e) : 0;
   }();
-  auto launch = [&](auto kern) {
+  auto launch = [&](auto kern, int threads) {
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.smem));
     // all column slices of a tile run concurrently so B blocks are read from
     // HBM once and hit L2 for the other slices
     const int64_t gx =
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
-    kern<<<dim3((unsigned)gx, (unsigned)tc.slices), kThreads, tc.smem, st>>>(
+    kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, tc.smem, st>>>(
         tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
         tc.stage_cap, cc, arp, fx_off, fx_idx, av, D1, D, dbg);
   };
+  const bool fused = joff != nullptr;
+  using F = Roles<4, 16>;
+  using U = Roles<8, 8>;
   if (tc.bn == 128)
-    launch(k_tc_tiles<128, 32>);
+    fused ? launch(k_tc_tiles<128, 32, 4, 16>, F::kThreads) : launch(k_tc_tiles<128, 32, 8, 8>, U::kThreads);
   else if (tc.bn == 64)
-    launch(k_tc_tiles<64, 16>);
+    fused ? launch(k_tc_tiles<64, 16, 4, 16>, F::kThreads) : launch(k_tc_tiles<64, 16, 8, 8>, U::kThreads);
   else
-    launch(k_tc_tiles<32, 8>);
+    fused ? launch(k_tc_tiles<32, 8, 4, 16>, F::kThreads) : launch(k_tc_tiles<32, 8, 8, 8>, U::kThreads);
   TFG_LAUNCH_CHECK();
 }
 
