@@ -723,6 +723,224 @@ __global__ void __launch_bounds__(288, 1)
   }
 }
 
+// ---- dependency-driven band sweep (SpMM-SpMM without fused tiles) ----------
+// The first op (D1 = B C) and wavefront 1 (D = A D1) as ONE persistent band
+// kernel over a single item list: first-op blocks in row order, each
+// wavefront-1 block placed after the first-op blocks that produce the D1 rows
+// it reads (plus a lag of two grid rounds).  Consumers publish a first-op
+// block by bumping its flag once per warp after their D1 stores are fenced;
+// the producer of a wavefront-1 block waits until every first-op block in
+// its D1 row range is published before its TMA copies of those rows, so D1
+// is read back from L2 while it is still resident instead of from HBM.  The
+// wavefront barrier of the reference (kernels.hpp:118-119) is relaxed to the
+// exact per-row dependencies; every D1 and D row is computed by the same
+// code and order as in the two-pass execution (bit-identical).  Items are
+// taken round-robin in list order by co-resident CTAs and dependencies only
+// point to earlier items, so every wait is on an item some CTA is already
+// processing.
+template <class T>
+struct BandSide {
+  int R, row0, nrows;
+  const int* rp;
+  const T* av;
+  const int* run_begin;
+  const int* run_start;
+  const int* run_len;
+  const int64_t* idx_off;
+  const uint16_t* lidx;
+  const T* X;
+  T* out;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class T, int VEC, int LPR, int NCH, int STAGES>
+__global__ void __launch_bounds__(288, 1)
+    k_spmm_band_sweep(int nitems, const int* __restrict__ items, const int2* __restrict__ dep,
+                      int* done1, int target, BandSide<T> s0, BandSide<T> s1, int stage_cap,
+                      int idx_cap, int val_cap, int cc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
+  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
+  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
+  const size_t bufbytes = xbytes + ibytes + vbytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NCONS = 8;
+  constexpr int kOpShift = 30;
+  constexpr int kBlkMask = (1 << kOpShift) - 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int nmine = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / G + 1 : 0;
+  if (warp == NCONS) {
+    // ---------------- producer ----------------
+    int m_k0 = 0, m_k1 = 0, m_rb = 0, m_re = 0, m_op = 0, m_b = 0;
+    int64_t m_i0 = 0, m_i1 = 0;
+    auto load_meta = [&](int base) {
+      const int itl = base + lane;
+      if (itl < nmine) {
+        const int code = __ldg(items + blockIdx.x + itl * G);
+        const int op = code >> kOpShift, b = code & kBlkMask;
+        const int R = op ? s1.R : s0.R, row0 = op ? s1.row0 : s0.row0;
+        const int nrows = op ? s1.nrows : s0.nrows;
+        const int* rp = op ? s1.rp : s0.rp;
+        const int* rbp = op ? s1.run_begin : s0.run_begin;
+        const int64_t* io = op ? s1.idx_off : s0.idx_off;
+        const int r_lo = row0 + b * R;
+        const int r_hi = min(r_lo + R, row0 + nrows);
+        m_k0 = __ldg(rp + r_lo);
+        m_k1 = __ldg(rp + r_hi);
+        m_rb = __ldg(rbp + b);
+        m_re = __ldg(rbp + b + 1);
+        m_i0 = __ldg(io + b);
+        m_i1 = __ldg(io + b + 1);
+        m_op = op;
+        m_b = b;
+      }
+    };
+    load_meta(0);
+    auto load_runs = [&](int it, int& rs, int& rl) {
+      const int rb = __shfl_sync(0xffffffffu, m_rb, it & 31);
+      const int re = __shfl_sync(0xffffffffu, m_re, it & 31);
+      const int op = __shfl_sync(0xffffffffu, m_op, it & 31);
+      rs = 0;
+      rl = 0;
+      if (rb + lane < re) {
+        rs = __ldg((op ? s1.run_start : s0.run_start) + rb + lane);
+        rl = __ldg((op ? s1.run_len : s0.run_len) + rb + lane);
+      }
+    };
+    int rs = 0, rl = 0;
+    if (nmine > 0) load_runs(0, rs, rl);
+    for (int it = 0; it < nmine; ++it) {
+      const int s = it % STAGES;
+      const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
+      const int k1 = __shfl_sync(0xffffffffu, m_k1, it & 31);
+      const int64_t i0 = __shfl_sync(0xffffffffu, m_i0, it & 31);
+      const int64_t i1 = __shfl_sync(0xffffffffu, m_i1, it & 31);
+      const int op = __shfl_sync(0xffffffffu, m_op, it & 31);
+      const int b = __shfl_sync(0xffffffffu, m_b, it & 31);
+      int off = rl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += y;
+      }
+      const int total_rows = __shfl_sync(0xffffffffu, off, 31);
+      off -= rl;
+      const int my_rs = rs, my_rl = rl;
+      if (it + 1 < nmine) {
+        if (((it + 1) & 31) == 0) load_meta(it + 1);
+        load_runs(it + 1, rs, rl);
+      }
+      if (op) {  // wavefront-1 block: wait for the first-op blocks it reads
+        const int2 d = __ldg(dep + b);
+        for (int f = d.x + lane; f <= d.y; f += 32)
+          while (ld_acquire_gpu(done1 + f) < target) __nanosleep(32);
+        __syncwarp();
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      }
+      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
+      unsigned char* base = smem_raw + (size_t)s * bufbytes;
+      T* xs = reinterpret_cast<T*>(base);
+      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
+      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
+      const T* av = op ? s1.av : s0.av;
+      for (int k = k0 + lane; k < k1; k += 32) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
+      cp_async_mbar_arrive(&full[s]);
+      __syncwarp();
+      if (lane == 0)
+        mbar_arrive_expect_tx(&full[s], (unsigned)((size_t)total_rows * cc * sizeof(T) +
+                                                   (size_t)(i1 - i0) * 2));
+      __syncwarp();
+      if (my_rl > 0) {
+        const T* X = op ? s1.X : s0.X;
+        const char* src = reinterpret_cast<const char*>(X + (size_t)my_rs * cc);
+        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
+        size_t left = (size_t)my_rl * cc * sizeof(T);
+        while (left) {
+          const unsigned chunk = (unsigned)min(left, (size_t)32768);
+          bulk_g2s(dst, src, chunk, &full[s]);
+          dst += chunk;
+          src += chunk;
+          left -= chunk;
+        }
+      }
+      if (lane == 0 && i1 > i0)
+        bulk_g2s(is, (op ? s1.lidx : s0.lidx) + i0, (unsigned)((i1 - i0) * 2), &full[s]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = group_mask(LPR);
+  const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
+  for (int it = 0; it < nmine; ++it) {
+    const int code = __ldg(items + blockIdx.x + it * G);
+    const int op = code >> kOpShift, b = code & kBlkMask;
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
+    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
+    const T* xs = reinterpret_cast<const T*>(base);
+    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
+    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
+    const int R = op ? s1.R : s0.R, row0 = op ? s1.row0 : s0.row0;
+    const int nrows = op ? s1.nrows : s0.nrows;
+    T* out = op ? s1.out : s0.out;
+    const int r_lo = row0 + b * R;
+    const int nr = min(R, row0 + nrows - r_lo);
+    const uint16_t* lrp = is;
+    const uint16_t* lsl = is + nr + 1;
+    for (int r = group; r < nr; r += ngroups) {
+      const int eb = lrp[r], ee = lrp[r + 1];
+      T acc[NCH][VEC];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+      for (int e0 = eb; e0 < ee; e0 += LPR) {
+        const int sl = e0 + gl < ee ? lsl[e0 + gl] : 0;
+        const int cnt = min(LPR, ee - e0);
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+          const int su = __shfl_sync(gmask, sl, u, LPR);
+          const T au = vs[e0 + u];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            T x[VEC];
+            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+          }
+        }
+      }
+      T* o = out + (size_t)(r_lo + r) * cc;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+    }
+    if (op == 0) {  // publish: this warp's D1 rows are globally visible
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(done1 + b, 1);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 template <class T, int VEC, int LPR, int NCH, int STAGES>
 __global__ void __launch_bounds__(288, 1)
     k_spmm_band4(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
@@ -1836,6 +2054,7 @@ struct SpmmWork {
   dbuf<int> run_begin, run_start, run_len;
   dbuf<int64_t> idx_off;
   dbuf<uint16_t> lidx;
+  std::vector<int> blk_xlo, blk_xhi;  // per band block: X rows read [lo, hi] (hi < lo: none)
 
   // Blocks of R consecutive rows whose X rows form <= kBandRuns contiguous
   // runs; adopted only when it at least halves the X rows gathered.
@@ -1869,7 +2088,7 @@ struct SpmmWork {
     if (nnz_total <= 0) return;
     for (int R : {256, 128, 64, 32, 16, 8, 4}) {
       const int nb = (int)((nrows + R - 1) / R);
-      std::vector<int> rb{0}, rs, rl, li;
+      std::vector<int> rb{0}, rs, rl, li, bxlo, bxhi;
       std::vector<int64_t> io{0};
       int64_t staged_total = 0;
       int scap = 0, icap = 0, vcap = 0;
@@ -1949,6 +2168,8 @@ struct SpmmWork {
           rs.push_back(r.first);
           rl.push_back(r.second);
         }
+        bxlo.push_back(runs.empty() ? 1 : runs.front().first);
+        bxhi.push_back(runs.empty() ? 0 : runs.back().first + runs.back().second - 1);
         rb.push_back((int)rs.size());
         // index record: row offsets, slots, [mini-group offsets, union entries]
         const size_t rec0 = li.size();
@@ -1971,6 +2192,8 @@ struct SpmmWork {
       banded = true;
       band_R = R;
       band_blocks = nb;
+      blk_xlo.swap(bxlo);
+      blk_xhi.swap(bxhi);
       stage_cap = scap;
       idx_cap = icap;
       val_cap = vcap;
@@ -2406,12 +2629,20 @@ struct tfg_plan {
   int64_t n_wide = 0;
   // (c) wavefront 1 / unfused second op
   tfg::SpmmWork second;
+  // (a)+(c) as one dependency-driven band sweep (k_spmm_band_sweep)
+  bool sweep = false;
+  int sw_nitems = 0, sw_grid = 0, sw_scap = 0, sw_icap = 0, sw_vcap = 0;
+  size_t sw_smem = 0;
+  uint32_t sw_epoch = 0;
+  tfg::dbuf<int> sw_items, sw_done;
+  tfg::dbuf<int2> sw_dep;
   tfg::dbuf<uint8_t> spill;
   tfg::dbuf<unsigned char> d1;
   // accounting
   int64_t spill_rows = 0, fused_rows = 0;
   int64_t first_rows = 0, second_rows = 0, nnz_processed = 0;
   int launches = 0;
+  void* sweep_out = nullptr;   // D of the execution in flight (sweep launch argument)
   int row_lo = 0, row_hi = 0;  // row block of a partition plan (multi-GPU)
   // algorithmic (compulsory) HBM bytes per stage: (a) first op, (b) fused
   // tiles, (c) wavefront-1 SpMM -- each input byte read once, each output
@@ -2444,6 +2675,58 @@ static size_t fused_gemm_smem(const tfg_plan& pl) {
   }
   return pl.gemm_kind == 2 ? GemmCfg<double, 64, 128, 16, 4, 8, 3>::SMEM
                            : GemmCfg<double, 64, 64, 16, 4, 4, 3>::SMEM;
+}
+
+// Launch (or, with grid_only, size) the band sweep for a plan.
+template <class T>
+static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int cc = pl.p.c_cols;
+  const int L = cc / VEC;
+  const SpmmWork& w0 = pl.fo_sparse;
+  const SpmmWork& w1 = pl.second;
+  auto side = [&](const SpmmWork& w, const int* rp, const void* av, const void* X, void* out) {
+    BandSide<T> b;
+    b.R = w.band_R;
+    b.row0 = w.row0;
+    b.nrows = (int)w.n_short;
+    b.rp = rp;
+    b.av = static_cast<const T*>(av);
+    b.run_begin = w.run_begin.p;
+    b.run_start = w.run_start.p;
+    b.run_len = w.run_len.p;
+    b.idx_off = w.idx_off.p;
+    b.lidx = w.lidx.p;
+    b.X = static_cast<const T*>(X);
+    b.out = static_cast<T*>(out);
+    return b;
+  };
+  int grid = 0;
+  auto go = [&](auto kern) {
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)pl.sw_smem));
+    int occ = 1;
+    TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 288, pl.sw_smem));
+    grid = (int)std::min<int64_t>(pl.sw_nitems, (int64_t)sm_count() * std::max(occ, 1));
+    if (grid_only) return;
+    ++pl.sw_epoch;
+    if ((int64_t)pl.sw_epoch * 8 > (int64_t)INT32_MAX - 64) {  // flags restart
+      TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
+      pl.sw_epoch = 1;
+    }
+    kern<<<grid, 288, pl.sw_smem, st>>>(
+        pl.sw_nitems, pl.sw_items.p, pl.sw_dep.p, pl.sw_done.p, (int)pl.sw_epoch * 8,
+        side(w0, pl.p.d_b_row_ptr, pl.p.d_b_val, pl.p.d_c, pl.d1.p),
+        side(w1, pl.p.d_a_row_ptr, pl.p.d_a_val, pl.d1.p, pl.sweep_out), pl.sw_scap, pl.sw_icap,
+        pl.sw_vcap, cc);
+    TFG_LAUNCH_CHECK();
+  };
+  if (L == 8) go(k_spmm_band_sweep<T, VEC, 8, 1, 2>);
+  else if (L == 16) go(k_spmm_band_sweep<T, VEC, 16, 1, 2>);
+  else if (L == 32) go(k_spmm_band_sweep<T, VEC, 32, 1, 2>);
+  else if (L == 64) go(k_spmm_band_sweep<T, VEC, 32, 2, 2>);
+  else throw runtime_error("band sweep: unsupported column count");
+  return grid;
 }
 
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
@@ -2844,14 +3127,81 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                           (int64_t)second_rows.size() * cc * el;
   }
 
+  // (a)+(c) as one dependency-driven band sweep: SpMM-SpMM, nothing fused,
+  // both passes band-staged over all rows
+  {
+    static const bool sweep_on = [] {
+      const char* e = getenv("TFG_SWEEP");
+      return !e || atoi(e) > 0;
+    }();
+    const SpmmWork& w0 = pl.fo_sparse;
+    const SpmmWork& w1 = pl.second;
+    if (sweep_on && !pr.b_is_dense && pl.n_ftiles == 0 && !partial && w0.banded && w1.banded &&
+        !w0.band_union && !w1.band_union && w0.n_long == 0 && w1.n_long == 0 && w0.row0 == 0 &&
+        w1.row0 == 0 && w0.n_short == n && w1.n_short == n) {
+      pl.sw_scap = std::max(w0.stage_cap, w1.stage_cap);
+      pl.sw_icap = std::max(w0.idx_cap, w1.idx_cap);
+      pl.sw_vcap = std::max(w0.val_cap, w1.val_cap);
+      const size_t buf = (size_t)pl.sw_scap * cc * pl.elem +
+                         ((size_t)pl.sw_icap * 2 + 15) / 16 * 16 +
+                         ((size_t)pl.sw_vcap * pl.elem + 15) / 16 * 16;
+      pl.sw_smem = 2 * buf;
+      if (pl.sw_smem <= kBandSmemMax) {
+        const int nb0 = w0.band_blocks, nb1 = w1.band_blocks;
+        pl.sw_nitems = nb0 + nb1;
+        pl.sw_grid = pl.elem == 8 ? sweep_launch<double>(pl, st, true)
+                                  : sweep_launch<float>(pl, st, true);
+        // item order: first-op block i at key i; wavefront-1 block k after the
+        // last first-op block it reads plus two grid rounds
+        const int64_t lag = 2 * (int64_t)pl.sw_grid;
+        std::vector<int2> dep(nb1);
+        std::vector<std::pair<int64_t, int>> keyed;
+        keyed.reserve(pl.sw_nitems);
+        for (int i = 0; i < nb0; ++i) keyed.emplace_back(2 * (int64_t)i, i);
+        for (int k = 0; k < nb1; ++k) {
+          const int lo = w1.blk_xlo[k], hi = w1.blk_xhi[k];
+          int2 d;
+          if (hi < lo) {
+            d = make_int2(0, -1);
+          } else {
+            d = make_int2(lo / w0.band_R, std::min(hi / w0.band_R, nb0 - 1));
+          }
+          dep[k] = d;
+          const int64_t key = 2 * (std::max<int64_t>(d.y, 0) + lag) + 1;
+          keyed.emplace_back(key, k | (1 << 30));
+        }
+        std::stable_sort(keyed.begin(), keyed.end(),
+                         [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& b) {
+                           return a.first < b.first;
+                         });
+        std::vector<int> items(keyed.size());
+        for (size_t q = 0; q < keyed.size(); ++q) items[q] = keyed[q].second;
+        pl.sw_items.alloc(items.size());
+        h2d(pl.sw_items.p, items.data(), items.size(), st);
+        pl.sw_dep.alloc(dep.size());
+        h2d(pl.sw_dep.p, dep.data(), dep.size(), st);
+        pl.sw_done.alloc(nb0);
+        TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
+        TFG_CUDA(cudaStreamSynchronize(st));
+        pl.sweep = true;
+        pl.stage_bytes[0] += pl.stage_bytes[2];  // one kernel does both passes
+        pl.stage_bytes[2] = 0;
+      }
+    }
+  }
+
   pl.launches = 0;
   if (pl.tc.on && (pl.n_fo_blocks > 0 || pl.n_ftiles > 0)) pl.launches += 1;  // C split
-  if (pr.b_is_dense)
-    pl.launches += pl.n_fo_blocks > 0;
-  else
-    pl.launches += pl.fo_sparse.launches();
-  pl.launches += pl.n_ftiles > 0;
-  pl.launches += pl.second.launches();
+  if (pl.sweep) {
+    pl.launches += 1;
+  } else {
+    if (pr.b_is_dense)
+      pl.launches += pl.n_fo_blocks > 0;
+    else
+      pl.launches += pl.fo_sparse.launches();
+    pl.launches += pl.n_ftiles > 0;
+    pl.launches += pl.second.launches();
+  }
   TFG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -2938,6 +3288,13 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (part == 1) goto wave1;
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
+  if (pl.sweep && part < 0) {  // both passes in one dependency-driven kernel
+    pl.sweep_out = D;
+    sweep_launch<T>(pl, st, false);
+    for (int e = 1; e <= 3; ++e)
+      if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
+    return;
+  }
   // (a)
   if constexpr (sizeof(T) == 4) {
     if (pl.tc.on && (pl.n_fo_blocks || pl.n_ftiles))
