@@ -729,8 +729,10 @@ __global__ void __launch_bounds__(288, 1)
 // wavefront-1 block placed after the first-op blocks that produce the D1 rows
 // it reads (plus a lag of two grid rounds).  Consumers publish a first-op
 // block by bumping its flag once per warp after their D1 stores are fenced;
-// the producer of a wavefront-1 block waits until every first-op block in
-// its D1 row range is published before its TMA copies of those rows, so D1
+// the producer of a wavefront-1 block waits until the completed prefix of
+// first-op blocks covers the last block of its D1 row range (a monotone
+// counter advanced from the flags by the waiters themselves, prefetched one
+// item ahead) before its TMA copies of those rows, so D1
 // is read back from L2 while it is still resident instead of from HBM.  The
 // wavefront barrier of the reference (kernels.hpp:118-119) is relaxed to the
 // exact per-row dependencies; every D1 and D row is computed by the same
@@ -757,11 +759,17 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <class T, int VEC, int LPR, int NCH, int STAGES>
 __global__ void __launch_bounds__(288, 1)
     k_spmm_band_sweep(int nitems, const int* __restrict__ items, const int2* __restrict__ dep,
-                      int* done1, int target, BandSide<T> s0, BandSide<T> s1, int stage_cap,
+                      int* done1, int target, unsigned long long* prefix,
+                      unsigned long long pbase, BandSide<T> s0, BandSide<T> s1, int stage_cap,
                       int idx_cap, int val_cap, int cc) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -823,6 +831,12 @@ __global__ void __launch_bounds__(288, 1)
     };
     int rs = 0, rl = 0;
     if (nmine > 0) load_runs(0, rs, rl);
+    const int nb0 = s0.nrows > 0 ? (s0.nrows + s0.R - 1) / s0.R : 0;
+    // first-op blocks [0, count) are complete (epoch-relative prefix counter)
+    auto done_count = [&](unsigned long long v) -> long long {
+      return v > pbase ? (long long)(v - pbase) : 0ll;
+    };
+    unsigned long long pre = ld_acquire_gpu64(prefix);
     for (int it = 0; it < nmine; ++it) {
       const int s = it % STAGES;
       const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
@@ -845,9 +859,22 @@ __global__ void __launch_bounds__(288, 1)
         load_runs(it + 1, rs, rl);
       }
       if (op) {  // wavefront-1 block: wait for the first-op blocks it reads
-        const int2 d = __ldg(dep + b);
-        for (int f = d.x + lane; f <= d.y; f += 32)
-          while (ld_acquire_gpu(done1 + f) < target) __nanosleep(32);
+        const int hi = __ldg(dep + b).y;
+        long long cnt = done_count(pre);
+        while (cnt <= hi) {
+          // advance the prefix over completed blocks, 32 flags per round
+          const long long f = cnt + lane;
+          const bool ok = f < nb0 && ld_acquire_gpu(done1 + f) >= target;
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          const int run = bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
+          if (run > 0) {
+            if (lane == 0) atomicMax(prefix, pbase + (unsigned long long)(cnt + run));
+            cnt += run;
+          } else {
+            __nanosleep(100);
+            cnt = max(cnt, done_count(ld_acquire_gpu64(prefix)));
+          }
+        }
         __syncwarp();
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
       }
@@ -879,6 +906,7 @@ __global__ void __launch_bounds__(288, 1)
       }
       if (lane == 0 && i1 > i0)
         bulk_g2s(is, (op ? s1.lidx : s0.lidx) + i0, (unsigned)((i1 - i0) * 2), &full[s]);
+      pre = ld_acquire_gpu64(prefix);  // prefetched for the next item
     }
     cp_async_wait<0>();
     return;
@@ -2636,6 +2664,7 @@ struct tfg_plan {
   uint32_t sw_epoch = 0;
   tfg::dbuf<int> sw_items, sw_done;
   tfg::dbuf<int2> sw_dep;
+  tfg::dbuf<unsigned long long> sw_prefix;  // epoch * (blocks + 1) + completed prefix
   tfg::dbuf<uint8_t> spill;
   tfg::dbuf<unsigned char> d1;
   // accounting
@@ -2712,10 +2741,14 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
     ++pl.sw_epoch;
     if ((int64_t)pl.sw_epoch * 8 > (int64_t)INT32_MAX - 64) {  // flags restart
       TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
+      TFG_CUDA(cudaMemsetAsync(pl.sw_prefix.p, 0, pl.sw_prefix.bytes(), st));
       pl.sw_epoch = 1;
     }
+    const unsigned long long pbase =
+        (unsigned long long)pl.sw_epoch * (unsigned long long)(pl.fo_sparse.band_blocks + 1);
     kern<<<grid, 288, pl.sw_smem, st>>>(
         pl.sw_nitems, pl.sw_items.p, pl.sw_dep.p, pl.sw_done.p, (int)pl.sw_epoch * 8,
+        pl.sw_prefix.p, pbase,
         side(w0, pl.p.d_b_row_ptr, pl.p.d_b_val, pl.p.d_c, pl.d1.p),
         side(w1, pl.p.d_a_row_ptr, pl.p.d_a_val, pl.d1.p, pl.sweep_out), pl.sw_scap, pl.sw_icap,
         pl.sw_vcap, cc);
@@ -3182,6 +3215,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         h2d(pl.sw_dep.p, dep.data(), dep.size(), st);
         pl.sw_done.alloc(nb0);
         TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
+        pl.sw_prefix.alloc(1);
+        TFG_CUDA(cudaMemsetAsync(pl.sw_prefix.p, 0, pl.sw_prefix.bytes(), st));
         TFG_CUDA(cudaStreamSynchronize(st));
         pl.sweep = true;
         pl.stage_bytes[0] += pl.stage_bytes[2];  // one kernel does both passes
