@@ -727,12 +727,12 @@ __global__ void __launch_bounds__(288, 1)
 // The first op (D1 = B C) and wavefront 1 (D = A D1) as ONE persistent band
 // kernel over a single item list: first-op blocks in row order, each
 // wavefront-1 block placed after the first-op blocks that produce the D1 rows
-// it reads (plus a lag of two grid rounds).  Consumers publish a first-op
-// block by bumping its flag once per warp after their D1 stores are fenced;
-// the producer of a wavefront-1 block waits until the completed prefix of
-// first-op blocks covers the last block of its D1 row range (a monotone
-// counter advanced from the flags by the waiters themselves, prefetched one
-// item ahead) before its TMA copies of those rows, so D1
+// it reads (plus a lag of two grid rounds).  First-op blocks are grouped in
+// chunks of C (C sized so any block's D1 row range spans <= 32 chunks);
+// consumers bump their chunk's counter once per warp after their D1 stores
+// are fenced.  The producer of a wavefront-1 block checks the chunks of its
+// D1 row range lane-parallel -- loads issued one item ahead, so the check is
+// off the critical path -- before its TMA copies of those rows, so D1
 // is read back from L2 while it is still resident instead of from HBM.  The
 // wavefront barrier of the reference (kernels.hpp:118-119) is relaxed to the
 // exact per-row dependencies; every D1 and D row is computed by the same
@@ -754,23 +754,17 @@ struct BandSide {
   T* out;
 };
 
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p));
   return v;
 }
 
 template <class T, int VEC, int LPR, int NCH, int STAGES>
 __global__ void __launch_bounds__(288, 1)
     k_spmm_band_sweep(int nitems, const int* __restrict__ items, const int2* __restrict__ dep,
-                      int* done1, int target, unsigned long long* prefix,
-                      unsigned long long pbase, BandSide<T> s0, BandSide<T> s1, int stage_cap,
-                      int idx_cap, int val_cap, int cc) {
+                      int* chunk_done, int chunk_shift, int epoch, BandSide<T> s0,
+                      BandSide<T> s1, int stage_cap, int idx_cap, int val_cap, int cc) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
@@ -832,11 +826,26 @@ __global__ void __launch_bounds__(288, 1)
     int rs = 0, rl = 0;
     if (nmine > 0) load_runs(0, rs, rl);
     const int nb0 = s0.nrows > 0 ? (s0.nrows + s0.R - 1) / s0.R : 0;
-    // first-op blocks [0, count) are complete (epoch-relative prefix counter)
-    auto done_count = [&](unsigned long long v) -> long long {
-      return v > pbase ? (long long)(v - pbase) : 0ll;
+    // chunk c is complete when all its blocks' 8 consumer warps published
+    auto chunk_target = [&](int c) {
+      return 8 * epoch * min(1 << chunk_shift, nb0 - (c << chunk_shift));
     };
-    unsigned long long pre = ld_acquire_gpu64(prefix);
+    // lane q: chunk (lo_chunk + q) of the item's range and its counter value
+    int pc = -1, pv = 0;
+    auto prefetch_deps = [&](int it2) {
+      pc = -1;
+      if (it2 >= nmine) return;
+      const int code = __ldg(items + blockIdx.x + it2 * G);
+      if (!(code >> kOpShift)) return;
+      const int2 d = __ldg(dep + (code & kBlkMask));
+      if (d.y < d.x) return;
+      const int c0 = d.x >> chunk_shift, c1 = d.y >> chunk_shift;
+      if (c0 + lane <= c1) {
+        pc = c0 + lane;
+        pv = ld_relaxed_gpu(chunk_done + pc);
+      }
+    };
+    prefetch_deps(0);
     for (int it = 0; it < nmine; ++it) {
       const int s = it % STAGES;
       const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
@@ -858,24 +867,17 @@ __global__ void __launch_bounds__(288, 1)
         if (((it + 1) & 31) == 0) load_meta(it + 1);
         load_runs(it + 1, rs, rl);
       }
-      if (op) {  // wavefront-1 block: wait for the first-op blocks it reads
-        const int hi = __ldg(dep + b).y;
-        long long cnt = done_count(pre);
-        while (cnt <= hi) {
-          // advance the prefix over completed blocks, 32 flags per round
-          const long long f = cnt + lane;
-          const bool ok = f < nb0 && ld_acquire_gpu(done1 + f) >= target;
-          const unsigned bal = __ballot_sync(0xffffffffu, ok);
-          const int run = bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
-          if (run > 0) {
-            if (lane == 0) atomicMax(prefix, pbase + (unsigned long long)(cnt + run));
-            cnt += run;
-          } else {
-            __nanosleep(100);
-            cnt = max(cnt, done_count(ld_acquire_gpu64(prefix)));
+      if (op) {  // wavefront-1 block: wait for the first-op chunks it reads
+        if (pc >= 0) {
+          const int tgt = chunk_target(pc);
+          while (pv < tgt) {
+            __nanosleep(64);
+            pv = ld_relaxed_gpu(chunk_done + pc);
           }
         }
         __syncwarp();
+        // acquire the publishers' D1 stores, then order them before the TMA
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
       }
       mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
@@ -906,7 +908,7 @@ __global__ void __launch_bounds__(288, 1)
       }
       if (lane == 0 && i1 > i0)
         bulk_g2s(is, (op ? s1.lidx : s0.lidx) + i0, (unsigned)((i1 - i0) * 2), &full[s]);
-      pre = ld_acquire_gpu64(prefix);  // prefetched for the next item
+      prefetch_deps(it + 1);  // dependency loads of the next item in flight now
     }
     cp_async_wait<0>();
     return;
@@ -962,7 +964,7 @@ __global__ void __launch_bounds__(288, 1)
     if (op == 0) {  // publish: this warp's D1 rows are globally visible
       __threadfence();
       __syncwarp();
-      if (lane == 0) atomicAdd(done1 + b, 1);
+      if (lane == 0) atomicAdd(chunk_done + (b >> chunk_shift), 1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -2662,9 +2664,9 @@ struct tfg_plan {
   int sw_nitems = 0, sw_grid = 0, sw_scap = 0, sw_icap = 0, sw_vcap = 0;
   size_t sw_smem = 0;
   uint32_t sw_epoch = 0;
-  tfg::dbuf<int> sw_items, sw_done;
+  int sw_chunk_shift = 0;                    // first-op blocks per dependency chunk (log2)
+  tfg::dbuf<int> sw_items, sw_done;         // sw_done: per chunk, 8 * blocks * epoch when done
   tfg::dbuf<int2> sw_dep;
-  tfg::dbuf<unsigned long long> sw_prefix;  // epoch * (blocks + 1) + completed prefix
   tfg::dbuf<uint8_t> spill;
   tfg::dbuf<unsigned char> d1;
   // accounting
@@ -2739,16 +2741,13 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
     grid = (int)std::min<int64_t>(pl.sw_nitems, (int64_t)sm_count() * std::max(occ, 1));
     if (grid_only) return;
     ++pl.sw_epoch;
-    if ((int64_t)pl.sw_epoch * 8 > (int64_t)INT32_MAX - 64) {  // flags restart
-      TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
-      TFG_CUDA(cudaMemsetAsync(pl.sw_prefix.p, 0, pl.sw_prefix.bytes(), st));
+    if ((int64_t)(pl.sw_epoch + 1) * 8 * ((int64_t)1 << pl.sw_chunk_shift) > (int64_t)INT32_MAX) {
+      TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));  // counters restart
       pl.sw_epoch = 1;
     }
-    const unsigned long long pbase =
-        (unsigned long long)pl.sw_epoch * (unsigned long long)(pl.fo_sparse.band_blocks + 1);
     kern<<<grid, 288, pl.sw_smem, st>>>(
-        pl.sw_nitems, pl.sw_items.p, pl.sw_dep.p, pl.sw_done.p, (int)pl.sw_epoch * 8,
-        pl.sw_prefix.p, pbase,
+        pl.sw_nitems, pl.sw_items.p, pl.sw_dep.p, pl.sw_done.p, pl.sw_chunk_shift,
+        (int)pl.sw_epoch,
         side(w0, pl.p.d_b_row_ptr, pl.p.d_b_val, pl.p.d_c, pl.d1.p),
         side(w1, pl.p.d_a_row_ptr, pl.p.d_a_val, pl.d1.p, pl.sweep_out), pl.sw_scap, pl.sw_icap,
         pl.sw_vcap, cc);
@@ -3186,7 +3185,15 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                                   : sweep_launch<float>(pl, st, true);
         // item order: first-op block i at key i; wavefront-1 block k after the
         // last first-op block it reads plus two grid rounds
-        const int64_t lag = 2 * (int64_t)pl.sw_grid;
+        // dependency chunks: any block's D1 range spans <= 32 of them
+        int max_span = 1;
+        for (int k = 0; k < nb1; ++k)
+          if (w1.blk_xhi[k] >= w1.blk_xlo[k])
+            max_span = std::max(max_span, w1.blk_xhi[k] / w0.band_R - w1.blk_xlo[k] / w0.band_R + 1);
+        int cs = 0;
+        while (((max_span + (1 << cs) - 1) >> cs) + 1 > 32) ++cs;
+        pl.sw_chunk_shift = cs;
+        const int64_t lag = 2 * (int64_t)pl.sw_grid + (1 << cs);
         std::vector<int2> dep(nb1);
         std::vector<std::pair<int64_t, int>> keyed;
         keyed.reserve(pl.sw_nitems);
@@ -3200,7 +3207,9 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
             d = make_int2(lo / w0.band_R, std::min(hi / w0.band_R, nb0 - 1));
           }
           dep[k] = d;
-          const int64_t key = 2 * (std::max<int64_t>(d.y, 0) + lag) + 1;
+          // after the last block of the last chunk it waits for
+          const int64_t last = std::min<int64_t>(((int64_t)(std::max(d.y, 0) >> cs) + 1) << cs, nb0) - 1;
+          const int64_t key = 2 * (last + lag) + 1;
           keyed.emplace_back(key, k | (1 << 30));
         }
         std::stable_sort(keyed.begin(), keyed.end(),
@@ -3213,10 +3222,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         h2d(pl.sw_items.p, items.data(), items.size(), st);
         pl.sw_dep.alloc(dep.size());
         h2d(pl.sw_dep.p, dep.data(), dep.size(), st);
-        pl.sw_done.alloc(nb0);
+        pl.sw_done.alloc(((int64_t)nb0 + (1 << cs) - 1) >> cs);
         TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
-        pl.sw_prefix.alloc(1);
-        TFG_CUDA(cudaMemsetAsync(pl.sw_prefix.p, 0, pl.sw_prefix.bytes(), st));
         TFG_CUDA(cudaStreamSynchronize(st));
         pl.sweep = true;
         pl.stage_bytes[0] += pl.stage_bytes[2];  // one kernel does both passes
