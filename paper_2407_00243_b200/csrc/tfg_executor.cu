@@ -764,7 +764,8 @@ template <class T, int VEC, int LPR, int NCH, int STAGES>
 __global__ void __launch_bounds__(288, 1)
     k_spmm_band_sweep(int nitems, const int* __restrict__ items, const int2* __restrict__ dep,
                       int* chunk_done, int chunk_shift, int epoch, BandSide<T> s0,
-                      BandSide<T> s1, int stage_cap, int idx_cap, int val_cap, int cc) {
+                      BandSide<T> s1, int stage_cap, int idx_cap, int val_cap, int cc,
+                      int dbg) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
@@ -867,7 +868,7 @@ __global__ void __launch_bounds__(288, 1)
         if (((it + 1) & 31) == 0) load_meta(it + 1);
         load_runs(it + 1, rs, rl);
       }
-      if (op) {  // wavefront-1 block: wait for the first-op chunks it reads
+      if (op && !(dbg & 1)) {  // wavefront-1 block: wait for the first-op chunks it reads
         if (pc >= 0) {
           const int tgt = chunk_target(pc);
           while (pv < tgt) {
@@ -961,7 +962,7 @@ __global__ void __launch_bounds__(288, 1)
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
     }
-    if (op == 0) {  // publish: this warp's D1 rows are globally visible
+    if (op == 0 && !(dbg & 2)) {  // publish: this warp's D1 rows are globally visible
       __threadfence();
       __syncwarp();
       if (lane == 0) atomicAdd(chunk_done + (b >> chunk_shift), 1);
@@ -2733,6 +2734,10 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
     return b;
   };
   int grid = 0;
+  static const int dbg = [] {  // timing experiments only: bit 0 no waits, bit 1 no publish
+    const char* e = getenv("TFG_SWEEP_DBG");
+    return e ? atoi(e) : 0;
+  }();
   auto go = [&](auto kern) {
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)pl.sw_smem));
@@ -2750,7 +2755,7 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
         (int)pl.sw_epoch,
         side(w0, pl.p.d_b_row_ptr, pl.p.d_b_val, pl.p.d_c, pl.d1.p),
         side(w1, pl.p.d_a_row_ptr, pl.p.d_a_val, pl.d1.p, pl.sweep_out), pl.sw_scap, pl.sw_icap,
-        pl.sw_vcap, cc);
+        pl.sw_vcap, cc, dbg);
     TFG_LAUNCH_CHECK();
   };
   if (L == 8) go(k_spmm_band_sweep<T, VEC, 8, 1, 2>);
