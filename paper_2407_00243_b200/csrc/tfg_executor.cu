@@ -2938,6 +2938,9 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
             for (int64_t v = 0; v < pl.n_ftiles; ++v)
               if (tc[v] > capc) wide_nnz += tnnz[v];
             const double cost = (double)(cc / bnc) * ft_rows * bc * 4 + 2.0 * wide_nnz * cc * 4;
+            if (getenv("TFG_DEBUG"))
+              fprintf(stderr, "[tfg] tc candidate bn %d cap %d wide-nnz %lld cost %.3g\n", bnc, capc,
+                      (long long)wide_nnz, cost);
             if (env_bn ? bnc == atoi(env_bn) : cost < best) {
               best = env_bn ? -1.0 : cost;
               best_bn = bnc;
