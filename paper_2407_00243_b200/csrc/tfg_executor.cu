@@ -3170,10 +3170,11 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   // (a)+(c) as one dependency-driven band sweep: SpMM-SpMM, nothing fused,
   // both passes band-staged over all rows
   {
-    static const bool sweep_on = [] {
-      const char* e = getenv("TFG_SWEEP");
-      return !e || atoi(e) > 0;
-    }();
+    // opt-in: measured slower than two band passes on cfg2 (0.61-0.73 vs
+    // 0.56 ms) although it moves 1 GB less DRAM -- the band SpMM is bound by
+    // the shared-memory data path, not HBM
+    const char* sweep_env = getenv("TFG_SWEEP");
+    const bool sweep_on = sweep_env && atoi(sweep_env) > 0;
     const SpmmWork& w0 = pl.fo_sparse;
     const SpmmWork& w1 = pl.second;
     if (sweep_on && !pr.b_is_dense && pl.n_ftiles == 0 && !partial && w0.banded && w1.banded &&
