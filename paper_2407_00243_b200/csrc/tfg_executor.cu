@@ -2645,6 +2645,7 @@ struct tfg_plan {
   tfg::TcPlan tc;                // fp32 dense B: tcgen05 3xTF32 first op (tfg_tc.cu)
   tfg::dbuf<int64_t> fx_off;     // tc fused rows: offsets into fx_idx (ft_jrows order)
   tfg::dbuf<int> fx_idx;         // per fused nonzero: stage slot (staged tile) or D1 row (wide)
+  tfg::dbuf<int> fx_aoff;        // per fused row: arp[j] - fx_off[q] (value offset)
   tfg::SpmmWork fo_sparse;       // sparse B: SpMM rows with X = C
   // (b) fused tiles
   int64_t n_ftiles = 0;
@@ -2980,11 +2981,15 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
           // nonzero in the kernel
           std::vector<int64_t> off(f_rows.size() + 1, 0);
           std::vector<uint8_t> rwide(f_rows.size());
+          std::vector<int> aoff(f_rows.size());
           for (int64_t v = 0; v < pl.n_ftiles; ++v)
             for (int64_t q = f_joff[v]; q < f_joff[v + 1]; ++q) {
               rwide[q] = wide[v];
               off[q + 1] = off[q] + (arp[f_rows[q] + 1] - arp[f_rows[q]]);
+              aoff[q] = (int)(arp[f_rows[q]] - off[q]);
             }
+          pl.fx_aoff.alloc(aoff.size());
+          h2d(pl.fx_aoff.p, aoff.data(), aoff.size(), st);
           pl.fx_off.alloc(off.size());
           h2d(pl.fx_off.p, off.data(), off.size(), st);
           pl.fx_idx.alloc(std::max<int64_t>(off.back(), 1));
@@ -3377,7 +3382,7 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (pl.n_ftiles && pl.fused_v2 && pl.tc.on) {
     if constexpr (sizeof(T) == 4)
       tc_run(pl.tc, pr.n, bc, cc, pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, pl.ft_joff.p,
-             pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p, pl.spill.p, pr.d_a_row_ptr, pl.fx_off.p,
+             pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p, pl.spill.p, pl.fx_aoff.p, pl.fx_off.p,
              pl.fx_idx.p, static_cast<const float*>(pr.d_a_val), reinterpret_cast<float*>(D1),
              reinterpret_cast<float*>(D), st);
   } else if (pl.n_ftiles && pl.fused_v2) {

@@ -209,14 +209,17 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
                const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
                const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
                const int* __restrict__ slot, const uint8_t* __restrict__ spill, int stage_cap,
-               int cc, const int* __restrict__ arp, const int64_t* __restrict__ fx_off,
+               int cc, const int* __restrict__ fx_aoff, const int64_t* __restrict__ fx_off,
                const int* __restrict__ fx_idx, const float* __restrict__ av, float* D1,
                float* __restrict__ D, int dbg) {
   using R = Roles<CONV, EPI>;
   constexpr int kConv = R::kConv, kEpi = R::kEpi, kMmaWarp = R::kMmaWarp, kEpi0 = R::kEpi0;
   constexpr int VEC = 4;
-  constexpr int NCH = BN / (LPR * VEC);
-  static_assert(NCH >= 1 && NCH * LPR * VEC == BN, "slice width");
+  // fused rows: 8 lanes per row (4 rows in flight per warp), NCH x 16 B each
+  constexpr int LPR2 = 8;
+  constexpr int NCH = BN / (LPR2 * VEC);
+  static_assert(NCH >= 1 && NCH * LPR2 * VEC == BN, "slice width");
+  static_assert(LPR >= 1, "unused");
   constexpr int NACC = nacc<BN>();
   static_assert(NACC >= 2 && NACC * BN + kOpStages * 64 <= (int)kTmemCols, "TMEM budget");
   constexpr int kEpiGroups = kEpi / 4;  // epilogue warps per TMEM lane quarter
@@ -389,9 +392,9 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
     const int m = q * 32 + lane;
     const bool first_op = t_joff == nullptr;
     auto named_sync = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(kEpi * 32) : "memory"); };
-    const int gl = et & (LPR - 1);
-    const unsigned gmask = group_mask(LPR);
-    const int group = et / LPR, ngroups = kEpi * 32 / LPR;
+    const int gl = et & (LPR2 - 1);
+    const unsigned gmask = group_mask(LPR2);
+    const int group = et / LPR2, ngroups = kEpi * 32 / LPR2;
     uint32_t b = 0;
     for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
       const int ilo = t_ilo[v], ihi = t_ihi[v];
@@ -431,22 +434,22 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
         const int xb = (int)fx_off[qq], xe = (int)fx_off[qq + 1];
-        const float* avj = av + (__ldg(arp + j) - xb);  // value of fused nonzero k: avj[k]
+        const float* avj = av + __ldg(fx_aoff + qq);  // value of fused nonzero k: avj[k]
         float acc2[NCH][VEC];
         if (wide) {
           auto xl = [&](int c, int chn, float(&xx)[VEC]) {
-            ldv<float, VEC>(xx, D1 + (size_t)c * cc + n0 + (chn * LPR + gl) * VEC);
+            ldv<float, VEC>(xx, D1 + (size_t)c * cc + n0 + (chn * LPR2 + gl) * VEC);
           };
-          spmm_row<float, VEC, LPR, NCH>(xb, xe, fx_idx, avj, gl, gmask, xl, acc2);
+          spmm_row<float, VEC, LPR2, NCH>(xb, xe, fx_idx, avj, gl, gmask, xl, acc2);
         } else {
           auto xl = [&](int c, int chn, float(&xx)[VEC]) {
-            ldv<float, VEC>(xx, stage + (size_t)c * BN + (chn * LPR + gl) * VEC);
+            ldv<float, VEC>(xx, stage + (size_t)c * BN + (chn * LPR2 + gl) * VEC);
           };
-          spmm_row<float, VEC, LPR, NCH>(xb, xe, fx_idx, avj, gl, gmask, xl, acc2);
+          spmm_row<float, VEC, LPR2, NCH>(xb, xe, fx_idx, avj, gl, gmask, xl, acc2);
         }
         float* o = D + (size_t)j * cc + n0;
 #pragma unroll
-        for (int chn = 0; chn < NCH; ++chn) stv<float, VEC>(o + (chn * LPR + gl) * VEC, acc2[chn]);
+        for (int chn = 0; chn < NCH; ++chn) stv<float, VEC>(o + (chn * LPR2 + gl) * VEC, acc2[chn]);
       }
       named_sync();  // stage free for the next tile
     }
@@ -554,7 +557,7 @@ void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st
 
 void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* ilo,
             const int* ihi, const int64_t* joff, const int* jrows, const uint8_t* wide,
-            const int* slot, const uint8_t* spill, const int* arp, const int64_t* fx_off,
+            const int* slot, const uint8_t* spill, const int* fx_aoff, const int64_t* fx_off,
             const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st) {
   (void)n;
   (void)bc;
@@ -571,7 +574,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, tc.smem, st>>>(
         tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
-        tc.stage_cap, cc, arp, fx_off, fx_idx, av, D1, D, dbg);
+        tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D, dbg);
   };
   const bool fused = joff != nullptr;
   using F = Roles<4, 16>;

@@ -44,10 +44,11 @@ void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st
 // D1 when spill[row] or the tile is wide, to the stage when slot[row] >= 0,
 // and the tile's fused rows jrows[joff[v] .. joff[v+1]) are computed into D.
 // fx_off / fx_idx: the fused rows' nonzeros as stage slots (staged tile) or
-// D1 rows (wide tile), in jrows order; values are read from av at arp[j].
+// D1 rows (wide tile), in jrows order; fused row q's values are
+// av[fx_aoff[q] + k] for k in [fx_off[q], fx_off[q+1]) (live CSR values).
 void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* ilo,
             const int* ihi, const int64_t* joff, const int* jrows, const uint8_t* wide,
-            const int* slot, const uint8_t* spill, const int* arp, const int64_t* fx_off,
+            const int* slot, const uint8_t* spill, const int* fx_aoff, const int64_t* fx_off,
             const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st);
 int tc_env_enabled();  // TFG_TC (default 1)
 
