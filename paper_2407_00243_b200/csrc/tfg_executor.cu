@@ -301,6 +301,12 @@ __device__ __forceinline__ void cp_async_small(void* smem, const void* gmem) {
 }
 
 constexpr int kBandRuns = 32;
+// diagonal lines of a stencil matrix: diagonals [first[l], first[l] + cnt[l])
+// of the ascending global offset set have consecutive column offsets
+struct DiaLines {
+  int nlines = 0, ndiag = 0;
+  int first[16] = {}, cnt[16] = {};
+};
 constexpr int kBandMG = 4;  // rows per register-reuse mini-group
 constexpr size_t kBandSmemMax = 200 * 1024;
 
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(288, 1)
                  const int* __restrict__ run_start, const int* __restrict__ run_len,
                  const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
                  int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
-                 T* __restrict__ out, int ldo) {
+                 T* __restrict__ out, int ldo, const DiaLines* __restrict__ = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int cc = ldx;
@@ -565,14 +571,69 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <class T, int VEC, int LPR, int NCH, int STAGES>
+// DIA (stencil) consumer: a warp takes a mini-group of 4 consecutive rows.
+// For a regular mini-group (every row has the global diagonal set) each
+// diagonal line's X rows are loaded once into a sliding register window and
+// applied to all 4 rows: row q, diagonal d of a line reads window slot q + d.
+// Per row the terms are still added in ascending column order (lines and
+// diagonals ascend), separately rounded -- the reference's order.  Other
+// mini-groups take the per-row path.
+template <class T, int VEC, int NCH>
+__device__ __forceinline__ void band_dia_group(const T* __restrict__ xs, const T* __restrict__ vs,
+                                               const uint16_t* lrp, const uint16_t* lsl, int cc,
+                                               int q0, const DiaLines& dl, int lane,
+                                               T* __restrict__ out_row0, int ldo) {
+  constexpr int M = 4, WMAX = M + 4;
+  T acc[M][NCH][VEC];
+#pragma unroll
+  for (int q = 0; q < M; ++q)
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[q][ch][v] = T(0);
+  int e[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) e[q] = lrp[q0 + q];
+  for (int l = 0; l < dl.nlines; ++l) {
+    const int d0 = dl.first[l], dc = dl.cnt[l];
+    const int base = lsl[e[0] + d0];  // slot of X row (row q0 + offset of d0)
+    T w[WMAX][NCH][VEC];
+#pragma unroll
+    for (int k = 0; k < WMAX; ++k)
+      if (k < M + dc - 1)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+          ldv<T, VEC>(w[k][ch], xs + (size_t)(base + k) * cc + (ch * 32 + lane) * VEC);
+#pragma unroll
+    for (int q = 0; q < M; ++q)
+#pragma unroll
+      for (int d = 0; d < 5; ++d)
+        if (d < dc) {
+          const T a = vs[e[q] + d0 + d];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              acc[q][ch][v] = fops<T>::add(acc[q][ch][v], fops<T>::mul(a, w[q + d][ch][v]));
+        }
+  }
+#pragma unroll
+  for (int q = 0; q < M; ++q)
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+      stv<T, VEC>(out_row0 + (size_t)q * ldo + (ch * 32 + lane) * VEC, acc[q][ch]);
+}
+
+template <class T, int VEC, int LPR, int NCH, int STAGES, bool DIA = false>
 __global__ void __launch_bounds__(288, 1)
     k_spmm_band3(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
                  const T* __restrict__ av, const int* __restrict__ run_begin,
                  const int* __restrict__ run_start, const int* __restrict__ run_len,
                  const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
                  int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
-                 T* __restrict__ out, int ldo) {
+                 T* __restrict__ out, int ldo, const DiaLines* __restrict__ dlp = nullptr) {
+  static_assert(!DIA || LPR == 32, "DIA consumer: a warp per row");
+
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int cc = ldx;
@@ -678,6 +739,8 @@ __global__ void __launch_bounds__(288, 1)
   const int gl = threadIdx.x & (LPR - 1);
   const unsigned gmask = group_mask(LPR);
   const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
+  DiaLines dl;
+  if constexpr (DIA) dl = *dlp;
   for (int it = 0; it < nmine; ++it) {
     const int b = blockIdx.x + it * G;
     const int s = it % STAGES;
@@ -690,7 +753,50 @@ __global__ void __launch_bounds__(288, 1)
     const int nr = min(R, row0 + nrows - r_lo);
     const uint16_t* lrp = is;
     const uint16_t* lsl = is + nr + 1;
+    if constexpr (DIA) {
+      const int nnzb = lrp[nr];
+      const uint32_t reg = (uint32_t)lsl[nnzb] | ((uint32_t)lsl[nnzb + 1] << 16);
+      const int nmg = (nr + 3) / 4;
+      for (int g = warp; g < nmg; g += NCONS) {
+        if ((reg >> g) & 1u) {
+          band_dia_group<T, VEC, NCH>(xs, vs, lrp, lsl, cc, 4 * g, dl, gl,
+                                      out + (size_t)(r_lo + 4 * g) * ldo, ldo);
+          continue;
+        }
+        for (int r = 4 * g; r < min(4 * g + 4, nr); ++r) {
+          const int eb = lrp[r], ee = lrp[r + 1];
+          T acc[NCH][VEC];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+          for (int e0 = eb; e0 < ee; e0 += LPR) {
+            const int sl = e0 + gl < ee ? lsl[e0 + gl] : 0;
+            const int cnt = min(LPR, ee - e0);
+            for (int u = 0; u < cnt; ++u) {
+              const int su = __shfl_sync(gmask, sl, u, LPR);
+              const T au = vs[e0 + u];
+#pragma unroll
+              for (int ch = 0; ch < NCH; ++ch) {
+                T x[VEC];
+                ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v)
+                  acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+              }
+            }
+          }
+          T* o = out + (size_t)(r_lo + r) * ldo;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      continue;
+    }
     for (int r = group; r < nr; r += ngroups) {
+
       const int eb = lrp[r], ee = lrp[r + 1];
       T acc[NCH][VEC];
 #pragma unroll
@@ -979,7 +1085,7 @@ __global__ void __launch_bounds__(288, 1)
                  const int* __restrict__ run_start, const int* __restrict__ run_len,
                  const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
                  int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
-                 T* __restrict__ out, int ldo) {
+                 T* __restrict__ out, int ldo, const DiaLines* __restrict__ = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int cc = ldx;
@@ -2086,6 +2192,12 @@ struct SpmmWork {
   dbuf<int64_t> idx_off;
   dbuf<uint16_t> lidx;
   std::vector<int> blk_xlo, blk_xhi;  // per band block: X rows read [lo, hi] (hi < lo: none)
+  // stencil (diagonal) structure: every row of a "regular" 4-row mini-group
+  // has exactly the global diagonal set; diagonals form lines of <= 5
+  // consecutive offsets (k_spmm_band3 DIA consumer)
+  bool dia = false;
+  DiaLines dia_lines{};
+  dbuf<DiaLines> dia_dev;
 
   // Blocks of R consecutive rows whose X rows form <= kBandRuns contiguous
   // runs; adopted only when it at least halves the X rows gathered.
@@ -2096,12 +2208,64 @@ struct SpmmWork {
       const char* e = getenv("TFG_BAND_KB");
       return e ? atoi(e) : 0;
     }();
+    detect_dia(row0, nrows, rp, ci, cc, elem);
     // smallest stage budget that admits a band layout (more CTAs per SM)
     for (int kb : {40, 64, 100}) {
       const int use = env_kb > 0 ? env_kb : kb;
       build_band_budget(row0, nrows, rp, ci, cc, elem, st, (size_t)use * 1024);
       if (banded || env_kb > 0) return;
     }
+  }
+
+  std::vector<int> dia_offs;  // the global diagonal offsets (col - row), ascending
+
+  void detect_dia(int row0, int64_t nrows, const std::vector<int>& rp, const std::vector<int>& ci,
+                  int cc, size_t elem) {
+    dia = false;
+    dia_offs.clear();
+    static const bool dia_on = [] {
+      const char* e = getenv("TFG_BAND_DIA");
+      return !e || atoi(e) > 0;
+    }();
+    if (!dia_on || (size_t)cc * elem != 512 && (size_t)cc * elem != 1024) return;
+    std::vector<int> offs;
+    for (int64_t r = row0; r < row0 + nrows; ++r)
+      for (int k = rp[r]; k < rp[r + 1]; ++k) {
+        const int o = ci[k] - (int)r;
+        if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+          offs.push_back(o);
+          if (offs.size() > 32) return;
+        }
+      }
+    std::sort(offs.begin(), offs.end());
+    DiaLines L{};
+    L.ndiag = (int)offs.size();
+    for (int d = 0; d < (int)offs.size();) {
+      int e = d + 1;
+      while (e < (int)offs.size() && offs[e] == offs[e - 1] + 1 && e - d < 5) ++e;
+      if (L.nlines == 16) return;
+      L.first[L.nlines] = d;
+      L.cnt[L.nlines] = e - d;
+      ++L.nlines;
+      d = e;
+    }
+    dia_offs = offs;
+    dia_lines = L;
+    dia = true;
+  }
+
+  // mini-group g (rows 4g..4g+3 of the block) is regular: all four rows exist
+  // and each has exactly the global diagonal set
+  bool dia_regular(int r_lo, int nr, int g, const std::vector<int>& rp,
+                   const std::vector<int>& ci) const {
+    if (4 * g + 3 >= nr) return false;
+    for (int q = 0; q < 4; ++q) {
+      const int r = r_lo + 4 * g + q;
+      if (rp[r + 1] - rp[r] != (int)dia_offs.size()) return false;
+      for (int d = 0; d < (int)dia_offs.size(); ++d)
+        if (ci[rp[r] + d] - r != dia_offs[d]) return false;
+    }
+    return true;
   }
 
   void build_band_budget(int row0, int64_t nrows, const std::vector<int>& rp,
@@ -2182,8 +2346,9 @@ struct SpmmWork {
           }
         }
         const int nmg = (nr + kBandMG - 1) / kBandMG;
-        const int irec = ((nr + 1 + (k1 - k0) + (use_union ? nmg + 1 + (int)uent.size() : 0)) + 7) /
-                         8 * 8;
+        const bool rec_dia = dia && !use_union && R <= 128;
+        const int irec = ((nr + 1 + (k1 - k0) + (use_union ? nmg + 1 + (int)uent.size() : 0) +
+                           (rec_dia ? 2 : 0)) + 7) / 8 * 8;
         const size_t need = (size_t)staged * row_bytes + (size_t)irec * 2 +
                             ((size_t)(k1 - k0) * elem + 15) / 16 * 16;
         if ((int)runs.size() > kBandRuns || staged > (use_union ? 4095 : 65535) || need > budget ||
@@ -2210,6 +2375,13 @@ struct SpmmWork {
           for (int v : mgoff) li.push_back(v);
           for (int v : uent) li.push_back(v);
         }
+        if (rec_dia) {
+          uint32_t mask = 0;
+          for (int g = 0; g < (nr + 3) / 4; ++g)
+            if (dia_regular(r_lo, nr, g, rp, ci)) mask |= 1u << g;
+          li.push_back((int)(mask & 0xffffu));
+          li.push_back((int)(mask >> 16));
+        }
         while ((li.size() - rec0) % 8) li.push_back(0);
         io.push_back((int64_t)li.size());
       }
@@ -2223,6 +2395,11 @@ struct SpmmWork {
       banded = true;
       band_R = R;
       band_blocks = nb;
+      if (!(dia && !use_union && R <= 128)) dia = false;
+      if (dia) {
+        dia_dev.alloc(1);
+        h2d(dia_dev.p, &dia_lines, 1, st);
+      }
       blk_xlo.swap(bxlo);
       blk_xhi.swap(bxhi);
       stage_cap = scap;
@@ -2426,6 +2603,12 @@ struct SpmmWork {
   int launches() const { return (n_short > 0) + 2 * (n_long > 0) + (grouped ? 1 : 0); }
 };
 
+// TFG_BAND_DIA=0 switches the stencil consumer off at execution time
+static bool dia_on() {
+  const char* e = getenv("TFG_BAND_DIA_EXEC");
+  return !e || atoi(e) > 0;
+}
+
 template <class T>
 static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
                                 const T* av, const T* X, int cc, T* out,
@@ -2444,10 +2627,26 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     }();
 #define TFG_BAND2(LPR, NCH, S)                                                               \
   if (ws == S) {                                                                             \
+    const size_t smem = w.band_smem / 2 * S;                                                 \
+    if constexpr (LPR == 32) {                                                               \
+      if (bv == 3 && w.dia && dia_on()) {                                                    \
+        auto kd = k_spmm_band3<T, VEC, LPR, NCH, S, true>;                                   \
+        TFG_CUDA(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                      (int)smem));                                           \
+        int occ = 1;                                                                         \
+        TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kd, 288, smem));        \
+        const int grid = (int)std::min<int64_t>(w.band_blocks, (int64_t)sm_count() * std::max(occ, 1)); \
+        kd<<<grid, 288, smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av,  \
+                                    w.run_begin.p, w.run_start.p, w.run_len.p, w.idx_off.p,   \
+                                    w.lidx.p, w.stage_cap, w.idx_cap, w.val_cap, X, cc, out, cc, \
+                                    w.dia_dev.p);                                             \
+        TFG_LAUNCH_CHECK();                                                                  \
+        return;                                                                              \
+      }                                                                                      \
+    }                                                                                        \
     auto kern = bv == 3 ? k_spmm_band3<T, VEC, LPR, NCH, S> : k_spmm_band2<T, VEC, LPR, NCH, S>; \
     if constexpr (LPR == 32)                                                                 \
       if (w.band_union && w.band_R >= 8 * kBandMG) kern = k_spmm_band4<T, VEC, LPR, NCH, S>;  \
-    const size_t smem = w.band_smem / 2 * S;                                                 \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                   (int)smem));                                               \
     int occ = 1;                                                                             \
@@ -2455,7 +2654,8 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     const int grid = (int)std::min<int64_t>(w.band_blocks, (int64_t)sm_count() * std::max(occ, 1)); \
     kern<<<grid, 288, smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av,   \
                                   w.run_begin.p, w.run_start.p, w.run_len.p, w.idx_off.p,    \
-                                  w.lidx.p, w.stage_cap, w.idx_cap, w.val_cap, X, cc, out, cc); \
+                                  w.lidx.p, w.stage_cap, w.idx_cap, w.val_cap, X, cc, out, cc, \
+                                  nullptr);                                                  \
     TFG_LAUNCH_CHECK();                                                                      \
     return;                                                                                  \
   }
