@@ -30,6 +30,9 @@ def main():
     variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
     for v in variants:
         env = dict(os.environ)
+        if v.startswith("X"):  # stencil (DIA-window) band consumer on/off at execution
+            env["TFG_BAND_DIA_EXEC"] = v[1:]
+            v = "-1"
         if v.startswith("D"):  # band sweep debug mask (timing only)
             env["TFG_SWEEP_DBG"] = v[1:]
             v = "-1"
