@@ -625,7 +625,7 @@ __device__ __forceinline__ void band_dia_group(const T* __restrict__ xs, const T
 }
 
 template <class T, int VEC, int LPR, int NCH, int STAGES, bool DIA = false>
-__global__ void __launch_bounds__(288, 1)
+__global__ void __launch_bounds__(288, (DIA && NCH == 1) ? 2 : 1)
     k_spmm_band3(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
                  const T* __restrict__ av, const int* __restrict__ run_begin,
                  const int* __restrict__ run_start, const int* __restrict__ run_len,
@@ -739,8 +739,12 @@ __global__ void __launch_bounds__(288, 1)
   const int gl = threadIdx.x & (LPR - 1);
   const unsigned gmask = group_mask(LPR);
   const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
-  DiaLines dl;
-  if constexpr (DIA) dl = *dlp;
+  __shared__ DiaLines dl_s;
+  if constexpr (DIA) {
+    if (threadIdx.x == 0) dl_s = *dlp;
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");  // consumer warps only
+  }
+  const DiaLines& dl = dl_s;
   for (int it = 0; it < nmine; ++it) {
     const int b = blockIdx.x + it * G;
     const int s = it % STAGES;
@@ -2209,8 +2213,10 @@ struct SpmmWork {
       return e ? atoi(e) : 0;
     }();
     detect_dia(row0, nrows, rp, ci, cc, elem);
-    // smallest stage budget that admits a band layout (more CTAs per SM)
+    // smallest stage budget that admits a band layout (more CTAs per SM); the
+    // stencil consumer wants >= 8 mini-groups (R >= 32) per block
     for (int kb : {40, 64, 100}) {
+      if (dia && kb == 40 && env_kb == 0) continue;
       const int use = env_kb > 0 ? env_kb : kb;
       build_band_budget(row0, nrows, rp, ci, cc, elem, st, (size_t)use * 1024);
       if (banded || env_kb > 0) return;
