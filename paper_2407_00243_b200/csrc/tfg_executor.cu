@@ -2216,7 +2216,7 @@ struct SpmmWork {
     // smallest stage budget that admits a band layout (more CTAs per SM); the
     // stencil consumer wants >= 8 mini-groups (R >= 32) per block
     for (int kb : {40, 64, 100}) {
-      if (dia && kb == 40 && env_kb == 0) continue;
+      if (dia && kb == 40 && env_kb == 0 && (size_t)cc * elem == 512) continue;
       const int use = env_kb > 0 ? env_kb : kb;
       build_band_budget(row0, nrows, rp, ci, cc, elem, st, (size_t)use * 1024);
       if (banded || env_kb > 0) return;
@@ -2352,7 +2352,7 @@ struct SpmmWork {
           }
         }
         const int nmg = (nr + kBandMG - 1) / kBandMG;
-        const bool rec_dia = dia && !use_union && R <= 128;
+        const bool rec_dia = dia && !use_union && R <= 128 && R >= 32;
         const int irec = ((nr + 1 + (k1 - k0) + (use_union ? nmg + 1 + (int)uent.size() : 0) +
                            (rec_dia ? 2 : 0)) + 7) / 8 * 8;
         const size_t need = (size_t)staged * row_bytes + (size_t)irec * 2 +
@@ -2401,7 +2401,8 @@ struct SpmmWork {
       banded = true;
       band_R = R;
       band_blocks = nb;
-      if (!(dia && !use_union && R <= 128)) dia = false;
+      // the stencil consumer needs >= 8 mini-groups per block (one per warp)
+      if (!(dia && !use_union && R <= 128 && R >= 32)) dia = false;
       if (dia) {
         dia_dev.alloc(1);
         h2d(dia_dev.p, &dia_lines, 1, st);
