@@ -624,6 +624,58 @@ __device__ __forceinline__ void band_dia_group(const T* __restrict__ xs, const T
       stv<T, VEC>(out_row0 + (size_t)q * ldo + (ch * 32 + lane) * VEC, acc[q][ch]);
 }
 
+// One row of a staged band block, a whole warp (LPR = 32) per row, reference
+// order.
+template <class T, int VEC, int NCH>
+__device__ __forceinline__ void band_row_warp(const T* __restrict__ xs, const T* __restrict__ vs,
+                                              const uint16_t* lrp, const uint16_t* lsl, int cc,
+                                              int r, int lane, T* __restrict__ o) {
+  const int eb = lrp[r], ee = lrp[r + 1];
+  T acc[NCH][VEC];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
+  for (int e0 = eb; e0 < ee; e0 += 32) {
+    const int sl = e0 + lane < ee ? lsl[e0 + lane] : 0;
+    const int cnt = min(32, ee - e0);
+    for (int u = 0; u < cnt; ++u) {
+      const int su = __shfl_sync(0xffffffffu, sl, u);
+      const T au = vs[e0 + u];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        T x[VEC];
+        ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * 32 + lane) * VEC);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
+      }
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * 32 + lane) * VEC, acc[ch]);
+}
+
+// All rows of a staged block with the stencil consumer: regular mini-groups
+// (bit g of the record's mask) through band_dia_group, the rest row by row.
+template <class T, int VEC, int NCH, int NWARPS>
+__device__ __forceinline__ void band_block_dia(const T* __restrict__ xs, const T* __restrict__ vs,
+                                               const uint16_t* lrp, const uint16_t* lsl, int cc,
+                                               int nr, const DiaLines& dl, int warp, int lane,
+                                               T* __restrict__ out_r0, int ldo) {
+  const int nnzb = lrp[nr];
+  const uint32_t reg = (uint32_t)lsl[nnzb] | ((uint32_t)lsl[nnzb + 1] << 16);
+  const int nmg = (nr + 3) / 4;
+  for (int g = warp; g < nmg; g += NWARPS) {
+    if ((reg >> g) & 1u) {
+      band_dia_group<T, VEC, NCH>(xs, vs, lrp, lsl, cc, 4 * g, dl, lane,
+                                  out_r0 + (size_t)(4 * g) * ldo, ldo);
+      continue;
+    }
+    for (int r = 4 * g; r < min(4 * g + 4, nr); ++r)
+      band_row_warp<T, VEC, NCH>(xs, vs, lrp, lsl, cc, r, lane, out_r0 + (size_t)r * ldo);
+  }
+}
+
 template <class T, int VEC, int LPR, int NCH, int STAGES, bool DIA = false>
 __global__ void __launch_bounds__(288, (DIA && NCH == 1) ? 2 : 1)
     k_spmm_band3(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
@@ -758,43 +810,8 @@ __global__ void __launch_bounds__(288, (DIA && NCH == 1) ? 2 : 1)
     const uint16_t* lrp = is;
     const uint16_t* lsl = is + nr + 1;
     if constexpr (DIA) {
-      const int nnzb = lrp[nr];
-      const uint32_t reg = (uint32_t)lsl[nnzb] | ((uint32_t)lsl[nnzb + 1] << 16);
-      const int nmg = (nr + 3) / 4;
-      for (int g = warp; g < nmg; g += NCONS) {
-        if ((reg >> g) & 1u) {
-          band_dia_group<T, VEC, NCH>(xs, vs, lrp, lsl, cc, 4 * g, dl, gl,
-                                      out + (size_t)(r_lo + 4 * g) * ldo, ldo);
-          continue;
-        }
-        for (int r = 4 * g; r < min(4 * g + 4, nr); ++r) {
-          const int eb = lrp[r], ee = lrp[r + 1];
-          T acc[NCH][VEC];
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-          for (int e0 = eb; e0 < ee; e0 += LPR) {
-            const int sl = e0 + gl < ee ? lsl[e0 + gl] : 0;
-            const int cnt = min(LPR, ee - e0);
-            for (int u = 0; u < cnt; ++u) {
-              const int su = __shfl_sync(gmask, sl, u, LPR);
-              const T au = vs[e0 + u];
-#pragma unroll
-              for (int ch = 0; ch < NCH; ++ch) {
-                T x[VEC];
-                ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
-#pragma unroll
-                for (int v = 0; v < VEC; ++v)
-                  acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
-              }
-            }
-          }
-          T* o = out + (size_t)(r_lo + r) * ldo;
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
-        }
-      }
+      band_block_dia<T, VEC, NCH, NCONS>(xs, vs, lrp, lsl, cc, nr, dl, warp, gl,
+                                         out + (size_t)r_lo * ldo, ldo);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       continue;
@@ -870,12 +887,13 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
   return v;
 }
 
-template <class T, int VEC, int LPR, int NCH, int STAGES>
-__global__ void __launch_bounds__(288, 1)
+template <class T, int VEC, int LPR, int NCH, int STAGES, bool DIA = false>
+__global__ void __launch_bounds__(288, (DIA && NCH == 1) ? 2 : 1)
     k_spmm_band_sweep(int nitems, const int* __restrict__ items, const int2* __restrict__ dep,
                       int* chunk_done, int chunk_shift, int epoch, BandSide<T> s0,
                       BandSide<T> s1, int stage_cap, int idx_cap, int val_cap, int cc,
-                      int dbg) {
+                      int dbg, const DiaLines* __restrict__ dl0p = nullptr,
+                      const DiaLines* __restrict__ dl1p = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
@@ -1028,6 +1046,14 @@ __global__ void __launch_bounds__(288, 1)
   const int gl = threadIdx.x & (LPR - 1);
   const unsigned gmask = group_mask(LPR);
   const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
+  __shared__ DiaLines dl_s[2];
+  if constexpr (DIA) {
+    if (threadIdx.x == 0) {
+      dl_s[0] = *dl0p;
+      dl_s[1] = *dl1p;
+    }
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");  // consumer warps only
+  }
   for (int it = 0; it < nmine; ++it) {
     const int code = __ldg(items + blockIdx.x + it * G);
     const int op = code >> kOpShift, b = code & kBlkMask;
@@ -1044,6 +1070,10 @@ __global__ void __launch_bounds__(288, 1)
     const int nr = min(R, row0 + nrows - r_lo);
     const uint16_t* lrp = is;
     const uint16_t* lsl = is + nr + 1;
+    if constexpr (DIA) {
+      band_block_dia<T, VEC, NCH, NCONS>(xs, vs, lrp, lsl, cc, nr, dl_s[op], warp, gl,
+                                         out + (size_t)r_lo * cc, cc);
+    } else
     for (int r = group; r < nr; r += ngroups) {
       const int eb = lrp[r], ee = lrp[r + 1];
       T acc[NCH][VEC];
@@ -2963,12 +2993,15 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
         (int)pl.sw_epoch,
         side(w0, pl.p.d_b_row_ptr, pl.p.d_b_val, pl.p.d_c, pl.d1.p),
         side(w1, pl.p.d_a_row_ptr, pl.p.d_a_val, pl.d1.p, pl.sweep_out), pl.sw_scap, pl.sw_icap,
-        pl.sw_vcap, cc, dbg);
+        pl.sw_vcap, cc, dbg, w0.dia_dev.p, w1.dia_dev.p);
     TFG_LAUNCH_CHECK();
   };
+  const bool dia = w0.dia && w1.dia && dia_on();
   if (L == 8) go(k_spmm_band_sweep<T, VEC, 8, 1, 2>);
   else if (L == 16) go(k_spmm_band_sweep<T, VEC, 16, 1, 2>);
+  else if (L == 32 && dia) go(k_spmm_band_sweep<T, VEC, 32, 1, 2, true>);
   else if (L == 32) go(k_spmm_band_sweep<T, VEC, 32, 1, 2>);
+  else if (L == 64 && dia) go(k_spmm_band_sweep<T, VEC, 32, 2, 2, true>);
   else if (L == 64) go(k_spmm_band_sweep<T, VEC, 32, 2, 2>);
   else throw runtime_error("band sweep: unsupported column count");
   return grid;
