@@ -28,8 +28,16 @@ print(json.dumps({k: [float(np.median([m for m, _ in v])), v[0][1] / float(np.me
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
     variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1"] + [str(k) for k in range(11)]
-    for v in variants:
+    for spec in variants:
         env = dict(os.environ)
+        # composite codes: "S1+D3" applies each part's environment in turn
+        parts = spec.split("+")
+        for extra in parts[:-1]:
+            key = {"X": "TFG_BAND_DIA_EXEC", "D": "TFG_SWEEP_DBG", "S": "TFG_SWEEP",
+                   "R": "TFG_TC_RING", "T": "TFG_TC_DBG"}.get(extra[:1])
+            if key:
+                env[key] = extra[1:]
+        v = parts[-1]
         if v.startswith("X"):  # stencil (DIA-window) band consumer on/off at execution
             env["TFG_BAND_DIA_EXEC"] = v[1:]
             v = "-1"
