@@ -87,7 +87,7 @@ def main():
         if v >= 0:
             env["TFG_SPMM_VARIANT"] = str(v)
         r = subprocess.run([sys.executable, "-c", CODE % (ROOT, cfg)], capture_output=True, text=True, env=env)
-        print(cfg, "variant", v, r.stdout.strip() or r.stderr[-500:], flush=True)
+        print(cfg, "variant", spec, r.stdout.strip() or r.stderr[-500:], flush=True)
 
 
 if __name__ == "__main__":
