@@ -207,6 +207,11 @@ tfg_status tfg_plan_info(const tfg_plan *plan, int64_t *spill_rows,
                          int64_t *fused_rows, int32_t *launches,
                          int64_t *scratch_bytes);
 
+/* Which kernel runs each stage, as a NUL-terminated string of the form
+ * "first_op=<k> fused=<k> wave1=<k>" (k: stencil3d, stencil2d, band, strip,
+ * tcgen05, gemm, ...); for reports and tests.  Truncated to len - 1 chars. */
+tfg_status tfg_plan_kernels(const tfg_plan *plan, char *buf, int32_t len);
+
 /* Execute once with CUDA events around each stage on `stream`, wait, and
  * report device milliseconds and algorithmic HBM bytes (each input byte read
  * once, each output byte written once) per stage:

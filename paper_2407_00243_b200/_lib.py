@@ -88,6 +88,7 @@ SIGNATURES = [
     ("tfg_plan_execute", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tfg_plan_stats", C.c_int, [C.c_void_p, i64p, i64p, i64p]),
     ("tfg_plan_info", C.c_int, [C.c_void_p, i64p, i64p, i32p, i64p]),
+    ("tfg_plan_kernels", C.c_int, [C.c_void_p, C.c_char_p, C.c_int32]),
     ("tfg_plan_profile", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, f64p, i64p]),
     ("tfg_plan_destroy", None, [C.c_void_p]),
     ("tfg_run_host", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p]),

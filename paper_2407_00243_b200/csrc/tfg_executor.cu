@@ -28,12 +28,15 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <memory>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "tfg_common.cuh"
 #include "tfg_device.cuh"
 #include "tfg_tc.cuh"
+#include "tfg_stencil.cuh"
 
 namespace tfg {
 namespace {
@@ -2460,6 +2463,9 @@ struct SpmmWork {
       return;
     }
   }
+  // grid stencil: the plane-streaming kernel replaces everything above
+  // (tfg_stencil.cu); set by the plan when every row is in the list
+  std::unique_ptr<StencilPlan> stencil;
   bool grouped = false;
   int64_t n_groups = 0, n_ucols = 0;
   int64_t n_pairs = 0;
@@ -2834,6 +2840,10 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
 template <class T>
 static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
                      const T* av, const T* X, int cc, T* out, cudaStream_t st) {
+  if (w.stencil) {
+    stencil_run(*w.stencil, rp, ci, av, out, st);
+    return;
+  }
   spmm_dispatch_short<T>(w, rp, ci, av, X, cc, out, st);
   if (w.n_long) {
     T* partial = reinterpret_cast<T*>(w.partial.p);
@@ -3005,6 +3015,27 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
   else if (L == 64) go(k_spmm_band_sweep<T, VEC, 32, 2, 2>);
   else throw runtime_error("band sweep: unsupported column count");
   return grid;
+}
+
+// Row-list SpMM over ALL rows of a grid-stencil CSR: switch it to the
+// plane-streaming kernel (tfg_stencil.cu).  X must hold n rows.
+static void attach_stencil(SpmmWork& w, int64_t n, const std::vector<int>& rp,
+                           const std::vector<int>& ci, const void* X, int cc, size_t elem) {
+  w.stencil.reset();
+  if (!stencil_env_enabled() || ci.empty() || !w.identity || w.row0 != 0 || w.n_short != n ||
+      w.n_long != 0 || n > INT32_MAX)
+    return;
+  StencilGeom g;
+  if (!stencil_detect((int)n, rp, ci, g)) return;
+  auto sp = std::make_unique<StencilPlan>();
+  if (!stencil_prepare(*sp, g, X, cc, (int)elem)) return;
+  if (getenv("TFG_DEBUG"))
+    fprintf(stderr,
+            "[tfg] stencil spmm: grid %d x %d x %d K=%d tile %d x %d zc %d ns %d slices %d "
+            "items %lld grid %d smem %zu\n",
+            g.nx, g.ny, g.nz, g.K, sp->tx, sp->ty, sp->zc, sp->ns, sp->slices,
+            (long long)sp->items, sp->grid, sp->smem);
+  w.stencil = std::move(sp);
 }
 
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
@@ -3328,6 +3359,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       TFG_CUDA(cudaStreamSynchronize(st));
     }
     pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st, bci.empty() ? nullptr : &bci);
+    if (pr.b_cols == n) attach_stencil(pl.fo_sparse, n, brp, bci, pr.d_c, cc, pl.elem);
   }
   // (c) second-op work (wavefront-1 rows, then the empty fused rows)
   if (!zero_rows.empty()) {
@@ -3342,6 +3374,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       TFG_CUDA(cudaStreamSynchronize(st));
     }
     pl.second.build(second_rows, arp, cc, pl.elem, st, aci.empty() ? nullptr : &aci);
+    attach_stencil(pl.second, n, arp, aci, pl.d1.p, cc, pl.elem);
   }
 
   // ---- algorithmic bytes per stage ------------------------------------
@@ -3423,6 +3456,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     const SpmmWork& w0 = pl.fo_sparse;
     const SpmmWork& w1 = pl.second;
     if (sweep_on && !pr.b_is_dense && pl.n_ftiles == 0 && !partial && w0.banded && w1.banded &&
+        !w0.stencil && !w1.stencil &&
         !w0.band_union && !w1.band_union && w0.n_long == 0 && w1.n_long == 0 && w0.row0 == 0 &&
         w1.row0 == 0 && w0.n_short == n && w1.n_short == n) {
       pl.sw_scap = std::max(w0.stage_cap, w1.stage_cap);
@@ -3778,6 +3812,40 @@ tfg_status tfg_plan_info(const tfg_plan* pl, int64_t* spill_rows, int64_t* fused
     if (fused_rows) *fused_rows = pl->fused_rows;
     if (launches) *launches = pl->launches + (pl->zero_d ? 1 : 0);
     if (scratch_bytes) *scratch_bytes = (int64_t)plan_scratch_bytes(*pl);
+  });
+}
+
+tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
+  return guard([&] {
+    if (!pl || !buf || len < 1) throw invalid_argument("plan_kernels: null plan or buffer");
+    auto spmm_kind = [](const SpmmWork& w) -> std::string {
+      if (w.n_short == 0 && w.n_long == 0) return "none";
+      std::string k;
+      if (w.stencil)
+        k = w.stencil->g.d3 ? "stencil3d" : "stencil2d";
+      else if (w.banded)
+        k = w.dia ? "band-dia" : "band";
+      else if (w.grouped)
+        k = "group";
+      else
+        k = w.skewed ? "strip-skewed" : "strip";
+      if (w.n_long) k += "+segments";
+      return k;
+    };
+    std::string fo;
+    if (pl->sweep)
+      fo = "sweep";
+    else if (pl->p.b_is_dense)
+      fo = pl->n_fo_blocks == 0 ? "none" : (pl->tc.on ? "tcgen05" : (pl->gemm_kind ? "gemm-v2" : "gemm"));
+    else
+      fo = spmm_kind(pl->fo_sparse);
+    std::string fu = pl->n_ftiles == 0 ? "none"
+                     : (pl->fused_v2 ? (pl->tc.on ? "tcgen05-tiles" : "gemm-tiles") : "tiles");
+    std::string w1 = pl->sweep ? "sweep" : spmm_kind(pl->second);
+    const std::string s = "first_op=" + fo + " fused=" + fu + " wave1=" + w1;
+    const size_t n = std::min(s.size(), (size_t)len - 1);
+    memcpy(buf, s.data(), n);
+    buf[n] = 0;
   });
 }
 

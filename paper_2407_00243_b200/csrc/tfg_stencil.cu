@@ -1,0 +1,614 @@
+// tfg_stencil.cu -- plane-streaming SpMM for grid stencils (see tfg_stencil.cuh).
+#include "tfg_stencil.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "tfg_device.cuh"
+
+namespace tfg {
+namespace {
+
+using dev::fops;
+using dev::ldv;
+using dev::stv;
+
+constexpr int kMaxNS = 8;      // plane ring depth cap
+constexpr size_t kSliceBytes = 512;  // column slice of X / out per CTA
+constexpr size_t kSmemBudget = 224 * 1024;
+
+struct StencilArgs {
+  int n, nx, ny, nz, nxy, K;
+  int zc, ns, slices, ntx, nty, cc;
+  long long items;
+  int plane_elems;
+  int pf;    // L2 prefetch distance (planes)
+  int full;  // the stencil is the whole 3x3 (x3) box: compile-time value offsets
+  int8_t rank[27];
+  const int* rp;
+  const int* ci;
+  const void* av;
+  void* out;
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void s_bar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void s_bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void s_bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void s_bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n ST_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      " @!p bra ST_WAIT_%=;\n}\n" ::"r"(s_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                       int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(s_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// Tile geometry.  2-D (9-point family): a tile is NW * M consecutive points
+// of one grid line, the sliding axis is y.  3-D (27-point family): a tile is
+// M x NW points of the (x, y) plane, one tile line per warp, sliding along z.
+template <bool D3, int NW, int M>
+struct Tile {
+  static constexpr int TX = D3 ? M : M * NW;
+  static constexpr int TY = D3 ? NW : 1;
+  static constexpr int ROW = TX + 2;           // plane row length incl. halo
+  static constexpr int TYH = D3 ? NW + 2 : 1;  // plane rows incl. halo
+};
+
+// Work item -> (column slice, x tile, y tile, z chunk); slices vary fastest so
+// co-resident CTAs share their tiles' halo rows in L2.
+__device__ __forceinline__ void decode_item(const StencilArgs& a, long long it, int& cs, int& itx,
+                                            int& ity, int& izc) {
+  cs = (int)(it % a.slices);
+  long long t = it / a.slices;
+  itx = (int)(t % a.ntx);
+  t /= a.ntx;
+  ity = (int)(t % a.nty);
+  izc = (int)(t / a.nty);
+}
+
+// Values of a warp's M consecutive rows are contiguous in the CSR: lanes load
+// them (one step ahead, coalesced) into registers and stage them in the
+// warp's shared-memory buffer, so the per-nonzero value reads are broadcast
+// shared loads instead of dependent global loads.
+template <class T, int VR>
+__device__ __forceinline__ void load_vals(const T* __restrict__ av, int v0, int v1, int lane,
+                                          T (&vr)[VR]) {
+#pragma unroll
+  for (int i = 0; i < VR; ++i) {
+    const int k = v0 + lane + 32 * i;
+    vr[i] = k < v1 ? __ldg(av + k) : T(0);
+  }
+}
+
+template <class T, int VEC>
+__device__ __forceinline__ void axpy(T (&acc)[VEC], T v, const T (&x)[VEC]) {
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = fops<T>::add(acc[e], fops<T>::mul(v, x[e]));
+}
+
+// One output plane z of a warp's M points.  P0/P1/P2: the shared-memory
+// planes z-1, z, z+1 of the tile (zero-filled outside the grid); rpl: lane
+// m <= M holds row_ptr of point m; valid: points inside the grid; sv: the
+// rows' values from row_ptr[point 0].
+template <class T, bool D3, int NW, int M>
+__device__ __forceinline__ void stencil_points(const StencilArgs& a, const T* __restrict__ P0,
+                                               const T* __restrict__ P1, const T* __restrict__ P2,
+                                               const T* __restrict__ sv, int rpl, unsigned valid,
+                                               int wy, int wx, int rbase, int cs, int lane) {
+  using TL = Tile<D3, NW, M>;
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int CW = (int)(kSliceBytes / sizeof(T));
+  constexpr int NL = D3 ? 9 : 3;
+  const int v0 = __shfl_sync(0xffffffffu, rpl, 0);
+  const int vM = __shfl_sync(0xffffffffu, rpl, M);
+  // every row has <= K nonzeros, so M * K of them means all M rows are full
+  const bool fast = a.full && valid == (1u << M) - 1 && vM - v0 == M * 3 * NL;
+  int vb[M + 1];
+  unsigned reg = 0;
+  if (!fast) {
+#pragma unroll
+    for (int m = 0; m <= M; ++m) vb[m] = __shfl_sync(0xffffffffu, rpl, m);
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+      if (((valid >> m) & 1u) && vb[m + 1] - vb[m] == a.K) reg |= 1u << m;
+  }
+  T acc[M][VEC];
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[m][v] = T(0);
+  const int col0 = wx * M;  // tile column of x - 1
+  if (fast) {
+    // whole box, every point interior: point m's value for line l, dx is
+    // sv[m * K + 3 * l + dx + 1] -- all offsets compile-time
+    constexpr int K = 3 * NL;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int dz = D3 ? l / 3 - 1 : l - 1;
+      const int dy = D3 ? l % 3 - 1 : 0;
+      const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+      const T* base = P + ((D3 ? (wy + 1 + dy) * TL::ROW : 0) + col0) * CW + lane * VEC;
+#pragma unroll
+      for (int k = 0; k < M + 2; ++k) {
+        T xr[VEC];
+        ldv<T, VEC>(xr, base + k * CW);
+        if (k < M) axpy<T, VEC>(acc[k], sv[k * K + 3 * l], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC>(acc[k - 1], sv[(k - 1) * K + 3 * l + 1], xr);
+        if (k >= 2) axpy<T, VEC>(acc[k - 2], sv[(k - 2) * K + 3 * l + 2], xr);
+      }
+    }
+  } else {
+    if (reg) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const int dz = D3 ? l / 3 - 1 : l - 1;
+        const int dy = D3 ? l % 3 - 1 : 0;
+        const int li = (dz + 1) * 3 + (dy + 1);
+        const int rk0 = a.rank[li * 3 + 0], rk1 = a.rank[li * 3 + 1], rk2 = a.rank[li * 3 + 2];
+        if (rk0 < 0 && rk1 < 0 && rk2 < 0) continue;
+        const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+        const T* base = P + ((D3 ? (wy + 1 + dy) * TL::ROW : 0) + col0) * CW + lane * VEC;
+#pragma unroll
+        for (int k = 0; k < M + 2; ++k) {
+          T xr[VEC];
+          ldv<T, VEC>(xr, base + k * CW);
+          // this row is neighbour dx = -1 of point k, 0 of k - 1, +1 of k - 2
+          if (k < M && rk0 >= 0 && ((reg >> k) & 1u))
+            axpy<T, VEC>(acc[k], sv[vb[k] - v0 + rk0], xr);
+          if (k >= 1 && k - 1 < M && rk1 >= 0 && ((reg >> (k - 1)) & 1u))
+            axpy<T, VEC>(acc[k - 1], sv[vb[k - 1] - v0 + rk1], xr);
+          if (k >= 2 && rk2 >= 0 && ((reg >> (k - 2)) & 1u))
+            axpy<T, VEC>(acc[k - 2], sv[vb[k - 2] - v0 + rk2], xr);
+        }
+      }
+    }
+    const unsigned irr = valid & ~reg;
+    if (irr) {  // grid-face rows: their own CSR order, neighbours from the planes
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        if (!((irr >> m) & 1u)) continue;
+        const int r = rbase + m;
+        for (int k = vb[m]; k < vb[m + 1]; ++k) {
+          int o = __ldg(a.ci + k) - r;
+          int dz = 0, dy = 0;
+          if (D3) {
+            dz = o > a.nxy / 2 ? 1 : (o < -(a.nxy / 2) ? -1 : 0);
+            o -= dz * a.nxy;
+            dy = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
+            o -= dy * a.nx;
+          } else {
+            dz = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
+            o -= dz * a.nx;
+          }
+          const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+          const int yy = D3 ? wy + 1 + dy : 0;
+          T xr[VEC];
+          ldv<T, VEC>(xr, P + (yy * TL::ROW + col0 + m + 1 + o) * CW + lane * VEC);
+          axpy<T, VEC>(acc[m], sv[k - v0], xr);
+        }
+      }
+    }
+  }
+  T* out = static_cast<T*>(a.out);
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+    if ((valid >> m) & 1u)
+      stv<T, VEC>(out + (size_t)(rbase + m) * a.cc + (size_t)cs * CW + lane * VEC, acc[m]);
+}
+
+template <class T, bool D3, int NW, int M, int MINB>
+__global__ void __launch_bounds__((NW + 1) * 32, MINB)
+    k_spmm_stencil(const __grid_constant__ CUtensorMap xmap, const StencilArgs a) {
+  using TL = Tile<D3, NW, M>;
+  constexpr int CW = (int)(kSliceBytes / sizeof(T));
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxNS], empty[kMaxNS];
+  T* planes = reinterpret_cast<T*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ns = a.ns;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      s_bar_init(&full[s], 1);
+      s_bar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t plane_bytes = (uint32_t)a.plane_elems * sizeof(T);
+  if (warp == NW) {
+    // ---------------- producer: one 4-D TMA copy per tile plane ----------------
+    if (lane == 0) {
+      // L2 prefetch runs a.pf planes ahead of the loads along this CTA's
+      // plane sequence (across item boundaries), so a ring slot's TMA load
+      // finds its plane in L2 instead of paying the HBM latency
+      long long pit = blockIdx.x;
+      int pcs = 0, pc1 = 0, pc2 = 0, pz = 0, pz1 = -1;
+      auto pf_next = [&]() {
+        while (pz > pz1) {
+          if (pit >= a.items) return;
+          int itx, ity, izc;
+          decode_item(a, pit, pcs, itx, ity, izc);
+          pit += gridDim.x;
+          pc1 = itx * TL::TX - 1;
+          pc2 = D3 ? ity * TL::TY - 1 : 0;
+          pz = izc * a.zc - 1;
+          pz1 = min(izc * a.zc + a.zc, a.nz);
+        }
+        tma_prefetch_4d(&xmap, pcs * CW, pc1, pc2, pz);
+        ++pz;
+      };
+      for (int k = 0; k < a.pf; ++k) pf_next();
+      uint32_t g = 0;
+      for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
+        int cs, itx, ity, izc;
+        decode_item(a, it, cs, itx, ity, izc);
+        const int z0 = izc * a.zc, z1 = min(z0 + a.zc, a.nz);
+        const int c1 = itx * TL::TX - 1;
+        const int c2 = D3 ? ity * TL::TY - 1 : 0;
+        for (int p = z0 - 1; p <= z1; ++p, ++g) {
+          if (a.pf) pf_next();
+          const int s = (int)(g % ns);
+          const uint32_t k = g / ns;
+          if (k > 0) s_bar_wait(&empty[s], (k - 1) & 1u);
+          s_bar_expect(&full[s], plane_bytes);
+          tma_4d(planes + (size_t)s * a.plane_elems, &xmap, cs * CW, c1, c2, p, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  constexpr int VR = (M * (D3 ? 27 : 9) + 31) / 32;  // value registers per lane
+  const T* __restrict__ av = static_cast<const T*>(a.av);
+  T* sv = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * VR * 32;
+  const int wy = D3 ? warp : 0, wx = D3 ? 0 : warp;
+  int s0 = 0;        // ring slot of the current item's plane z-1
+  uint32_t p0 = 0;   // its full-barrier phase parity
+  for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
+    int cs, itx, ity, izc;
+    decode_item(a, it, cs, itx, ity, izc);
+    const int z0 = izc * a.zc, z1 = min(z0 + a.zc, a.nz);
+    const int nzl = z1 - z0;
+    const int x = itx * TL::TX + wx * M;
+    const int y = D3 ? ity * TL::TY + wy : 0;
+    const bool yvalid = y < a.ny;
+    const bool live = yvalid && x < a.nx && lane <= M;
+    unsigned valid = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+      if (yvalid && x + m < a.nx) valid |= 1u << m;
+    const int r0 = (z0 * a.ny + y) * a.nx + x;  // point 0 at output plane z0
+    // row pointers three planes ahead, values two planes ahead
+    auto rp_at = [&](int jj) {
+      return live && jj < nzl ? __ldg(a.rp + min(r0 + jj * a.nxy + lane, a.n)) : 0;
+    };
+    int rpa = rp_at(0), rpb = rp_at(1), rpc = rp_at(2);
+    T vr0[VR], vr1[VR];
+    load_vals<T, VR>(av, __shfl_sync(0xffffffffu, rpa, 0), __shfl_sync(0xffffffffu, rpa, M),
+                     lane, vr0);
+    load_vals<T, VR>(av, __shfl_sync(0xffffffffu, rpb, 0), __shfl_sync(0xffffffffu, rpb, M),
+                     lane, vr1);
+    for (int j = 0; j < nzl; ++j) {
+#pragma unroll
+      for (int i = 0; i < VR; ++i) sv[lane + 32 * i] = vr0[i];
+      const int rp_j = rpa;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < VR; ++i) vr0[i] = vr1[i];
+      if (j + 2 < nzl)
+        load_vals<T, VR>(av, __shfl_sync(0xffffffffu, rpc, 0), __shfl_sync(0xffffffffu, rpc, M),
+                         lane, vr1);
+      rpa = rpb;
+      rpb = rpc;
+      rpc = rp_at(j + 3);
+      // ring positions of planes z-1 (s0), z (s1), z+1 (s2)
+      int s1 = s0 + 1, s2;
+      uint32_t p1 = p0, p2;
+      if (s1 == ns) s1 = 0, p1 ^= 1u;
+      s2 = s1 + 1;
+      p2 = p1;
+      if (s2 == ns) s2 = 0, p2 ^= 1u;
+      if (j == 0) {
+        s_bar_wait(&full[s0], p0);
+        s_bar_wait(&full[s1], p1);
+      }
+      s_bar_wait(&full[s2], p2);
+      stencil_points<T, D3, NW, M>(a, planes + (size_t)s0 * a.plane_elems,
+                                   planes + (size_t)s1 * a.plane_elems,
+                                   planes + (size_t)s2 * a.plane_elems, sv, rp_j, valid, wy, wx,
+                                   r0 + j * a.nxy, cs, lane);
+      __syncwarp();
+      if (lane == 0) {
+        s_bar_arrive(&empty[s0]);
+        if (j == nzl - 1) {
+          s_bar_arrive(&empty[s1]);
+          s_bar_arrive(&empty[s2]);
+        }
+      }
+      if (j == nzl - 1) {  // the next item starts at the plane after s2
+        s0 = s2 + 1;
+        p0 = p2;
+        if (s0 == ns) s0 = 0, p0 ^= 1u;
+      } else {
+        s0 = s1;
+        p0 = p1;
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int env_int(const char* name, int def) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : def;
+}
+
+// Every nonzero of the CSR decomposes as an in-grid neighbour of its row.
+bool check_geom(int n, const std::vector<int>& rp, const std::vector<int>& ci, int nx, int ny,
+                StencilGeom& g) {
+  const int64_t nxy = (int64_t)nx * ny;
+  if (nx < 3 || (ny > 1 && ny < 3) || n % nxy != 0) return false;
+  const int nz = (int)(n / nxy);
+  bool used[27] = {};
+  for (int r = 0; r < n; ++r) {
+    const int x = r % nx, y = (int)((r / nx) % ny), z = (int)(r / nxy);
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      int64_t o = (int64_t)ci[k] - r;
+      int dz, dy = 0;
+      if (ny > 1) {
+        dz = o > nxy / 2 ? 1 : (o < -(nxy / 2) ? -1 : 0);
+        o -= dz * nxy;
+        dy = o > nx / 2 ? 1 : (o < -(nx / 2) ? -1 : 0);
+        o -= (int64_t)dy * nx;
+      } else {
+        dz = o > nx / 2 ? 1 : (o < -(nx / 2) ? -1 : 0);
+        o -= (int64_t)dz * nx;
+      }
+      const int dx = (int)o;
+      if (dx < -1 || dx > 1) return false;
+      if (x + dx < 0 || x + dx >= nx || y + dy < 0 || y + dy >= ny || z + dz < 0 ||
+          z + dz >= nz)
+        return false;
+      used[((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1)] = true;
+    }
+  }
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = nz;
+  g.d3 = ny > 1;
+  g.K = 0;
+  for (int q = 0; q < 27; ++q) g.rank[q] = used[q] ? (int8_t)g.K++ : (int8_t)-1;
+  return g.K > 0;
+}
+
+}  // namespace
+
+int stencil_env_enabled() { return env_int("TFG_STENCIL", 1); }
+
+bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& ci,
+                    StencilGeom& g) {
+  g = StencilGeom{};
+  if (n < 9 || (int)rp.size() < n + 1 || rp[n] == 0 || (int64_t)ci.size() < rp[n]) return false;
+  // the offset set (col - row) over all rows; a grid stencil has <= 27
+  std::vector<int64_t> offs;
+  for (int r = 0; r < n; ++r)
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      const int64_t o = (int64_t)ci[k] - r;
+      if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+        offs.push_back(o);
+        if (offs.size() > 27) return false;
+      }
+    }
+  std::sort(offs.begin(), offs.end());
+  std::vector<int64_t> pos;
+  for (int64_t o : offs)
+    if (o >= 2) pos.push_back(o);
+  if (pos.empty()) return false;
+  // x stride: the smallest offset >= 2 is nx + dx for some dx in {-1, 0, 1}
+  for (int64_t nxc : {pos[0] + 1, pos[0], pos[0] - 1}) {
+    if (nxc < 3 || nxc > n) continue;
+    if (check_geom(n, rp, ci, (int)nxc, 1, g)) return true;
+    // 3-D: the smallest offset beyond the x line is nx*ny + dy*nx + dx
+    for (int64_t o2 : pos) {
+      if (o2 <= nxc + 1) continue;
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int64_t nxy = o2 - dy * nxc - dx;
+          if (nxy % nxc != 0) continue;
+          const int64_t nyc = nxy / nxc;
+          if (nyc < 3 || n % nxy != 0) continue;
+          if (check_geom(n, rp, ci, (int)nxc, (int)nyc, g)) return true;
+        }
+      break;
+    }
+  }
+  g = StencilGeom{};
+  return false;
+}
+
+bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int cc, int elem) {
+  sp.on = false;
+  if (!stencil_env_enabled() || g.nx == 0) return false;
+  if ((size_t)cc * elem % kSliceBytes != 0 || (uintptr_t)X % 16 != 0) return false;
+  auto enc = encode_tiled();
+  if (!enc) return false;
+  sp.g = g;
+  sp.elem = elem;
+  sp.cc = cc;
+  const int m_env = env_int("TFG_STENCIL_M", 0);
+  sp.M = m_env == 4 || m_env == 8 ? m_env : 4;
+  sp.cw = (int)(kSliceBytes / elem);
+  sp.slices = (int)((size_t)cc * elem / kSliceBytes);
+  // warps per CTA: 2-D tiles of 4 warps (32 points, small planes, several
+  // CTAs per SM with a deep ring); 3-D tiles of 8 x 8 points (one CTA per SM)
+  const int nw_env = env_int("TFG_STENCIL_NW", 0);
+  sp.nw = nw_env == 4 || nw_env == 8 ? nw_env : 8;
+  if (g.d3) {
+    sp.ty = sp.nw;
+    sp.tx = sp.M;
+    sp.tyh = sp.ty + 2;
+  } else {
+    sp.ty = 1;
+    sp.tx = sp.M * sp.nw;
+    sp.tyh = 1;
+  }
+  sp.ntx = (g.nx + sp.tx - 1) / sp.tx;
+  sp.nty = (g.ny + sp.ty - 1) / sp.ty;
+  sp.plane_bytes = (size_t)sp.cw * (sp.tx + 2) * sp.tyh * elem;
+  const size_t vbytes = (size_t)sp.nw * ((sp.M * (g.d3 ? 27 : 9) + 31) / 32) * 32 * elem;
+  // CTAs per SM, then the deepest ring that fits (>= 3 planes in use)
+  const int per_env = env_int("TFG_STENCIL_CTAS", 0);
+  int per_sm = per_env > 0 ? per_env : (g.d3 ? 1 : 2);
+  int ns = 0;
+  for (; per_sm >= 1; --per_sm) {
+    const size_t budget = kSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
+    ns = (int)std::min<size_t>(kMaxNS, (budget - std::min(budget, vbytes)) / sp.plane_bytes);
+    if (ns >= 3) break;
+  }
+  if (per_sm < 1 || ns < 3) return false;
+  const int ns_env = env_int("TFG_STENCIL_NS", 0);
+  if (ns_env >= 3) ns = std::min(ns, ns_env);
+  sp.ns = ns;
+  sp.pf = std::max(0, env_int("TFG_STENCIL_PF", 0));  // L2 prefetch measured no gain
+  sp.smem = ns * sp.plane_bytes + vbytes;
+  sp.grid = sm_count() * per_sm;
+  // z chunk: balance items over the persistent grid (each item re-reads two
+  // halo planes)
+  const int64_t tiles = (int64_t)sp.ntx * sp.nty * sp.slices;
+  const int zc_env = env_int("TFG_STENCIL_ZC", 0);
+  int best = g.nz;
+  double best_cost = 1e300;
+  // short chunks measured best on cfg2 (16 planes: 0.239 ms vs 0.26 at 24-28)
+  for (int zc = std::min(8, g.nz); zc <= std::min(16, std::max(1, g.nz)); ++zc) {
+    const int64_t nzc = (g.nz + zc - 1) / zc;
+    const int64_t items = tiles * nzc;
+    const double waves = (double)((items + sp.grid - 1) / sp.grid);
+    const double cost = waves * (zc + 2);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = zc;
+    }
+  }
+  sp.zc = zc_env > 0 ? zc_env : best;
+  sp.nzc = (g.nz + sp.zc - 1) / sp.zc;
+  sp.items = tiles * sp.nzc;
+  sp.grid = (int)std::min<int64_t>(sp.grid, sp.items);
+  cuuint64_t dims[4] = {(cuuint64_t)cc, (cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
+  cuuint64_t strides[3] = {(cuuint64_t)cc * elem, (cuuint64_t)cc * elem * g.nx,
+                           (cuuint64_t)cc * elem * g.nx * g.ny};
+  cuuint32_t box[4] = {(cuuint32_t)sp.cw, (cuuint32_t)(sp.tx + 2), (cuuint32_t)sp.tyh, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  if (enc(&sp.xmap, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+          4, const_cast<void*>(X), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  sp.on = true;
+  return true;
+}
+
+template <class T, bool D3, int NW, int M>
+static void stencil_launch(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
+  auto kern = k_spmm_stencil<T, D3, NW, M, D3 ? 1 : 2>;
+  TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
+  kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, a);
+  TFG_LAUNCH_CHECK();
+}
+
+template <class T, bool D3>
+static void stencil_launch_d(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
+  if (sp.nw == 8 && sp.M == 8)
+    stencil_launch<T, D3, 8, 8>(sp, a, st);
+  else if (sp.nw == 8)
+    stencil_launch<T, D3, 8, 4>(sp, a, st);
+  else if (sp.M == 8)
+    stencil_launch<T, D3, 4, 8>(sp, a, st);
+  else
+    stencil_launch<T, D3, 4, 4>(sp, a, st);
+}
+
+template <class T>
+static void stencil_launch_t(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
+  if (sp.g.d3)
+    stencil_launch_d<T, true>(sp, a, st);
+  else
+    stencil_launch_d<T, false>(sp, a, st);
+}
+
+void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void* av, void* out,
+                 cudaStream_t st) {
+  StencilArgs a{};
+  const StencilGeom& g = sp.g;
+  a.n = g.nx * g.ny * g.nz;
+  a.nx = g.nx;
+  a.ny = g.ny;
+  a.nz = g.nz;
+  a.nxy = g.nx * g.ny;
+  a.K = g.K;
+  a.zc = sp.zc;
+  a.ns = sp.ns;
+  a.slices = sp.slices;
+  a.ntx = sp.ntx;
+  a.nty = sp.nty;
+  a.cc = sp.cc;
+  a.items = sp.items;
+  a.plane_elems = (int)(sp.plane_bytes / sp.elem);
+  a.full = g.K == (g.d3 ? 27 : 9);
+  a.pf = sp.pf;
+  memcpy(a.rank, g.rank, sizeof(a.rank));
+  a.rp = rp;
+  a.ci = ci;
+  a.av = av;
+  a.out = out;
+  if (sp.elem == 8)
+    stencil_launch_t<double>(sp, a, st);
+  else
+    stencil_launch_t<float>(sp, a, st);
+}
+
+}  // namespace tfg

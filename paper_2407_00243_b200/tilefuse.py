@@ -479,6 +479,12 @@ class Plan:
         self.spill_rows, self.fused_rows = sp.value, fr.value
         self.launches, self.scratch_bytes = la.value, sb.value
 
+    def kernels(self) -> dict:
+        """Kernel chosen for each stage: {"first_op": ..., "fused": ..., "wave1": ...}."""
+        buf = C.create_string_buffer(256)
+        check(lib().tfg_plan_kernels(self._h, buf, 256))
+        return dict(kv.split("=", 1) for kv in buf.value.decode().split())
+
     def stats(self):
         """RunStats (kernels.hpp:46-50): first_op_rows, second_op_rows, nnz_processed."""
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()

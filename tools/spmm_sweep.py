@@ -32,6 +32,10 @@ def main():
         env = dict(os.environ)
         # composite codes: "S1+D3" applies each part's environment in turn
         parts = spec.split("+")
+        for extra in [q for q in parts if q.startswith("@")]:  # "@VAR=value": any env knob
+            k_, v_ = extra[1:].split("=", 1)
+            env[k_] = v_
+        parts = [q for q in parts if not q.startswith("@")] or ["-1"]
         for extra in parts[:-1]:
             key = {"X": "TFG_BAND_DIA_EXEC", "D": "TFG_SWEEP_DBG", "S": "TFG_SWEEP",
                    "R": "TFG_TC_RING", "T": "TFG_TC_DBG"}.get(extra[:1])
