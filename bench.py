@@ -352,6 +352,7 @@ def run_ours(args, rank, world, dist):
             "bytes_alg": w.bytes_alg(plan.spill_rows), "bytes_alg_stages": step_bytes,
             "step_hbm_frac_of_peak": (step_bytes / (single_ms * 1e-3) / 1e9) / peak,
             "stages_ms": {k: v[0] for k, v in stage_avg.items()},
+            "kernels": plan.kernels(),
             "l2": f"flushed between timed steps ({args.flush_mib} MiB write, outside the events)",
             "parallelism": parallelism},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,

@@ -98,6 +98,20 @@ __device__ __forceinline__ void decode_item(const StencilArgs& a, long long it, 
   izc = (int)(t / a.nty);
 }
 
+template <int BYTES>
+__device__ __forceinline__ void cp_async_ca(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s_u32(dst)), "l"(src),
+               "n"(BYTES)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // Values of a warp's M consecutive rows are contiguous in the CSR: lanes load
 // them (one step ahead, coalesced) into registers and stage them in the
 // warp's shared-memory buffer, so the per-nonzero value reads are broadcast
@@ -290,9 +304,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     return;
   }
   // ---------------- consumers ----------------
-  constexpr int VR = (M * (D3 ? 27 : 9) + 31) / 32;  // value registers per lane
+  // Per warp, the values and row pointers of its points stream into shared
+  // memory by cp.async, values two output planes ahead and row pointers four
+  // ahead (one commit group per plane), so no consumer instruction waits on
+  // a global load.
+  constexpr int VR = (M * (D3 ? 27 : 9) + 31) / 32;  // value elements per lane and plane
+  constexpr int VS = VR * 32;                         // value slot (elements)
   const T* __restrict__ av = static_cast<const T*>(a.av);
-  T* sv = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * VR * 32;
+  T* svb = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * 3 * VS;
+  int* srp = reinterpret_cast<int*>(reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) +
+                                    (size_t)NW * 3 * VS) + warp * 8 * 16;
   const int wy = D3 ? warp : 0, wx = D3 ? 0 : warp;
   int s0 = 0;        // ring slot of the current item's plane z-1
   uint32_t p0 = 0;   // its full-barrier phase parity
@@ -310,29 +331,38 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     for (int m = 0; m < M; ++m)
       if (yvalid && x + m < a.nx) valid |= 1u << m;
     const int r0 = (z0 * a.ny + y) * a.nx + x;  // point 0 at output plane z0
-    // row pointers three planes ahead, values two planes ahead
-    auto rp_at = [&](int jj) {
-      return live && jj < nzl ? __ldg(a.rp + min(r0 + jj * a.nxy + lane, a.n)) : 0;
+    auto issue_rp = [&](int jj) {
+      if (live && jj < nzl) cp_async_ca<4>(srp + (jj & 7) * 16 + lane, a.rp + min(r0 + jj * a.nxy + lane, a.n));
     };
-    int rpa = rp_at(0), rpb = rp_at(1), rpc = rp_at(2);
-    T vr0[VR], vr1[VR];
-    load_vals<T, VR>(av, __shfl_sync(0xffffffffu, rpa, 0), __shfl_sync(0xffffffffu, rpa, M),
-                     lane, vr0);
-    load_vals<T, VR>(av, __shfl_sync(0xffffffffu, rpb, 0), __shfl_sync(0xffffffffu, rpb, M),
-                     lane, vr1);
+    const bool wlive = yvalid && x < a.nx;  // warp-uniform: the warp has points
+    auto issue_vals = [&](int jj) {  // row pointers of plane jj must be visible
+      if (!wlive || jj >= nzl) return;
+      const int v0 = srp[(jj & 7) * 16], v1 = srp[(jj & 7) * 16 + M];
+      T* dst = svb + (jj % 3) * VS;
+#pragma unroll
+      for (int i = 0; i < VR; ++i) {
+        const int k = v0 + lane + 32 * i;
+        if (k < v1) cp_async_ca<sizeof(T)>(dst + lane + 32 * i, av + k);
+      }
+    };
+    issue_rp(0);
+    issue_rp(1);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    issue_vals(0);
+    issue_rp(2);
+    cp_async_commit();
+    issue_vals(1);
+    issue_rp(3);
+    cp_async_commit();
     for (int j = 0; j < nzl; ++j) {
-#pragma unroll
-      for (int i = 0; i < VR; ++i) sv[lane + 32 * i] = vr0[i];
-      const int rp_j = rpa;
+      cp_async_wait<1>();  // values of plane j, row pointers of plane j + 2
       __syncwarp();
-#pragma unroll
-      for (int i = 0; i < VR; ++i) vr0[i] = vr1[i];
-      if (j + 2 < nzl)
-        load_vals<T, VR>(av, __shfl_sync(0xffffffffu, rpc, 0), __shfl_sync(0xffffffffu, rpc, M),
-                         lane, vr1);
-      rpa = rpb;
-      rpb = rpc;
-      rpc = rp_at(j + 3);
+      issue_vals(j + 2);
+      issue_rp(j + 4);
+      cp_async_commit();
+      const int rp_j = live ? srp[(j & 7) * 16 + lane] : 0;
       // ring positions of planes z-1 (s0), z (s1), z+1 (s2)
       int s1 = s0 + 1, s2;
       uint32_t p1 = p0, p2;
@@ -347,8 +377,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       s_bar_wait(&full[s2], p2);
       stencil_points<T, D3, NW, M>(a, planes + (size_t)s0 * a.plane_elems,
                                    planes + (size_t)s1 * a.plane_elems,
-                                   planes + (size_t)s2 * a.plane_elems, sv, rp_j, valid, wy, wx,
-                                   r0 + j * a.nxy, cs, lane);
+                                   planes + (size_t)s2 * a.plane_elems, svb + (j % 3) * VS, rp_j,
+                                   valid, wy, wx, r0 + j * a.nxy, cs, lane);
       __syncwarp();
       if (lane == 0) {
         s_bar_arrive(&empty[s0]);
@@ -366,6 +396,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
         p0 = p1;
       }
     }
+    cp_async_wait<0>();
   }
 }
 
@@ -480,14 +511,13 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   sp.g = g;
   sp.elem = elem;
   sp.cc = cc;
-  const int m_env = env_int("TFG_STENCIL_M", 0);
-  sp.M = m_env == 4 || m_env == 8 ? m_env : 4;
+  sp.M = 4;  // 8 points per warp measured slower (register pressure, fewer warps)
   sp.cw = (int)(kSliceBytes / elem);
   sp.slices = (int)((size_t)cc * elem / kSliceBytes);
   // warps per CTA: 2-D tiles of 4 warps (32 points, small planes, several
   // CTAs per SM with a deep ring); 3-D tiles of 8 x 8 points (one CTA per SM)
   const int nw_env = env_int("TFG_STENCIL_NW", 0);
-  sp.nw = nw_env == 4 || nw_env == 8 ? nw_env : 8;
+  sp.nw = nw_env == 4 || nw_env == 8 ? nw_env : 4;
   if (g.d3) {
     sp.ty = sp.nw;
     sp.tx = sp.M;
@@ -500,10 +530,12 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   sp.ntx = (g.nx + sp.tx - 1) / sp.tx;
   sp.nty = (g.ny + sp.ty - 1) / sp.ty;
   sp.plane_bytes = (size_t)sp.cw * (sp.tx + 2) * sp.tyh * elem;
-  const size_t vbytes = (size_t)sp.nw * ((sp.M * (g.d3 ? 27 : 9) + 31) / 32) * 32 * elem;
+  // per warp: 3 value slots + 8 row-pointer slots (consumer cp.async ring)
+  const size_t vbytes =
+      (size_t)sp.nw * (3 * ((sp.M * (g.d3 ? 27 : 9) + 31) / 32) * 32 * elem + 8 * 16 * 4);
   // CTAs per SM, then the deepest ring that fits (>= 3 planes in use)
   const int per_env = env_int("TFG_STENCIL_CTAS", 0);
-  int per_sm = per_env > 0 ? per_env : (g.d3 ? 1 : 2);
+  int per_sm = per_env > 0 ? std::min(per_env, sp.nw == 8 ? 2 : 4) : (sp.nw == 8 ? (g.d3 ? 1 : 2) : 3);
   int ns = 0;
   for (; per_sm >= 1; --per_sm) {
     const size_t budget = kSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
@@ -516,6 +548,7 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   sp.ns = ns;
   sp.pf = std::max(0, env_int("TFG_STENCIL_PF", 0));  // L2 prefetch measured no gain
   sp.smem = ns * sp.plane_bytes + vbytes;
+  sp.per_sm = per_sm;
   sp.grid = sm_count() * per_sm;
   // z chunk: balance items over the persistent grid (each item re-reads two
   // halo planes)
@@ -552,24 +585,31 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   return true;
 }
 
-template <class T, bool D3, int NW, int M>
+template <class T, bool D3, int NW, int MINB>
 static void stencil_launch(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
-  auto kern = k_spmm_stencil<T, D3, NW, M, D3 ? 1 : 2>;
+  auto kern = k_spmm_stencil<T, D3, NW, 4, MINB>;
   TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
   kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, a);
   TFG_LAUNCH_CHECK();
 }
 
+// register budget cut for the resident CTAs per SM the plan chose
 template <class T, bool D3>
 static void stencil_launch_d(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
-  if (sp.nw == 8 && sp.M == 8)
-    stencil_launch<T, D3, 8, 8>(sp, a, st);
-  else if (sp.nw == 8)
-    stencil_launch<T, D3, 8, 4>(sp, a, st);
-  else if (sp.M == 8)
-    stencil_launch<T, D3, 4, 8>(sp, a, st);
-  else
-    stencil_launch<T, D3, 4, 4>(sp, a, st);
+  const int r = sp.per_sm;
+  if (sp.nw == 8) {
+    if (r >= 2)
+      stencil_launch<T, D3, 8, 2>(sp, a, st);
+    else
+      stencil_launch<T, D3, 8, 1>(sp, a, st);
+  } else {
+    if (r >= 4)
+      stencil_launch<T, D3, 4, 4>(sp, a, st);
+    else if (r == 3)
+      stencil_launch<T, D3, 4, 3>(sp, a, st);
+    else
+      stencil_launch<T, D3, 4, 2>(sp, a, st);
+  }
 }
 
 template <class T>

@@ -53,6 +53,7 @@ struct StencilPlan {
   int ntx = 0, nty = 0, nzc = 0;
   int64_t items = 0;
   size_t plane_bytes = 0, smem = 0;
+  int per_sm = 1;       // resident CTAs per SM the launch is built for
   int grid = 0;
   alignas(64) CUtensorMap xmap;  // X as (cc, nx, ny, nz), box (cw, tx + 2, tyh, 1)
 };

@@ -187,7 +187,9 @@ def test_band_sweep_bit_exact(cuda, monkeypatch):
         monkeypatch.setenv("TFG_SWEEP", "0")
         want = P.Plan(prob, s).execute().cpu().numpy()
         monkeypatch.setenv("TFG_SWEEP", "1")
+        monkeypatch.setenv("TFG_STENCIL", "0")  # the stencil kernel takes stencils by default
         plan = P.Plan(prob, s)
+        monkeypatch.setenv("TFG_STENCIL", "1")
         assert plan.launches == 1, name  # both passes in the one sweep kernel
         out = torch.full((w.n, w.c_cols), float("nan"), dtype=getattr(torch, w.dtype.name),
                          device="cuda")

@@ -138,3 +138,19 @@ def test_stencil_nan_poison(cuda, oracle):
     d = plan.execute(out).cpu().numpy()
     assert np.isfinite(d).all()
     assert np.array_equal(d, oracle_d(oracle, a, a, c, np.float64))
+
+
+@pytest.mark.parametrize("knobs", [{"TFG_STENCIL_NW": "8"}, {"TFG_STENCIL_CTAS": "2"},
+                                   {"TFG_STENCIL_CTAS": "4"}, {"TFG_STENCIL_NS": "3"},
+                                   {"TFG_STENCIL_ZC": "5", "TFG_STENCIL_PF": "3"}])
+def test_stencil_tile_configs(cuda, oracle, monkeypatch, knobs):
+    """Every tile / ring / occupancy configuration the plan can pick gives the
+    same bits (partial tiles in x, y and z included)."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    for nx, ny, nz, offs, cc in ((12, 10, 9, BOX3, 128), (70, 1, 33, BOX2, 64)):
+        a = grid_stencil(nx, ny, nz, offs, 13)
+        c = np.random.default_rng(14).uniform(-1, 1, (a.n_rows, cc))
+        d, ks = run_plan(a, a, c, np.float64)
+        assert "stencil" in ks["wave1"], ks
+        assert np.array_equal(d, oracle_d(oracle, a, a, c, np.float64))
