@@ -2928,6 +2928,9 @@ struct tfg_plan {
   // tiles, (c) wavefront-1 SpMM -- each input byte read once, each output
   // byte written once (the roofline numerator)
   int64_t stage_bytes[3] = {0, 0, 0};
+  int64_t d1_read_rows = 0;  // distinct D1 rows wavefront 1 reads
+  // SpMM-SpMM on a 2-D stencil pair: both passes in one kernel, D1 on chip
+  std::unique_ptr<tfg::StencilPlan> stencil2;
 };
 
 namespace tfg {
@@ -3440,9 +3443,28 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       pl.stage_bytes[1] = b;
     }
     if (!second_rows.empty())
-      pl.stage_bytes[2] = csr_rows_bytes(second_rows, arp) +
-                          distinct_cols(second_rows, pr.d_a_row_ptr, pr.d_a_col_idx, n) * cc * el +
+      pl.d1_read_rows = distinct_cols(second_rows, pr.d_a_row_ptr, pr.d_a_col_idx, n);
+      pl.stage_bytes[2] = csr_rows_bytes(second_rows, arp) + pl.d1_read_rows * cc * el +
                           (int64_t)second_rows.size() * cc * el;
+  }
+
+  // D = A (B C) for a 2-D stencil pair with every row in both passes: one
+  // fused kernel keeps D1 in shared memory (tfg_stencil.cu, k_spmm2_stencil)
+  pl.stencil2.reset();
+  if (!pr.b_is_dense && !partial && pl.fo_sparse.stencil && pl.second.stencil) {
+    auto sp = std::make_unique<StencilPlan>();
+    if (stencil2_prepare(*sp, pl.fo_sparse.stencil->g, pl.second.stencil->g, pr.d_c, cc,
+                         (int)pl.elem)) {
+      pl.stencil2 = std::move(sp);
+      // D1 is neither written to nor read from HBM
+      const int64_t el = (int64_t)pl.elem;
+      pl.stage_bytes[0] += pl.stage_bytes[2] - (int64_t)n * cc * el - pl.d1_read_rows * cc * el;
+      pl.stage_bytes[2] = 0;
+      if (getenv("TFG_DEBUG"))
+        fprintf(stderr, "[tfg] fused stencil: tile %d zc %d ns %d per_sm %d items %lld smem %zu\n",
+                pl.stencil2->tx, pl.stencil2->zc, pl.stencil2->ns, pl.stencil2->per_sm,
+                (long long)pl.stencil2->items, pl.stencil2->smem);
+    }
   }
 
   // (a)+(c) as one dependency-driven band sweep: SpMM-SpMM, nothing fused,
@@ -3456,7 +3478,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     const SpmmWork& w0 = pl.fo_sparse;
     const SpmmWork& w1 = pl.second;
     if (sweep_on && !pr.b_is_dense && pl.n_ftiles == 0 && !partial && w0.banded && w1.banded &&
-        !w0.stencil && !w1.stencil &&
+        !w0.stencil && !w1.stencil && !pl.stencil2 &&
         !w0.band_union && !w1.band_union && w0.n_long == 0 && w1.n_long == 0 && w0.row0 == 0 &&
         w1.row0 == 0 && w0.n_short == n && w1.n_short == n) {
       pl.sw_scap = std::max(w0.stage_cap, w1.stage_cap);
@@ -3522,7 +3544,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
 
   pl.launches = 0;
   if (pl.tc.on && (pl.n_fo_blocks > 0 || pl.n_ftiles > 0)) pl.launches += 1;  // C split
-  if (pl.sweep) {
+  if (pl.sweep || pl.stencil2) {
     pl.launches += 1;
   } else {
     if (pr.b_is_dense)
@@ -3618,6 +3640,13 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (part == 1) goto wave1;
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
+  if (pl.stencil2 && part < 0) {  // both passes in one kernel, D1 in shared memory
+    stencil2_run(*pl.stencil2, pr.d_b_row_ptr, pr.d_b_col_idx, pr.d_b_val, pr.d_a_row_ptr,
+                 pr.d_a_col_idx, pr.d_a_val, D, st);
+    for (int e = 1; e <= 3; ++e)
+      if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
+    return;
+  }
   if (pl.sweep && part < 0) {  // both passes in one dependency-driven kernel
     pl.sweep_out = D;
     sweep_launch<T>(pl, st, false);
@@ -3833,7 +3862,9 @@ tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
       return k;
     };
     std::string fo;
-    if (pl->sweep)
+    if (pl->stencil2)
+      fo = "stencil2d-fused";
+    else if (pl->sweep)
       fo = "sweep";
     else if (pl->p.b_is_dense)
       fo = pl->n_fo_blocks == 0 ? "none" : (pl->tc.on ? "tcgen05" : (pl->gemm_kind ? "gemm-v2" : "gemm"));
@@ -3841,7 +3872,7 @@ tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
       fo = spmm_kind(pl->fo_sparse);
     std::string fu = pl->n_ftiles == 0 ? "none"
                      : (pl->fused_v2 ? (pl->tc.on ? "tcgen05-tiles" : "gemm-tiles") : "tiles");
-    std::string w1 = pl->sweep ? "sweep" : spmm_kind(pl->second);
+    std::string w1 = pl->stencil2 ? "stencil2d-fused" : (pl->sweep ? "sweep" : spmm_kind(pl->second));
     const std::string s = "first_op=" + fo + " fused=" + fu + " wave1=" + w1;
     const size_t n = std::min(s.size(), (size_t)len - 1);
     memcpy(buf, s.data(), n);

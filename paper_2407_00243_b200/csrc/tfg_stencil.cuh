@@ -53,6 +53,8 @@ struct StencilPlan {
   int ntx = 0, nty = 0, nzc = 0;
   int64_t items = 0;
   size_t plane_bytes = 0, smem = 0;
+  size_t plane2_bytes = 0;  // fused kernel: D1 plane
+  StencilGeom g2;           // fused kernel: A's stencil (g is B's)
   int per_sm = 1;       // resident CTAs per SM the launch is built for
   int grid = 0;
   alignas(64) CUtensorMap xmap;  // X as (cc, nx, ny, nz), box (cw, tx + 2, tyh, 1)
@@ -69,5 +71,14 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
 void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void* av, void* out,
                  cudaStream_t st);
 int stencil_env_enabled();  // TFG_STENCIL (default 1)
+
+// Fused D = A (B C) for a pair of 2-D stencils on the same grid (gb: B, ga:
+// A), D1 kept on chip (registers).  false: not eligible or not enabled (the
+// plan keeps two stencil passes).  Opt-in: TFG_STENCIL_FUSE=1.
+bool stencil2_prepare(StencilPlan& sp, const StencilGeom& gb, const StencilGeom& ga,
+                      const void* C, int cc, int elem);
+void stencil2_run(const StencilPlan& sp, const int* b_rp, const int* b_ci, const void* b_av,
+                  const int* a_rp, const int* a_ci, const void* a_av, void* out,
+                  cudaStream_t st);
 
 }  // namespace tfg

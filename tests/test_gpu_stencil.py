@@ -60,10 +60,10 @@ def oracle_d(oracle, a, b, c, dt, osched=None):
 
 CASES = [
     # (nx, ny, nz, offsets, c_cols, dtype, expected kernel)
-    (64, 1, 40, BOX2, 64, np.float64, "stencil2d"),      # whole tiles
-    (70, 1, 33, BOX2, 128, np.float64, "stencil2d"),     # partial tile, 2 column slices
-    (37, 1, 29, FIVE, 64, np.float64, "stencil2d"),      # partial lines
-    (64, 1, 21, BOX2, 128, np.float32, "stencil2d"),     # fp32: 128-float slices
+    (64, 1, 40, BOX2, 64, np.float64, "stencil2d"),    # whole tiles
+    (70, 1, 33, BOX2, 128, np.float64, "stencil2d"),   # partial tile, 2 column slices
+    (37, 1, 29, FIVE, 64, np.float64, "stencil2d"),    # partial lines
+    (64, 1, 21, BOX2, 128, np.float32, "stencil2d"),   # fp32: 128-float slices
     (16, 16, 12, BOX3, 64, np.float64, "stencil3d"),
     (12, 10, 9, BOX3, 128, np.float64, "stencil3d"),     # partial tiles in x and y
     (9, 11, 7, SEVEN, 64, np.float64, "stencil3d"),
@@ -154,3 +154,28 @@ def test_stencil_tile_configs(cuda, oracle, monkeypatch, knobs):
         d, ks = run_plan(a, a, c, np.float64)
         assert "stencil" in ks["wave1"], ks
         assert np.array_equal(d, oracle_d(oracle, a, a, c, np.float64))
+
+
+@pytest.mark.parametrize("knobs", [{}, {"TFG_STENCIL2_NW": "8"}, {"TFG_STENCIL2_CTAS": "3"},
+                                   {"TFG_STENCIL2_ZC": "3"}, {"TFG_STENCIL_NS": "3"}])
+def test_fused_stencil_pair(cuda, oracle, monkeypatch, knobs):
+    """The opt-in fused 2-D kernel (D1 in registers, halo recomputed per warp)
+    gives the two-pass bits and the oracle's, for every tile configuration;
+    short grids (fewer planes than a chunk) and ragged tiles included."""
+    monkeypatch.setenv("TFG_STENCIL_FUSE", "1")  # opt-in kernel
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    for nx, nz, offs_a, offs_b, cc in ((70, 33, BOX2, BOX2, 64), (61, 7, BOX2, FIVE, 128),
+                                       (30, 2, FIVE, BOX2, 64), (128, 17, BOX2, BOX2, 64)):
+        a = grid_stencil(nx, 1, nz, offs_a, 15)
+        b = grid_stencil(nx, 1, nz, offs_b, 16)
+        c = np.random.default_rng(17).uniform(-1, 1, (a.n_rows, cc))
+        d, ks = run_plan(a, b, c, np.float64)
+        assert ks["wave1"] == "stencil2d-fused", ks
+        monkeypatch.setenv("TFG_STENCIL_FUSE", "0")
+        d2, ks2 = run_plan(a, b, c, np.float64)
+        monkeypatch.setenv("TFG_STENCIL_FUSE", "1")
+        assert ks2["wave1"] == "stencil2d", ks2
+        want = oracle_d(oracle, a, b, c, np.float64)
+        assert np.array_equal(d, want), (nx, nz, max_rel_err(d, want))
+        assert np.array_equal(d2, want)
