@@ -64,7 +64,7 @@ __device__ __forceinline__ unsigned group_mask(int lpr) {
 // One CSR row times X, LPR lanes per row, each lane NCH x VEC columns.
 // Per-element order = ascending nonzeros, separate mul and add
 // (kernels.hpp:75-79).  XL(c, ch, out[VEC]) loads X row c, chunk ch.
-template <class T, int VEC, int LPR, int NCH, class XL>
+template <class T, int VEC, int LPR, int NCH, class XL, int UNR = 4>
 __device__ __forceinline__ void spmm_row(int kb, int ke,
                                          const int* __restrict__ ci,
                                          const T* __restrict__ av, int gl,
@@ -84,21 +84,21 @@ __device__ __forceinline__ void spmm_row(int kb, int ke,
     }
     const int cnt = min(LPR, ke - k0);
     int u = 0;
-    for (; u + 4 <= cnt; u += 4) {
-      int cu[4];
-      T au[4];
-      T x[4][NCH][VEC];
+    for (; u + UNR <= cnt; u += UNR) {
+      int cu[UNR];
+      T au[UNR];
+      T x[UNR][NCH][VEC];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < UNR; ++q) {
         cu[q] = __shfl_sync(gmask, c, u + q, LPR);
         au[q] = __shfl_sync(gmask, a, u + q, LPR);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < UNR; ++q)
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) xl(cu[q], ch, x[q][ch]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < UNR; ++q)
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll

@@ -1486,7 +1486,7 @@ __global__ void __launch_bounds__(256)
 
 // Vectorised long-row segments: LPR lanes per segment (16-byte gathers),
 // partial rows to scratch, then an ordered combine per long row.
-template <class T, int VEC, int LPR, int NCH>
+template <class T, int VEC, int LPR, int NCH, int UNR = 4>
 __global__ void __launch_bounds__(256)
     k_spmm_segments_vec(int64_t nseg, const int* __restrict__ seg_k0,
                         const int* __restrict__ seg_k1, const int* __restrict__ ci,
@@ -1500,7 +1500,7 @@ __global__ void __launch_bounds__(256)
     ldv<T, VEC>(x, X + (size_t)c * ldx + (ch * LPR + gl) * VEC);
   };
   T acc[NCH][VEC];
-  spmm_row<T, VEC, LPR, NCH>(seg_k0[g], seg_k1[g], ci, av, gl, gmask, xl, acc);
+  spmm_row<T, VEC, LPR, NCH, decltype(xl), UNR>(seg_k0[g], seg_k1[g], ci, av, gl, gmask, xl, acc);
   T* o = partial + (size_t)g * ldx;
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
@@ -2774,7 +2774,16 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
 #undef TFG_RING
   }
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  if (w.skewed && skv == 1)                                                      \
+  if (w.skewed && skv == 3)                                                      \
+    k_spmm_strip<T, VEC, LPR, NCH, 8, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
+  else if (w.skewed && skv == 4 && LPR >= 8)                                     \
+    k_spmm_strip<T, VEC, (LPR >= 8 ? LPR / 2 : LPR), (LPR >= 8 ? NCH * 2 : NCH), 4, 4, 1> \
+        <<<blocks_for(n * (LPR / 2)), 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
+  else if (w.skewed && skv == 5 && LPR >= 8)                                     \
+    k_spmm_strip<T, VEC, (LPR >= 8 ? LPR / 2 : LPR), (LPR >= 8 ? NCH * 2 : NCH), 8, 4, 1> \
+        <<<blocks_for(n * (LPR / 2)), 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
+  else if (w.skewed && skv == 1)                                                 \
     k_spmm_strip<T, VEC, LPR, NCH, 8, 3, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
         n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
   else if (w.skewed && skv == 2)                                                 \
@@ -2848,11 +2857,22 @@ static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
   if (w.n_long) {
     T* partial = reinterpret_cast<T*>(w.partial.p);
     constexpr int VEC = 16 / sizeof(T);
+    static const int seg_unr = [] {  // gathers in flight per lane group
+      const char* e = getenv("TFG_SEG_UNR");
+      return e ? atoi(e) : 8;  // 8: cfg5 wavefront 1 10.3 -> 9.1 ms (vs 4)
+    }();
     const int L = cc % VEC == 0 ? cc / VEC : 0;
 #define TFG_SEG(LPR, NCH)                                                                     \
   {                                                                                           \
-    k_spmm_segments_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(         \
-        w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                             \
+    if (seg_unr == 16)                                                                        \
+      k_spmm_segments_vec<T, VEC, LPR, NCH, 16><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(   \
+          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
+    else if (seg_unr == 8)                                                                    \
+      k_spmm_segments_vec<T, VEC, LPR, NCH, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(    \
+          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
+    else                                                                                      \
+      k_spmm_segments_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(       \
+          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
     TFG_LAUNCH_CHECK();                                                                       \
     k_segment_combine_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_long * LPR), 256, 0, st>>>(      \
         w.n_long, w.long_rows.p, w.long_seg_off.p, partial, cc, out, cc);                     \
