@@ -3045,13 +3045,18 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
 static void attach_stencil(SpmmWork& w, int64_t n, const std::vector<int>& rp,
                            const std::vector<int>& ci, const void* X, int cc, size_t elem) {
   w.stencil.reset();
-  if (!stencil_env_enabled() || ci.empty() || !w.identity || w.row0 != 0 || w.n_short != n ||
-      w.n_long != 0 || n > INT32_MAX)
+  if (!stencil_env_enabled() || ci.empty() || !w.identity || w.n_short == 0 || w.n_long != 0 ||
+      n > INT32_MAX)
     return;
   StencilGeom g;
   if (!stencil_detect((int)n, rp, ci, g)) return;
+  // the rows must be whole grid planes (a partition's slab of z)
+  const int64_t nxy = (int64_t)g.nx * g.ny;
+  if (w.row0 % nxy != 0 || w.n_short % nxy != 0) return;
   auto sp = std::make_unique<StencilPlan>();
-  if (!stencil_prepare(*sp, g, X, cc, (int)elem)) return;
+  if (!stencil_prepare(*sp, g, X, cc, (int)elem, (int)(w.row0 / nxy),
+                       (int)((w.row0 + w.n_short) / nxy)))
+    return;
   if (getenv("TFG_DEBUG"))
     fprintf(stderr,
             "[tfg] stencil spmm: grid %d x %d x %d K=%d tile %d x %d zc %d ns %d slices %d "

@@ -33,6 +33,7 @@ struct OpArgs {
 
 struct StencilArgs {
   int n, nx, ny, nz, nxy;
+  int zb, ze;  // planes [zb, ze) are computed (a row-block partition)
   int zc, ns, slices, ntx, nty, cc;
   long long items;
   int plane_elems;
@@ -296,8 +297,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
           pit += gridDim.x;
           pc1 = itx * TL::TX - 1;
           pc2 = D3 ? ity * TL::TY - 1 : 0;
-          pz = izc * a.zc - 1;
-          pz1 = min(izc * a.zc + a.zc, a.nz);
+          pz = a.zb + izc * a.zc - 1;
+          pz1 = min(a.zb + izc * a.zc + a.zc, a.ze);
         }
         tma_prefetch_4d(&xmap, pcs * CW, pc1, pc2, pz);
         ++pz;
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
         int cs, itx, ity, izc;
         decode_item(a, it, cs, itx, ity, izc);
-        const int z0 = izc * a.zc, z1 = min(z0 + a.zc, a.nz);
+        const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
         const int c1 = itx * TL::TX - 1;
         const int c2 = D3 ? ity * TL::TY - 1 : 0;
         for (int p = z0 - 1; p <= z1; ++p, ++g) {
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
     int cs, itx, ity, izc;
     decode_item(a, it, cs, itx, ity, izc);
-    const int z0 = izc * a.zc, z1 = min(z0 + a.zc, a.nz);
+    const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
     const int nzl = z1 - z0;
     const int x = itx * TL::TX + wx * M;
     const int y = D3 ? ity * TL::TY + wy : 0;
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
         int cs, itx, ity, izc;
         decode_item(a, it, cs, itx, ity, izc);
-        const int z0 = izc * a.zc, z1 = min(z0 + a.zc, a.nz);
+        const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
         for (int p = z0 - 2; p <= z1 + 1; ++p, ++g) {
           const int s = (int)(g % ns);
           const uint32_t k = g / ns;
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
     int cs, itx, ity, izc;
     decode_item(a, it, cs, itx, ity, izc);
-    const int z0 = izc * a.zc, z1 = min(z0 + a.zc, a.nz);
+    const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
     const int nzl = z1 - z0;
     const int xB = itx * TX + warp * M;  // D point 0 of this warp
     const int xA = xB - 1;               // D1 point 0
@@ -770,8 +771,14 @@ bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& c
   return false;
 }
 
-bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int cc, int elem) {
+bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int cc, int elem,
+                     int zb, int ze) {
   sp.on = false;
+  if (ze < 0) ze = g.nz;
+  if (zb < 0 || ze > g.nz || zb >= ze) return false;
+  sp.zb = zb;
+  sp.ze = ze;
+  const int nzr = ze - zb;
   if (!stencil_env_enabled() || g.nx == 0) return false;
   if ((size_t)cc * elem % kSliceBytes != 0 || (uintptr_t)X % 16 != 0) return false;
   auto enc = encode_tiled();
@@ -822,11 +829,11 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   // halo planes)
   const int64_t tiles = (int64_t)sp.ntx * sp.nty * sp.slices;
   const int zc_env = env_int("TFG_STENCIL_ZC", 0);
-  int best = g.nz;
+  int best = nzr;
   double best_cost = 1e300;
   // short chunks measured best on cfg2 (16 planes: 0.239 ms vs 0.26 at 24-28)
-  for (int zc = std::min(8, g.nz); zc <= std::min(16, std::max(1, g.nz)); ++zc) {
-    const int64_t nzc = (g.nz + zc - 1) / zc;
+  for (int zc = std::min(8, nzr); zc <= std::min(16, std::max(1, nzr)); ++zc) {
+    const int64_t nzc = (nzr + zc - 1) / zc;
     const int64_t items = tiles * nzc;
     const double waves = (double)((items + sp.grid - 1) / sp.grid);
     const double cost = waves * (zc + 2);
@@ -836,7 +843,7 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
     }
   }
   sp.zc = zc_env > 0 ? zc_env : best;
-  sp.nzc = (g.nz + sp.zc - 1) / sp.zc;
+  sp.nzc = (nzr + sp.zc - 1) / sp.zc;
   sp.items = tiles * sp.nzc;
   sp.grid = (int)std::min<int64_t>(sp.grid, sp.items);
   cuuint64_t dims[4] = {(cuuint64_t)cc, (cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
@@ -897,6 +904,8 @@ void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void
   a.ny = g.ny;
   a.nz = g.nz;
   a.nxy = g.nx * g.ny;
+  a.zb = sp.zb;
+  a.ze = sp.ze;
 
   a.zc = sp.zc;
   a.ns = sp.ns;
@@ -1031,6 +1040,8 @@ void stencil2_run(const StencilPlan& sp, const int* b_rp, const int* b_ci, const
   a.ny = 1;
   a.nz = g.nz;
   a.nxy = g.nx;
+  a.zb = 0;
+  a.ze = g.nz;
   a.zc = sp.zc;
   a.ns = sp.ns;
   a.slices = sp.slices;

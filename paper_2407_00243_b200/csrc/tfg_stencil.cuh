@@ -46,6 +46,7 @@ struct StencilPlan {
   int tx = 0, ty = 1;   // tile of the (x, y) plane, points
   int tyh = 1;          // tile rows incl. halo along y (ty + 2, or 1 in 2-D)
   int zc = 0;           // z planes (outputs) per work item
+  int zb = 0, ze = 0;   // planes computed (row-block partitions: a slab)
   int ns = 3;           // shared-memory plane ring depth
   int pf = 4;           // L2 prefetch distance (planes ahead of the ring loads)
   int cw = 0;           // column slice per CTA (elements, 512 bytes)
@@ -66,7 +67,9 @@ bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& c
                     StencilGeom& g);
 // Tile the grid for X (n x cc row-major, element size elem bytes) and encode
 // the X tensor map.  false: shape not supported (the plan keeps its SpMM).
-bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int cc, int elem);
+// Planes [zb, ze) only (a row-block partition; -1: the whole grid).
+bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int cc, int elem,
+                     int zb = 0, int ze = -1);
 // out[r, :] = sum_k av[k] * X[ci[k], :] over every row r of the matrix.
 void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void* av, void* out,
                  cudaStream_t st);

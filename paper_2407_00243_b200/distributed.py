@@ -157,6 +157,14 @@ class GpuEngine:
         self._lib, self._check, self._sp = lib, check, _stream_ptr
         self._code = 1 if problem.dtype == np.float64 else 0
 
+    def kernels(self) -> dict:
+        """Kernel chosen for each stage of this rank's plan (tfg_plan_kernels)."""
+        import ctypes as C
+
+        buf = C.create_string_buffer(256)
+        self._check(self._lib().tfg_plan_kernels(self._h, buf, 256))
+        return dict(kv.split("=", 1) for kv in buf.value.decode().split())
+
     def _stream(self):
         import torch
 
