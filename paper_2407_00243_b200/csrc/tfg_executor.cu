@@ -1486,8 +1486,8 @@ __global__ void __launch_bounds__(256)
 
 // Vectorised long-row segments: LPR lanes per segment (16-byte gathers),
 // partial rows to scratch, then an ordered combine per long row.
-template <class T, int VEC, int LPR, int NCH, int UNR = 4>
-__global__ void __launch_bounds__(256)
+template <class T, int VEC, int LPR, int NCH, int UNR = 4, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
     k_spmm_segments_vec(int64_t nseg, const int* __restrict__ seg_k0,
                         const int* __restrict__ seg_k1, const int* __restrict__ ci,
                         const T* __restrict__ av, const T* __restrict__ X, int ldx,
@@ -2774,7 +2774,10 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
 #undef TFG_RING
   }
 #define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  if (w.skewed && skv == 3)                                                      \
+  if (w.skewed && skv == 6)                                                      \
+    k_spmm_strip<T, VEC, LPR, NCH, 4, 8, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
+  else if (w.skewed && skv == 3)                                                 \
     k_spmm_strip<T, VEC, LPR, NCH, 8, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
         n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
   else if (w.skewed && skv == 4 && LPR >= 8)                                     \
@@ -2789,8 +2792,11 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
   else if (w.skewed && skv == 2)                                                 \
     k_spmm_strip<T, VEC, LPR, NCH, 8, 2, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
         n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else if (w.skewed)                                                             \
+  else if (w.skewed && skv == 8)                                                 \
     k_spmm_strip<T, VEC, LPR, NCH, 4, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
+  else if (w.skewed) /* 2 gathers in flight, full occupancy: cfg3 1.02 -> 0.76 ms */ \
+    k_spmm_strip<T, VEC, LPR, NCH, 2, 8, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
         n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
   else                                                                           \
     k_spmm_strip<T, VEC, LPR, NCH, 4, 4><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
@@ -2864,7 +2870,16 @@ static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
     const int L = cc % VEC == 0 ? cc / VEC : 0;
 #define TFG_SEG(LPR, NCH)                                                                     \
   {                                                                                           \
-    if (seg_unr == 16)                                                                        \
+    if (seg_unr == 2)                                                                         \
+      k_spmm_segments_vec<T, VEC, LPR, NCH, 2, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
+          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
+    else if (seg_unr == 3)                                                                    \
+      k_spmm_segments_vec<T, VEC, LPR, NCH, 4, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
+          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
+    else if (seg_unr == 5)                                                                    \
+      k_spmm_segments_vec<T, VEC, LPR, NCH, 8, 4><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
+          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
+    else if (seg_unr == 16)                                                                   \
       k_spmm_segments_vec<T, VEC, LPR, NCH, 16><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(   \
           w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
     else if (seg_unr == 8)                                                                    \
