@@ -220,12 +220,18 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
     }
     const unsigned irr = valid & ~reg;
     if (irr) {  // grid-face rows: their own CSR order, neighbours from the planes
+      // the rows' column indices, lane-parallel and all issued up front
+      // (one memory round trip for the group, not one per nonzero)
+      int cl[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        cl[m] = ((irr >> m) & 1u) && vb[m] + lane < vb[m + 1] ? __ldg(op.ci + vb[m] + lane) : 0;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         if (!((irr >> m) & 1u)) continue;
         const int r = rbase + m;
-        for (int k = vb[m]; k < vb[m + 1]; ++k) {
-          int o = __ldg(op.ci + k) - r;
+        for (int k = vb[m]; k < vb[m + 1]; ++k) {  // <= 27 nonzeros: one lane each
+          int o = __shfl_sync(0xffffffffu, cl[m], k - vb[m]) - r;
           int dz = 0, dy = 0;
           if (D3) {
             dz = o > a.nxy / 2 ? 1 : (o < -(a.nxy / 2) ? -1 : 0);
