@@ -3,7 +3,8 @@ from an ncu report of `bench.py --quick` and record it for bench.py's
 roofline.traffic field.
 
 usage: python tools/traffic.py <report.ncu-rep> <config> <stage>...
-  stages are matched to the captured launches in order (e.g. first_op wave1_spmm)
+  stages are matched to the captured launches in order (e.g. first_op wave1_spmm);
+  "name:N" sums N consecutive launches into one stage, "-" skips a launch
 writes/updates profiles/ncu_traffic.json: {config: {stage: {kernel, bytes, ...}}}
 """
 import json
@@ -27,12 +28,25 @@ def main():
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     d = data.setdefault(cfg, {})
-    for stage, r in zip(stages, rows):
-        rd = to_bytes(r["dram__bytes_read.sum"], r.get("dram__bytes_read.sum.unit", "byte"))
-        wr = to_bytes(r["dram__bytes_write.sum"], r.get("dram__bytes_write.sum.unit", "byte"))
-        d[stage] = {"kernel": r["kernel"][:120], "dram_bytes": rd + wr, "dram_read": rd,
-                    "dram_write": wr, "ncu_time_us": r["gpu__time_duration.sum"],
-                    "source": os.path.basename(rep)}
+    # a stage may span several launches: "wave1_spmm:3" sums the next three;
+    # "-" skips a launch (e.g. a small prep kernel)
+    k = 0
+    for spec in stages:
+        name, _, cnt = spec.partition(":")
+        cnt = int(cnt or 1)
+        group = rows[k:k + cnt]
+        k += cnt
+        if name == "-":
+            continue
+        rd = sum(to_bytes(r["dram__bytes_read.sum"], r.get("dram__bytes_read.sum.unit", "byte"))
+                 for r in group)
+        wr = sum(to_bytes(r["dram__bytes_write.sum"], r.get("dram__bytes_write.sum.unit", "byte"))
+                 for r in group)
+        tus = sum(float(r["gpu__time_duration.sum"]) * (1e3 if r.get("gpu__time_duration.sum.unit") == "ms" else 1.0)
+                  for r in group)
+        d[name] = {"kernel": " + ".join(r["kernel"][:60] for r in group), "dram_bytes": rd + wr,
+                   "dram_read": rd, "dram_write": wr, "ncu_time_us": tus, "launches": cnt,
+                   "source": os.path.basename(rep)}
     json.dump(data, open(path, "w"), indent=1)
     print(json.dumps(d, indent=1))
 
