@@ -2966,6 +2966,8 @@ struct tfg_plan {
   int64_t d1_read_rows = 0;  // distinct D1 rows wavefront 1 reads
   // SpMM-SpMM on a 2-D stencil pair: both passes in one kernel, D1 on chip
   std::unique_ptr<tfg::StencilPlan> stencil2;
+  // SpMM-SpMM on a stencil pair: both passes in one dependency-driven sweep
+  std::unique_ptr<tfg::StencilSweep> stencil_sweep;
 };
 
 namespace tfg {
@@ -3518,6 +3520,17 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                 (long long)pl.stencil2->items, pl.stencil2->smem);
     }
   }
+  pl.stencil_sweep.reset();
+  if (!pl.stencil2 && !pr.b_is_dense && !partial && pl.fo_sparse.stencil && pl.second.stencil) {
+    auto sw = std::make_unique<StencilSweep>();
+    if (stencil_sweep_prepare(*sw, *pl.fo_sparse.stencil, *pl.second.stencil)) {
+      pl.stencil_sweep = std::move(sw);
+      // D1 is still written once; wavefront 1 reads it back from L2
+      const int64_t el = (int64_t)pl.elem;
+      pl.stage_bytes[0] += pl.stage_bytes[2] - pl.d1_read_rows * cc * el;
+      pl.stage_bytes[2] = 0;
+    }
+  }
 
   // (a)+(c) as one dependency-driven band sweep: SpMM-SpMM, nothing fused,
   // both passes band-staged over all rows
@@ -3596,7 +3609,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
 
   pl.launches = 0;
   if (pl.tc.on && (pl.n_fo_blocks > 0 || pl.n_ftiles > 0)) pl.launches += 1;  // C split
-  if (pl.sweep || pl.stencil2) {
+  if (pl.sweep || pl.stencil2 || pl.stencil_sweep) {
     pl.launches += 1;
   } else {
     if (pr.b_is_dense)
@@ -3702,6 +3715,14 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (pl.stencil2 && part < 0) {  // both passes in one kernel, D1 in shared memory
     stencil2_run(*pl.stencil2, pr.d_b_row_ptr, pr.d_b_col_idx, pr.d_b_val, pr.d_a_row_ptr,
                  pr.d_a_col_idx, pr.d_a_val, D, st);
+    for (int e = 1; e <= 3; ++e)
+      if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
+    return;
+  }
+  if (pl.stencil_sweep && part < 0) {  // both stencil passes, one dependency-driven kernel
+    stencil_sweep_run(*pl.stencil_sweep, *pl.fo_sparse.stencil, *pl.second.stencil,
+                      pr.d_b_row_ptr, pr.d_b_col_idx, pr.d_b_val, pr.d_a_row_ptr, pr.d_a_col_idx,
+                      pr.d_a_val, pl.d1.p, D, st);
     for (int e = 1; e <= 3; ++e)
       if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
     return;
@@ -3923,6 +3944,8 @@ tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
     std::string fo;
     if (pl->stencil2)
       fo = "stencil2d-fused";
+    else if (pl->stencil_sweep)
+      fo = "stencil-sweep";
     else if (pl->sweep)
       fo = "sweep";
     else if (pl->p.b_is_dense)
@@ -3931,7 +3954,9 @@ tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
       fo = spmm_kind(pl->fo_sparse);
     std::string fu = pl->n_ftiles == 0 ? "none"
                      : (pl->fused_v2 ? (pl->tc.on ? "tcgen05-tiles" : "gemm-tiles") : "tiles");
-    std::string w1 = pl->stencil2 ? "stencil2d-fused" : (pl->sweep ? "sweep" : spmm_kind(pl->second));
+    std::string w1 = pl->stencil2        ? "stencil2d-fused"
+                     : pl->stencil_sweep ? "stencil-sweep"
+                     : (pl->sweep ? "sweep" : spmm_kind(pl->second));
     const std::string s = "first_op=" + fo + " fused=" + fu + " wave1=" + w1;
     const size_t n = std::min(s.size(), (size_t)len - 1);
     memcpy(buf, s.data(), n);

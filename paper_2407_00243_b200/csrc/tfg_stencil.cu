@@ -38,9 +38,13 @@ struct StencilArgs {
   long long items;
   int plane_elems;
   int plane2_elems;  // fused kernel: D1 plane (the ring planes hold C)
-  int pf;            // L2 prefetch distance (planes)
   OpArgs op[2];      // [0]: the single SpMM (or B of the fused chain), [1]: A of the chain
   void* out;
+  void* out1;               // sweep: D (out = D1)
+  const int* sweep_items;   // sweep: op << 30 | item of op, in launch order
+  int* sweep_done;          // sweep: first-op items finished per z chunk (cumulative)
+  int sweep_target;         // sweep: counter value of a complete chunk this launch
+  int nzc;                  // z chunks per tile
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
@@ -71,15 +75,6 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(s_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
-                                                int c3) {
-  asm volatile(
-      "cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
-          reinterpret_cast<uint64_t>(map)),
-      "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 
@@ -268,9 +263,39 @@ __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArg
     if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * ostride, acc[m]);
 }
 
-template <class T, bool D3, int NW, int M, int MINB>
+__device__ __forceinline__ int ld_relaxed_gpu_s(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Work item `it` of the launch: in a sweep, items[it] = op << 30 | item of op
+// (op 0: first op X = C -> D1, op 1: second op X = D1 -> D); otherwise op 0.
+template <bool SWEEP>
+__device__ __forceinline__ void item_of(const StencilArgs& a, long long it, int& op,
+                                        long long& sub) {
+  if constexpr (SWEEP) {
+    const int code = __ldg(a.sweep_items + it);
+    op = code >> 30;
+    sub = code & ((1 << 30) - 1);
+  } else {
+    op = 0;
+    sub = it;
+  }
+}
+
+// SWEEP: both SpMM passes of D = A (B C) as one persistent kernel over an
+// item list in which every second-op item follows the first-op z-chunks it
+// reads (its own and both neighbours) by a lag of a few chunk rows, so the
+// D1 planes it loads are still in L2.  A CTA publishes a finished first-op
+// item with a per-chunk counter (barrier of its compute warps, gpu-scope
+// fence, atomic add); the producer of a second-op item waits for the
+// counters of its chunks before its TMA copies of D1.  Same rows, same
+// order, same bits as two launches.
+template <class T, bool D3, int NW, int M, int MINB, bool SWEEP = false>
 __global__ void __launch_bounds__((NW + 1) * 32, MINB)
-    k_spmm_stencil(const __grid_constant__ CUtensorMap xmap, const StencilArgs a) {
+    k_spmm_stencil(const __grid_constant__ CUtensorMap xmap,
+                   const __grid_constant__ CUtensorMap xmap1, const StencilArgs a) {
   using TL = Tile<D3, NW, M>;
   constexpr int CW = (int)(kSliceBytes / sizeof(T));
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -290,40 +315,32 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   if (warp == NW) {
     // ---------------- producer: one 4-D TMA copy per tile plane ----------------
     if (lane == 0) {
-      // L2 prefetch runs a.pf planes ahead of the loads along this CTA's
-      // plane sequence (across item boundaries), so a ring slot's TMA load
-      // finds its plane in L2 instead of paying the HBM latency
-      long long pit = blockIdx.x;
-      int pcs = 0, pc1 = 0, pc2 = 0, pz = 0, pz1 = -1;
-      auto pf_next = [&]() {
-        while (pz > pz1) {
-          if (pit >= a.items) return;
-          int itx, ity, izc;
-          decode_item(a, pit, pcs, itx, ity, izc);
-          pit += gridDim.x;
-          pc1 = itx * TL::TX - 1;
-          pc2 = D3 ? ity * TL::TY - 1 : 0;
-          pz = a.zb + izc * a.zc - 1;
-          pz1 = min(a.zb + izc * a.zc + a.zc, a.ze);
-        }
-        tma_prefetch_4d(&xmap, pcs * CW, pc1, pc2, pz);
-        ++pz;
-      };
-      for (int k = 0; k < a.pf; ++k) pf_next();
       uint32_t g = 0;
       for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
+        int op;
+        long long sub;
+        item_of<SWEEP>(a, it, op, sub);
         int cs, itx, ity, izc;
-        decode_item(a, it, cs, itx, ity, izc);
+        decode_item(a, sub, cs, itx, ity, izc);
         const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
         const int c1 = itx * TL::TX - 1;
         const int c2 = D3 ? ity * TL::TY - 1 : 0;
+        if constexpr (SWEEP) {
+          if (op == 1) {  // D1 planes of chunks izc - 1 .. izc + 1 must be published
+            const int clo = max(izc - 1, 0), chi = min(izc + 1, a.nzc - 1);
+            for (int ch = clo; ch <= chi; ++ch)
+              while (ld_relaxed_gpu_s(a.sweep_done + ch) < a.sweep_target) __nanosleep(128);
+            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          }
+        }
+        const CUtensorMap* map = (SWEEP && op) ? &xmap1 : &xmap;
         for (int p = z0 - 1; p <= z1; ++p, ++g) {
-          if (a.pf) pf_next();
           const int s = (int)(g % ns);
           const uint32_t k = g / ns;
           if (k > 0) s_bar_wait(&empty[s], (k - 1) & 1u);
           s_bar_expect(&full[s], plane_bytes);
-          tma_4d(planes + (size_t)s * a.plane_elems, &xmap, cs * CW, c1, c2, p, &full[s]);
+          tma_4d(planes + (size_t)s * a.plane_elems, map, cs * CW, c1, c2, p, &full[s]);
         }
       }
     }
@@ -336,7 +353,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   // a global load.
   constexpr int VR = (M * (D3 ? 27 : 9) + 31) / 32;  // value elements per lane and plane
   constexpr int VS = VR * 32;                         // value slot (elements)
-  const T* __restrict__ av = static_cast<const T*>(a.op[0].av);
   T* svb = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * 3 * VS;
   int* srp = reinterpret_cast<int*>(reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) +
                                     (size_t)NW * 3 * VS) + warp * 8 * 16;
@@ -344,8 +360,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   int s0 = 0;        // ring slot of the current item's plane z-1
   uint32_t p0 = 0;   // its full-barrier phase parity
   for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
+    int op;
+    long long sub;
+    item_of<SWEEP>(a, it, op, sub);
+    const OpArgs& opa = a.op[op];
+    const T* __restrict__ av = static_cast<const T*>(opa.av);
+    T* const outb = static_cast<T*>(op ? a.out1 : a.out);
     int cs, itx, ity, izc;
-    decode_item(a, it, cs, itx, ity, izc);
+    decode_item(a, sub, cs, itx, ity, izc);
     const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
     const int nzl = z1 - z0;
     const int x = itx * TL::TX + wx * M;
@@ -358,7 +380,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       if (yvalid && x + m < a.nx) valid |= 1u << m;
     const int r0 = (z0 * a.ny + y) * a.nx + x;  // point 0 at output plane z0
     auto issue_rp = [&](int jj) {
-      if (live && jj < nzl) cp_async_ca<4>(srp + (jj & 7) * 16 + lane, a.op[0].rp + min(r0 + jj * a.nxy + lane, a.n));
+      if (live && jj < nzl) cp_async_ca<4>(srp + (jj & 7) * 16 + lane, opa.rp + min(r0 + jj * a.nxy + lane, a.n));
     };
     const bool wlive = yvalid && x < a.nx;  // warp-uniform: the warp has points
     auto issue_vals = [&](int jj) {  // row pointers of plane jj must be visible
@@ -403,9 +425,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       s_bar_wait(&full[s2], p2);
       const int rb = r0 + j * a.nxy;
       stencil_points<T, D3, M, TL::ROW>(
-          a, a.op[0], planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
+          a, opa, planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
           planes + (size_t)s2 * a.plane_elems, svb + (j % 3) * VS, rp_j, valid, wy, wx * M, rb,
-          static_cast<T*>(a.out) + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
+          outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
           a.cc, lane);
       __syncwarp();
       if (lane == 0) {
@@ -425,6 +447,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       }
     }
     cp_async_wait<0>();
+    if constexpr (SWEEP) {
+      if (op == 0) {  // publish: this item's D1 rows are visible at gpu scope
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(a.sweep_done + izc, 1);
+        }
+      }
+    }
   }
 }
 
@@ -827,7 +858,6 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   const int ns_env = env_int("TFG_STENCIL_NS", 0);
   if (ns_env >= 3) ns = std::min(ns, ns_env);
   sp.ns = ns;
-  sp.pf = std::max(0, env_int("TFG_STENCIL_PF", 0));  // L2 prefetch measured no gain
   sp.smem = ns * sp.plane_bytes + vbytes;
   sp.per_sm = per_sm;
   sp.grid = sm_count() * per_sm;
@@ -870,7 +900,7 @@ template <class T, bool D3, int NW, int MINB>
 static void stencil_launch(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
   auto kern = k_spmm_stencil<T, D3, NW, 4, MINB>;
   TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
-  kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, a);
+  kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, sp.xmap, a);
   TFG_LAUNCH_CHECK();
 }
 
@@ -920,10 +950,10 @@ void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void
   a.nty = sp.nty;
   a.cc = sp.cc;
   a.items = sp.items;
+  a.nzc = sp.nzc;
   a.plane_elems = (int)(sp.plane_bytes / sp.elem);
   a.op[0].K = g.K;
   a.op[0].full = g.K == (g.d3 ? 27 : 9);
-  a.pf = sp.pf;
   memcpy(a.op[0].rank, g.rank, sizeof(g.rank));
   a.op[0].rp = rp;
   a.op[0].ci = ci;
@@ -974,7 +1004,6 @@ bool stencil2_prepare(StencilPlan& sp, const StencilGeom& gb, const StencilGeom&
   const int ns_env = env_int("TFG_STENCIL_NS", 0);
   if (ns_env >= 3) ns = std::min(ns, ns_env);
   sp.ns = ns;
-  sp.pf = 0;
   sp.smem = ns * sp.plane_bytes + fixed;
   sp.per_sm = per_sm;
   sp.grid = sm_count() * per_sm;
@@ -1057,7 +1086,6 @@ void stencil2_run(const StencilPlan& sp, const int* b_rp, const int* b_ci, const
   a.items = sp.items;
   a.plane_elems = (int)(sp.plane_bytes / sp.elem);
   a.plane2_elems = (int)(sp.plane2_bytes / sp.elem);
-  a.pf = 0;
   fill_op(a.op[0], sp.g, b_rp, b_ci, b_av);
   fill_op(a.op[1], sp.g2, a_rp, a_ci, a_av);
   a.out = out;
@@ -1065,6 +1093,121 @@ void stencil2_run(const StencilPlan& sp, const int* b_rp, const int* b_ci, const
     stencil2_launch_t<double>(sp, a, st);
   else
     stencil2_launch_t<float>(sp, a, st);
+}
+
+// ---- both passes as one dependency-driven sweep (k_spmm_stencil<..., true>) ----
+bool stencil_sweep_prepare(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1) {
+  sw.on = false;
+  // opt-in: on cfg2 0.42 ms per step at a lag of 16-24 chunk rows, equal to
+  // two passes; shorter lags stall on the dependencies (lag 3: 0.77 ms) and
+  // longer ones let D1 fall out of L2 before it is read
+  if (env_int("TFG_STENCIL_SWEEP", 0) == 0 || !p0.on || !p1.on) return false;
+  const StencilGeom &g0 = p0.g, &g1 = p1.g;
+  if (g0.nx != g1.nx || g0.ny != g1.ny || g0.nz != g1.nz || g0.d3 != g1.d3) return false;
+  if (p0.zb != 0 || p0.ze != g0.nz || p1.zb != 0 || p1.ze != g1.nz) return false;
+  if (p0.nw != p1.nw || p0.M != p1.M || p0.tx != p1.tx || p0.ty != p1.ty || p0.zc != p1.zc ||
+      p0.ns != p1.ns || p0.slices != p1.slices || p0.smem != p1.smem || p0.elem != p1.elem)
+    return false;
+  const int64_t ipc = (int64_t)p0.ntx * p0.nty * p0.slices;  // items per z chunk
+  const int nzc = p0.nzc;
+  const int lag = std::max(1, env_int("TFG_STENCIL_SWEEP_LAG", 16));
+  std::vector<int> items;
+  items.reserve((size_t)(2 * ipc * nzc));
+  for (int c = 0; c < nzc + lag; ++c) {
+    if (c < nzc)
+      for (int64_t q = 0; q < ipc; ++q) items.push_back((int)(c * ipc + q));
+    if (c - lag >= 0)
+      for (int64_t q = 0; q < ipc; ++q) items.push_back((int)((1 << 30) | ((c - lag) * ipc + q)));
+  }
+  if ((int64_t)items.size() >= (1 << 30)) return false;
+  sw.items.alloc(items.size());
+  h2d(sw.items.p, items.data(), items.size(), 0);
+  sw.done.alloc(nzc);
+  TFG_CUDA(cudaMemset(sw.done.p, 0, sw.done.bytes()));
+  TFG_CUDA(cudaDeviceSynchronize());
+  sw.nitems = (int64_t)items.size();
+  sw.ipc = ipc;
+  sw.epoch = 0;
+  sw.on = true;
+  return true;
+}
+
+template <class T, bool D3, int NW, int MINB>
+static void sweep_launch_k(const StencilPlan& sp, const StencilPlan& sp1, const StencilArgs& a,
+                           cudaStream_t st) {
+  auto kern = k_spmm_stencil<T, D3, NW, 4, MINB, true>;
+  TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
+  int occ = 0;
+  TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NW + 1) * 32, sp.smem));
+  // every CTA must be resident: items wait on earlier items of other CTAs
+  const int grid = (int)std::min<int64_t>(a.items, (int64_t)sm_count() * std::max(occ, 1));
+  kern<<<grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, sp1.xmap, a);
+  TFG_LAUNCH_CHECK();
+}
+
+template <class T, bool D3>
+static void sweep_launch_d(const StencilPlan& sp, const StencilPlan& sp1, const StencilArgs& a,
+                           cudaStream_t st) {
+  const int r = sp.per_sm;
+  if (sp.nw == 8) {
+    if (r >= 2)
+      sweep_launch_k<T, D3, 8, 2>(sp, sp1, a, st);
+    else
+      sweep_launch_k<T, D3, 8, 1>(sp, sp1, a, st);
+  } else {
+    if (r >= 4)
+      sweep_launch_k<T, D3, 4, 4>(sp, sp1, a, st);
+    else if (r == 3)
+      sweep_launch_k<T, D3, 4, 3>(sp, sp1, a, st);
+    else
+      sweep_launch_k<T, D3, 4, 2>(sp, sp1, a, st);
+  }
+}
+
+void stencil_sweep_run(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1,
+                       const int* b_rp, const int* b_ci, const void* b_av, const int* a_rp,
+                       const int* a_ci, const void* a_av, void* d1, void* out, cudaStream_t st) {
+  ++sw.epoch;
+  if ((int64_t)(sw.epoch + 1) * sw.ipc > (int64_t)INT32_MAX) {  // counters restart
+    TFG_CUDA(cudaMemsetAsync(sw.done.p, 0, sw.done.bytes(), st));
+    sw.epoch = 1;
+  }
+  StencilArgs a{};
+  const StencilGeom& g = p0.g;
+  a.n = g.nx * g.ny * g.nz;
+  a.nx = g.nx;
+  a.ny = g.ny;
+  a.nz = g.nz;
+  a.nxy = g.nx * g.ny;
+  a.zb = 0;
+  a.ze = g.nz;
+  a.zc = p0.zc;
+  a.ns = p0.ns;
+  a.slices = p0.slices;
+  a.ntx = p0.ntx;
+  a.nty = p0.nty;
+  a.cc = p0.cc;
+  a.items = sw.nitems;
+  a.nzc = p0.nzc;
+  a.plane_elems = (int)(p0.plane_bytes / p0.elem);
+  fill_op(a.op[0], p0.g, b_rp, b_ci, b_av);
+  fill_op(a.op[1], p1.g, a_rp, a_ci, a_av);
+  a.out = d1;
+  a.out1 = out;
+  a.sweep_items = sw.items.p;
+  a.sweep_done = sw.done.p;
+  a.sweep_target = (int)(sw.epoch * sw.ipc);
+  if (p0.elem == 8) {
+    if (g.d3)
+      sweep_launch_d<double, true>(p0, p1, a, st);
+    else
+      sweep_launch_d<double, false>(p0, p1, a, st);
+  } else {
+    if (g.d3)
+      sweep_launch_d<float, true>(p0, p1, a, st);
+    else
+      sweep_launch_d<float, false>(p0, p1, a, st);
+  }
 }
 
 }  // namespace tfg

@@ -48,7 +48,6 @@ struct StencilPlan {
   int zc = 0;           // z planes (outputs) per work item
   int zb = 0, ze = 0;   // planes computed (row-block partitions: a slab)
   int ns = 3;           // shared-memory plane ring depth
-  int pf = 4;           // L2 prefetch distance (planes ahead of the ring loads)
   int cw = 0;           // column slice per CTA (elements, 512 bytes)
   int slices = 0;       // cc / cw
   int ntx = 0, nty = 0, nzc = 0;
@@ -74,6 +73,22 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
 void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void* av, void* out,
                  cudaStream_t st);
 int stencil_env_enabled();  // TFG_STENCIL (default 1)
+
+// Both SpMM passes of D = A (B C) (p0: B with X = C into D1, p1: A with X =
+// D1 into D) as one persistent dependency-driven kernel: second-op items
+// follow the first-op z chunks they read, so D1 is read back from L2.
+// Opt-in: TFG_STENCIL_SWEEP=1 (lag in chunk rows: TFG_STENCIL_SWEEP_LAG).
+struct StencilSweep {
+  bool on = false;
+  int64_t nitems = 0, ipc = 0;
+  uint32_t epoch = 0;
+  dbuf<int> items;  // op << 30 | item of op, launch order
+  dbuf<int> done;   // per z chunk: first-op items finished (cumulative over launches)
+};
+bool stencil_sweep_prepare(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1);
+void stencil_sweep_run(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1,
+                       const int* b_rp, const int* b_ci, const void* b_av, const int* a_rp,
+                       const int* a_ci, const void* a_av, void* d1, void* out, cudaStream_t st);
 
 // Fused D = A (B C) for a pair of 2-D stencils on the same grid (gb: B, ga:
 // A), D1 kept on chip (registers).  false: not eligible or not enabled (the

@@ -142,7 +142,7 @@ def test_stencil_nan_poison(cuda, oracle):
 
 @pytest.mark.parametrize("knobs", [{"TFG_STENCIL_NW": "8"}, {"TFG_STENCIL_CTAS": "2"},
                                    {"TFG_STENCIL_CTAS": "4"}, {"TFG_STENCIL_NS": "3"},
-                                   {"TFG_STENCIL_ZC": "5", "TFG_STENCIL_PF": "3"}])
+                                   {"TFG_STENCIL_ZC": "5"}])
 def test_stencil_tile_configs(cuda, oracle, monkeypatch, knobs):
     """Every tile / ring / occupancy configuration the plan can pick gives the
     same bits (partial tiles in x, y and z included)."""
@@ -224,3 +224,27 @@ def test_stencil_partitions(cuda, oracle, nx, ny, nz, offs, world):
         got[rows] = outs[r].cpu().numpy()[rows]
     osched = oracle.build_schedule(n, n, a.row_ptr, a.col_idx, OCfg(**cfg.__dict__))
     assert np.array_equal(got, oracle_d(oracle, a, a, c, np.float64, osched))
+
+
+@pytest.mark.parametrize("lag", ["1", "3", "16"])
+def test_stencil_sweep_opt_in(cuda, oracle, monkeypatch, lag):
+    """The opt-in dependency-driven sweep (both passes in one persistent
+    kernel, per-chunk completion counters carrying an epoch) gives the oracle's
+    bits on repeated executions, 2-D and 3-D, for short and long lags."""
+    import torch
+
+    monkeypatch.setenv("TFG_STENCIL_SWEEP", "1")
+    monkeypatch.setenv("TFG_STENCIL_SWEEP_LAG", lag)
+    for nx, ny, nz, offs, cc in ((64, 1, 48, BOX2, 64), (12, 10, 9, BOX3, 128)):
+        a = grid_stencil(nx, ny, nz, offs, 20)
+        b = grid_stencil(nx, ny, nz, offs, 21)
+        c = np.random.default_rng(22).uniform(-1, 1, (a.n_rows, cc))
+        prob = P.DeviceProblem(a, b, c, np.float64)
+        plan = P.Plan(prob, None)
+        assert plan.kernels()["wave1"] == "stencil-sweep", plan.kernels()
+        assert plan.launches == 1
+        want = oracle_d(oracle, a, b, c, np.float64)
+        out = torch.empty((a.n_rows, cc), dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            out.fill_(float("nan"))
+            assert np.array_equal(plan.execute(out).cpu().numpy(), want)
