@@ -2988,11 +2988,12 @@ static int gemm_variant() {
 
 // FP64 first-op GEMM thread tile (BN = 64): 0 = 64x64 blocks of 4x4 (256
 // threads), 1 = 128x64 of 8x8 (128 threads), 2 = 128x64 of 8x4 (256
-// threads; cfg1 first op 0.062 -> 0.056 ms), 3 = as 1 with BK = 32
+// threads), 3 = as 1 with BK = 32, 4 = 64x64 of 8x4 (128 threads; cfg1
+// first op 0.062 (0) -> 0.056 (2) -> 0.047 ms: more, smaller blocks)
 static int gemm_variant_f64() {
   static const int gv = [] {
     const char* e = getenv("TFG_GEMM_F64");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 4;
   }();
   return gv;
 }
@@ -3146,7 +3147,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       pl.gemm_kind = 1;  // BN = 64
     if (pl.gemm_kind)
       pl.gemm_bm = (pl.elem == 4 && (pl.gemm_kind == 1 || gemm_variant() == 2)) ? 128 : 64;
-    if (pl.gemm_kind == 1 && pl.elem == 8 && gemm_variant_f64() >= 1) pl.gemm_bm = 128;
+    if (pl.gemm_kind == 1 && pl.elem == 8 && gemm_variant_f64() >= 1 && gemm_variant_f64() <= 3)
+      pl.gemm_bm = 128;
     if (pl.gemm_kind && pl.elem == 4 &&
         tc_prepare(pl.tc, static_cast<const float*>(pr.d_b_dense), n, bc, cc))
       pl.gemm_bm = 128;
@@ -3697,6 +3699,8 @@ static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc,
       launch_gemm_v2_cfg<T, 128, 64, 16, 8, 4>(pl, B, bc, C, cc, D1, st);
     else if (g64 == 3)
       launch_gemm_v2_cfg<T, 128, 64, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
+    else if (g64 == 4)
+      launch_gemm_v2_cfg<T, 64, 64, 16, 8, 4>(pl, B, bc, C, cc, D1, st);
     else
       launch_gemm_v2_cfg<T, 64, 64, 16, 4, 4>(pl, B, bc, C, cc, D1, st);
   }
