@@ -2540,7 +2540,8 @@ struct SpmmWork {
   }
 
   void build(const std::vector<int>& rows, const std::vector<int>& rp, int cc,
-             size_t elem, cudaStream_t st, const std::vector<int>* ci = nullptr) {
+             size_t elem, cudaStream_t st, const std::vector<int>* ci = nullptr,
+             bool stencil_rows = false) {  // stencil_rows: the stencil kernel takes them
     std::vector<int> sh, lg, k0, k1;
     std::vector<int64_t> off{0};
     sh.reserve(rows.size());
@@ -2620,7 +2621,7 @@ struct SpmmWork {
       const char* e = getenv("TFG_SPMM_BAND");
       return !e || atoi(e) > 0;
     }();
-    if (band_on && ci && identity && (cc % vec == 0) &&
+    if (band_on && ci && identity && !stencil_rows && (cc % vec == 0) &&
         (cc / vec == 8 || cc / vec == 16 || cc / vec == 32 || cc / vec == 64))
       build_band(row0, n_short, rp, *ci, cc, elem, st);
     if (getenv("TFG_DEBUG"))
@@ -2633,7 +2634,7 @@ struct SpmmWork {
       const char* e = getenv("TFG_SPMM_GROUPS");
       return e && atoi(e) > 0;
     }();
-    if (groups_on && ci && (cc == 32 * vec || cc == 64 * vec) && !sh.empty())
+    if (groups_on && ci && !stencil_rows && (cc == 32 * vec || cc == 64 * vec) && !sh.empty())
       build_groups(sh, rp, *ci, st);
   }
   size_t bytes() const {
@@ -3071,14 +3072,28 @@ static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
 
 // Row-list SpMM over ALL rows of a grid-stencil CSR: switch it to the
 // plane-streaming kernel (tfg_stencil.cu).  X must hold n rows.
-static void attach_stencil(SpmmWork& w, int64_t n, const std::vector<int>& rp,
-                           const std::vector<int>& ci, const void* X, int cc, size_t elem) {
-  w.stencil.reset();
-  if (!stencil_env_enabled() || ci.empty() || !w.identity || w.n_short == 0 || w.n_long != 0 ||
-      n > INT32_MAX)
-    return;
+// The grid geometry of an n x n CSR (host copies), or g.nx == 0.
+static StencilGeom probe_stencil(int64_t n, const std::vector<int>& rp,
+                                 const std::vector<int>& ci) {
   StencilGeom g;
-  if (!stencil_detect((int)n, rp, ci, g)) return;
+  if (stencil_env_enabled() && !ci.empty() && n <= INT32_MAX) stencil_detect((int)n, rp, ci, g);
+  return g;
+}
+
+// The row list is a whole-plane slab of the grid (what the stencil kernel runs).
+static bool stencil_rows(const std::vector<int>& rows, const StencilGeom& g, int cc,
+                         size_t elem) {
+  if (g.nx == 0 || rows.empty() || (size_t)cc * elem % 512 != 0) return false;
+  const int64_t nxy = (int64_t)g.nx * g.ny;
+  for (size_t q = 1; q < rows.size(); ++q)
+    if (rows[q] != rows[q - 1] + 1) return false;
+  return rows[0] % nxy == 0 && (int64_t)rows.size() % nxy == 0;
+}
+
+static void attach_stencil(SpmmWork& w, const StencilGeom& g, const void* X, int cc,
+                           size_t elem) {
+  w.stencil.reset();
+  if (g.nx == 0 || !w.identity || w.n_short == 0 || w.n_long != 0) return;
   // the rows must be whole grid planes (a partition's slab of z)
   const int64_t nxy = (int64_t)g.nx * g.ny;
   if (w.row0 % nxy != 0 || w.n_short % nxy != 0) return;
@@ -3134,6 +3149,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   std::vector<int> fo_rows;  // first-op rows handled by stage (a)
   std::vector<int> second_rows;
   std::vector<int> zero_rows;  // empty fused rows, written by the SpMM stage
+  StencilGeom gB;              // B's grid-stencil geometry (sparse B), probed once
   if (pr.b_is_dense) {
     // fast path: cp.async pipelined GEMM when the shapes and pointers allow
     const int V = 16 / (int)pl.elem;
@@ -3417,8 +3433,10 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       d2h(bci.data(), pr.d_b_col_idx, bci.size(), st);
       TFG_CUDA(cudaStreamSynchronize(st));
     }
-    pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st, bci.empty() ? nullptr : &bci);
-    if (pr.b_cols == n) attach_stencil(pl.fo_sparse, n, brp, bci, pr.d_c, cc, pl.elem);
+    if (pr.b_cols == n) gB = probe_stencil(n, brp, bci);
+    pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st, bci.empty() ? nullptr : &bci,
+                       stencil_rows(fo_rows, gB, cc, pl.elem));
+    attach_stencil(pl.fo_sparse, gB, pr.d_c, cc, pl.elem);
   }
   // (c) second-op work (wavefront-1 rows, then the empty fused rows)
   if (!zero_rows.empty()) {
@@ -3432,8 +3450,13 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       d2h(aci.data(), pr.d_a_col_idx, aci.size(), st);
       TFG_CUDA(cudaStreamSynchronize(st));
     }
-    pl.second.build(second_rows, arp, cc, pl.elem, st, aci.empty() ? nullptr : &aci);
-    attach_stencil(pl.second, n, arp, aci, pl.d1.p, cc, pl.elem);
+    // A aliased with B (SpMM-SpMM with B = A): same pattern, same geometry
+    const bool same = !pr.b_is_dense && pr.d_a_row_ptr == pr.d_b_row_ptr &&
+                      pr.d_a_col_idx == pr.d_b_col_idx && pr.b_cols == n;
+    const StencilGeom gA = same ? gB : probe_stencil(n, arp, aci);
+    pl.second.build(second_rows, arp, cc, pl.elem, st, aci.empty() ? nullptr : &aci,
+                    stencil_rows(second_rows, gA, cc, pl.elem));
+    attach_stencil(pl.second, gA, pl.d1.p, cc, pl.elem);
   }
 
   // ---- algorithmic bytes per stage ------------------------------------

@@ -773,14 +773,22 @@ bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& c
   if (n < 9 || (int)rp.size() < n + 1 || rp[n] == 0 || (int64_t)ci.size() < rp[n]) return false;
   // the offset set (col - row) over all rows; a grid stencil has <= 27
   std::vector<int64_t> offs;
-  for (int r = 0; r < n; ++r)
-    for (int k = rp[r]; k < rp[r + 1]; ++k) {
-      const int64_t o = (int64_t)ci[k] - r;
-      if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
-        offs.push_back(o);
-        if (offs.size() > 27) return false;
+  int pb = 0, pe = 0;  // previous row's CSR range: most rows repeat its offsets
+  for (int r = 0; r < n; ++r) {
+    const int b = rp[r], e = rp[r + 1];
+    bool same = e - b == pe - pb && r > 0;
+    for (int k = b; same && k < e; ++k) same = ci[k] - r == ci[pb + (k - b)] - (r - 1);
+    if (!same)
+      for (int k = b; k < e; ++k) {
+        const int64_t o = (int64_t)ci[k] - r;
+        if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+          offs.push_back(o);
+          if (offs.size() > 27) return false;
+        }
       }
-    }
+    pb = b;
+    pe = e;
+  }
   std::sort(offs.begin(), offs.end());
   std::vector<int64_t> pos;
   for (int64_t o : offs)
