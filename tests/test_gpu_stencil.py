@@ -248,3 +248,39 @@ def test_stencil_sweep_opt_in(cuda, oracle, monkeypatch, lag):
         for _ in range(3):
             out.fill_(float("nan"))
             assert np.array_equal(plan.execute(out).cpu().numpy(), want)
+
+
+def test_stencil_random_battery(cuda, oracle):
+    """Seeded random grids, stencil subsets, dropped entries, column counts and
+    dtypes: whatever kernel the plan picks, SpMM-SpMM stays bit-exact."""
+    rng = np.random.default_rng(2024)
+    kinds = set()
+    for case in range(24):
+        d3 = bool(rng.integers(0, 2))
+        if d3:
+            nx, ny, nz = (int(v) for v in rng.integers(3, 14, size=3))
+            box = BOX3
+        else:
+            nx, ny, nz = int(rng.integers(3, 90)), 1, int(rng.integers(2, 40))
+            box = BOX2
+        keep = [o for o in box if o == (0, 0, 0) or rng.random() < 0.8]
+        dt = np.float32 if rng.random() < 0.3 else np.float64
+        cc = int(rng.choice([64, 128, 256] if dt == np.float32 else [64, 128]))
+        a = grid_stencil(nx, ny, nz, keep, 100 + case, dt)
+        b = grid_stencil(nx, ny, nz, keep, 200 + case, dt)
+        if rng.random() < 0.3:  # drop a few nonzeros of A: some rows lose neighbours
+            rp, ci, v = a.row_ptr, a.col_idx, a.values
+            drop = np.zeros(ci.size, bool)
+            drop[rng.choice(ci.size, size=max(1, ci.size // 50), replace=False)] = True
+            rows = np.repeat(np.arange(a.n_rows), np.diff(rp))
+            keep_m = ~drop
+            rp2 = np.zeros(a.n_rows + 1, np.int64)
+            np.cumsum(np.bincount(rows[keep_m], minlength=a.n_rows), out=rp2[1:])
+            a = P.Csr(a.n_rows, a.n_cols, rp2.astype(np.int32), ci[keep_m], v[keep_m])
+        c = rng.uniform(-1, 1, (a.n_rows, cc)).astype(dt)
+        d, ks = run_plan(a, b, c, dt)
+        kinds.add(ks["wave1"])
+        want = oracle_d(oracle, a, b, c, dt)
+        assert np.array_equal(d, want), (case, nx, ny, nz, len(keep), cc, dt, ks,
+                                         max_rel_err(d, want))
+    assert any("stencil" in k for k in kinds), kinds
