@@ -23,6 +23,7 @@ constexpr size_t kSmemBudget = 224 * 1024;
 
 // One sparse operand (a stencil CSR) of a kernel.
 struct OpArgs {
+  unsigned used;  // 27-bit mask of the stencil's neighbours (bit ((dz+1)*3+(dy+1))*3+(dx+1))
   int K;     // nonzeros of a full row
   int full;  // the stencil is the whole 3x3 (x3) box: compile-time value offsets
   int8_t rank[27];
@@ -45,6 +46,7 @@ struct StencilArgs {
   int* sweep_done;          // sweep: first-op items finished per z chunk (cumulative)
   int sweep_target;         // sweep: counter value of a complete chunk this launch
   int nzc;                  // z chunks per tile
+  int dbg_fast;             // timing experiment only: every group takes the fast path (wrong D)
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
@@ -139,12 +141,27 @@ __device__ __forceinline__ void axpy(T (&acc)[VEC], T v, const T (&x)[VEC]) {
 // planes z-1, z, z+1 of the tile (zero-filled outside the grid); rpl: lane
 // m <= M holds row_ptr of point m; valid: points inside the grid; sv: the
 // rows' values from row_ptr[point 0].
+// 27-bit neighbour masks, bit ((dz+1)*3 + (dy+1))*3 + (dx+1)
+constexpr unsigned nb_bits(int axis, int d) {  // all neighbours with offset d along axis (0 x, 1 y, 2 z)
+  unsigned m = 0;
+  for (int q = 0; q < 27; ++q) {
+    const int dx = q % 3 - 1, dy = (q / 3) % 3 - 1, dz = q / 9 - 1;
+    if ((axis == 0 ? dx : (axis == 1 ? dy : dz)) == d) m |= 1u << q;
+  }
+  return m;
+}
+
+// One output plane of a warp's M points into acc.  P0/P1/P2: the
+// shared-memory planes z-1, z, z+1 of the tile (zero-filled outside the
+// grid); rpl: lane m <= M holds row_ptr of point m; valid: points inside the
+// grid; sv: the rows' values from row_ptr[point 0]; (px, py, pz): grid
+// position of point 0.
 template <class T, bool D3, int M, int ROW>
 __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpArgs& op,
                                                 const T* __restrict__ P0, const T* __restrict__ P1,
                                                 const T* __restrict__ P2, const T* __restrict__ sv,
                                                 int rpl, unsigned valid, int wy, int col0,
-                                                int rbase, int lane,
+                                                int rbase, int px, int py, int pz, int lane,
                                                 T (&acc)[M][16 / sizeof(T)]) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int CW = (int)(kSliceBytes / sizeof(T));
@@ -155,16 +172,7 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
   // the window rows of points outside the tile are still in the plane
   // buffer (or the next shared-memory region), so the fast path computes all
   // M points and stores only the valid ones
-  const bool fast = op.full && valid != 0 && vM - v0 == M * 3 * NL;
-  int vb[M + 1];
-  unsigned reg = 0;
-  if (!fast) {
-#pragma unroll
-    for (int m = 0; m <= M; ++m) vb[m] = __shfl_sync(0xffffffffu, rpl, m);
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-      if (((valid >> m) & 1u) && vb[m + 1] - vb[m] == op.K) reg |= 1u << m;
-  }
+  const bool fast = op.full && valid != 0 && (vM - v0 == M * 3 * NL || a.dbg_fast);
 #pragma unroll
   for (int m = 0; m < M; ++m)
 #pragma unroll
@@ -188,61 +196,103 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
         if (k >= 2) axpy<T, VEC>(acc[k - 2], sv[(k - 2) * K + 3 * l + 2], xr);
       }
     }
-  } else {
-    if (reg) {
+    return;
+  }
+  // Grid-face points: a row whose nonzero count equals the number of its
+  // in-grid stencil neighbours holds exactly those (every nonzero was checked
+  // to be an in-grid neighbour at plan time), so its value for neighbour bit
+  // q sits at popc(mask & (2^q - 1)) -- the same compile-time loop as the
+  // fast path, predicated per point.  Other rows (missing in-grid
+  // neighbours) walk their own CSR entries.
+  int vb[M + 1];
 #pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        const int dz = D3 ? l / 3 - 1 : l - 1;
-        const int dy = D3 ? l % 3 - 1 : 0;
-        const int li = (dz + 1) * 3 + (dy + 1);
-        const int rk0 = op.rank[li * 3 + 0], rk1 = op.rank[li * 3 + 1], rk2 = op.rank[li * 3 + 2];
-        if (rk0 < 0 && rk1 < 0 && rk2 < 0) continue;
-        const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
-        const T* base = P + ((D3 ? (wy + 1 + dy) * ROW : 0) + col0) * CW + lane * VEC;
+  for (int m = 0; m <= M; ++m) vb[m] = __shfl_sync(0xffffffffu, rpl, m);
+  unsigned pm[M];
+  unsigned geo = 0;
+  {
+    unsigned face = op.used;
+    if (D3) {
+      if (py == 0) face &= ~nb_bits(1, -1);
+      if (py == a.ny - 1) face &= ~nb_bits(1, 1);
+    }
+    if (pz == 0) face &= ~nb_bits(D3 ? 2 : 2, -1);
+    if (pz == a.nz - 1) face &= ~nb_bits(2, 1);
 #pragma unroll
-        for (int k = 0; k < M + 2; ++k) {
-          T xr[VEC];
-          ldv<T, VEC>(xr, base + k * CW);
-          // this row is neighbour dx = -1 of point k, 0 of k - 1, +1 of k - 2
-          if (k < M && rk0 >= 0 && ((reg >> k) & 1u))
-            axpy<T, VEC>(acc[k], sv[vb[k] - v0 + rk0], xr);
-          if (k >= 1 && k - 1 < M && rk1 >= 0 && ((reg >> (k - 1)) & 1u))
-            axpy<T, VEC>(acc[k - 1], sv[vb[k - 1] - v0 + rk1], xr);
-          if (k >= 2 && rk2 >= 0 && ((reg >> (k - 2)) & 1u))
-            axpy<T, VEC>(acc[k - 2], sv[vb[k - 2] - v0 + rk2], xr);
+    for (int m = 0; m < M; ++m) {
+      unsigned pmm = face;
+      if (px + m == 0) pmm &= ~nb_bits(0, -1);
+      if (px + m == a.nx - 1) pmm &= ~nb_bits(0, 1);
+      pm[m] = pmm;
+      if (((valid >> m) & 1u) && vb[m + 1] - vb[m] == __popc(pmm)) geo |= 1u << m;
+    }
+  }
+  if (geo) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int dz = D3 ? l / 3 - 1 : l - 1;
+      const int dy = D3 ? l % 3 - 1 : 0;
+      const int li = (dz + 1) * 3 + (dy + 1);
+      if (!(op.used & (7u << (3 * li)))) continue;
+      const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+      const T* base = P + ((D3 ? (wy + 1 + dy) * ROW : 0) + col0) * CW + lane * VEC;
+      // the line's values of all M points first (independent shared loads,
+      // absent neighbours read a dummy slot), then the predicated updates:
+      // a face group costs about what an interior group does, so the CTA's
+      // other warps are not held at the plane ring by it
+      T vl[M][3];
+      unsigned pr = 0;  // bit 3 m + j: point m has neighbour dx = j - 1 on this line
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int q = 3 * li + j;
+          const bool has = ((geo >> m) & 1u) && ((pm[m] >> q) & 1u);
+          pr |= (unsigned)has << (3 * m + j);
+          vl[m][j] = sv[has ? vb[m] - v0 + __popc(pm[m] & ((1u << q) - 1u)) : 0];
+        }
+#pragma unroll
+      for (int k = 0; k < M + 2; ++k) {
+        T xr[VEC];
+        ldv<T, VEC>(xr, base + k * CW);
+        // this row is neighbour dx = -1 of point k, 0 of k - 1, +1 of k - 2
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int m = k - j;
+          if (m < 0 || m >= M) continue;
+          if ((pr >> (3 * m + j)) & 1u) axpy<T, VEC>(acc[m], vl[m][j], xr);
         }
       }
     }
-    const unsigned irr = valid & ~reg;
-    if (irr) {  // grid-face rows: their own CSR order, neighbours from the planes
-      // the rows' column indices, lane-parallel and all issued up front
-      // (one memory round trip for the group, not one per nonzero)
-      int cl[M];
+  }
+  const unsigned irr = valid & ~geo;
+  if (irr) {  // rows missing in-grid neighbours: their own CSR order
+    // the rows' column indices, lane-parallel and all issued up front
+    // (one memory round trip for the group, not one per nonzero)
+    int cl[M];
 #pragma unroll
-      for (int m = 0; m < M; ++m)
-        cl[m] = ((irr >> m) & 1u) && vb[m] + lane < vb[m + 1] ? __ldg(op.ci + vb[m] + lane) : 0;
+    for (int m = 0; m < M; ++m)
+      cl[m] = ((irr >> m) & 1u) && vb[m] + lane < vb[m + 1] ? __ldg(op.ci + vb[m] + lane) : 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        if (!((irr >> m) & 1u)) continue;
-        const int r = rbase + m;
-        for (int k = vb[m]; k < vb[m + 1]; ++k) {  // <= 27 nonzeros: one lane each
-          int o = __shfl_sync(0xffffffffu, cl[m], k - vb[m]) - r;
-          int dz = 0, dy = 0;
-          if (D3) {
-            dz = o > a.nxy / 2 ? 1 : (o < -(a.nxy / 2) ? -1 : 0);
-            o -= dz * a.nxy;
-            dy = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
-            o -= dy * a.nx;
-          } else {
-            dz = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
-            o -= dz * a.nx;
-          }
-          const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
-          const int yy = D3 ? wy + 1 + dy : 0;
-          T xr[VEC];
-          ldv<T, VEC>(xr, P + (yy * ROW + col0 + m + 1 + o) * CW + lane * VEC);
-          axpy<T, VEC>(acc[m], sv[k - v0], xr);
+    for (int m = 0; m < M; ++m) {
+      if (!((irr >> m) & 1u)) continue;
+      const int r = rbase + m;
+      for (int k = vb[m]; k < vb[m + 1]; ++k) {  // <= 27 nonzeros: one lane each
+        int o = __shfl_sync(0xffffffffu, cl[m], k - vb[m]) - r;
+        int dz = 0, dy = 0;
+        if (D3) {
+          dz = o > a.nxy / 2 ? 1 : (o < -(a.nxy / 2) ? -1 : 0);
+          o -= dz * a.nxy;
+          dy = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
+          o -= dy * a.nx;
+        } else {
+          dz = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
+          o -= dz * a.nx;
         }
+        const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+        const int yy = D3 ? wy + 1 + dy : 0;
+        T xr[VEC];
+        ldv<T, VEC>(xr, P + (yy * ROW + col0 + m + 1 + o) * CW + lane * VEC);
+        axpy<T, VEC>(acc[m], sv[k - v0], xr);
       }
     }
   }
@@ -253,11 +303,12 @@ __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArg
                                                const T* __restrict__ P0, const T* __restrict__ P1,
                                                const T* __restrict__ P2, const T* __restrict__ sv,
                                                int rpl, unsigned valid, int wy, int col0,
-                                               int rbase, T* __restrict__ outp, int ostride,
-                                               int lane) {
+                                               int rbase, int px, int py, int pz,
+                                               T* __restrict__ outp, int ostride, int lane) {
   constexpr int VEC = 16 / sizeof(T);
   T acc[M][VEC];
-  stencil_compute<T, D3, M, ROW>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase, lane, acc);
+  stencil_compute<T, D3, M, ROW>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase, px, py, pz,
+                                 lane, acc);
 #pragma unroll
   for (int m = 0; m < M; ++m)
     if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * ostride, acc[m]);
@@ -427,7 +478,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       stencil_points<T, D3, M, TL::ROW>(
           a, opa, planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
           planes + (size_t)s2 * a.plane_elems, svb + (j % 3) * VS, rp_j, valid, wy, wx * M, rb,
-          outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
+          x, y, z0 + j, outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
           a.cc, lane);
       __syncwarp();
       if (lane == 0) {
@@ -668,7 +719,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
         stencil_compute<T, false, MA, ROWC>(
             a, a.op[0], cpl + (size_t)s0 * a.plane_elems, cpl + (size_t)s1 * a.plane_elems,
             cpl + (size_t)s2 * a.plane_elems, svA + (u % 3) * VS, rp_u, validA, 0, warp * M,
-            rowA(u), lane, Dn);
+            rowA(u), xA, 0, z0 - 1 + u, lane, Dn);
       }
       __syncwarp();
       if (lane == 0) {
@@ -959,10 +1010,14 @@ void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void
   a.cc = sp.cc;
   a.items = sp.items;
   a.nzc = sp.nzc;
+  a.dbg_fast = env_int("TFG_STENCIL_DBG_FAST", 0);
   a.plane_elems = (int)(sp.plane_bytes / sp.elem);
   a.op[0].K = g.K;
   a.op[0].full = g.K == (g.d3 ? 27 : 9);
   memcpy(a.op[0].rank, g.rank, sizeof(g.rank));
+  a.op[0].used = 0;
+  for (int q = 0; q < 27; ++q)
+    if (g.rank[q] >= 0) a.op[0].used |= 1u << q;
   a.op[0].rp = rp;
   a.op[0].ci = ci;
   a.op[0].av = av;
@@ -1065,6 +1120,9 @@ static void stencil2_launch_t(const StencilPlan& sp, const StencilArgs& a, cudaS
 }
 
 static void fill_op(OpArgs& o, const StencilGeom& g, const int* rp, const int* ci, const void* av) {
+  o.used = 0;
+  for (int q = 0; q < 27; ++q)
+    if (g.rank[q] >= 0) o.used |= 1u << q;
   o.K = g.K;
   o.full = g.K == (g.d3 ? 27 : 9);
   memcpy(o.rank, g.rank, sizeof(g.rank));
