@@ -242,14 +242,18 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
       T vl[M][3];
       unsigned pr = 0;  // bit 3 m + j: point m has neighbour dx = j - 1 on this line
 #pragma unroll
-      for (int m = 0; m < M; ++m)
+      for (int m = 0; m < M; ++m) {
+        const unsigned bits = ((geo >> m) & 1u) ? (pm[m] >> (3 * li)) & 7u : 0u;
+        pr |= bits << (3 * m);
+        // value index of the line's first present neighbour, then +1 per bit
+        int idx = vb[m] - v0 + __popc(pm[m] & ((1u << (3 * li)) - 1u));
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-          const int q = 3 * li + j;
-          const bool has = ((geo >> m) & 1u) && ((pm[m] >> q) & 1u);
-          pr |= (unsigned)has << (3 * m + j);
-          vl[m][j] = sv[has ? vb[m] - v0 + __popc(pm[m] & ((1u << q) - 1u)) : 0];
+          const bool has = (bits >> j) & 1u;
+          vl[m][j] = sv[has ? idx : 0];
+          idx += has;
         }
+      }
 #pragma unroll
       for (int k = 0; k < M + 2; ++k) {
         T xr[VEC];
