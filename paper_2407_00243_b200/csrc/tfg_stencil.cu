@@ -156,7 +156,18 @@ constexpr unsigned nb_bits(int axis, int d) {  // all neighbours with offset d a
 // grid); rpl: lane m <= M holds row_ptr of point m; valid: points inside the
 // grid; sv: the rows' values from row_ptr[point 0]; (px, py, pz): grid
 // position of point 0.
-template <class T, bool D3, int M, int ROW>
+// Padded value layout of a full-box group (PAD): point m's three values of
+// line l at sv[m * 4 * NL + 4 * l + j] -- one 16-byte aligned group per line
+// -- so a point's line values come in one (fp32) or two (fp64) shared loads.
+template <bool D3>
+__device__ __forceinline__ int pad_index(int t) {  // t = m * K + 3 l + j
+  constexpr int K = D3 ? 27 : 9;
+  const int m = t / K, r = t - m * K;
+  const int l = r / 3;
+  return m * (4 * (D3 ? 9 : 3)) + 4 * l + (r - 3 * l);
+}
+
+template <class T, bool D3, int M, int ROW, bool PAD = false>
 __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpArgs& op,
                                                 const T* __restrict__ P0, const T* __restrict__ P1,
                                                 const T* __restrict__ P2, const T* __restrict__ sv,
@@ -177,6 +188,38 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
   for (int m = 0; m < M; ++m)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[m][v] = T(0);
+  if (fast && PAD) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int dz = D3 ? l / 3 - 1 : l - 1;
+      const int dy = D3 ? l % 3 - 1 : 0;
+      const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+      const T* base = P + ((D3 ? (wy + 1 + dy) * ROW : 0) + col0) * CW + lane * VEC;
+      T vl[M][4];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const T* q = sv + m * 4 * NL + 4 * l;
+        if constexpr (sizeof(T) == 8) {
+          T v01[2];
+          ldv<T, 2>(v01, q);
+          vl[m][0] = v01[0];
+          vl[m][1] = v01[1];
+          vl[m][2] = q[2];
+        } else {
+          ldv<T, 4>(vl[m], q);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < M + 2; ++k) {
+        T xr[VEC];
+        ldv<T, VEC>(xr, base + k * CW);
+        if (k < M) axpy<T, VEC>(acc[k], vl[k][0], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC>(acc[k - 1], vl[k - 1][1], xr);
+        if (k >= 2) axpy<T, VEC>(acc[k - 2], vl[k - 2][2], xr);
+      }
+    }
+    return;
+  }
   if (fast) {
     // whole box, every point interior: point m's value for line l, dx is
     // sv[m * K + 3 * l + dx + 1] -- all offsets compile-time
@@ -302,7 +345,7 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
   }
 }
 
-template <class T, bool D3, int M, int ROW>
+template <class T, bool D3, int M, int ROW, bool PAD = false>
 __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArgs& op,
                                                const T* __restrict__ P0, const T* __restrict__ P1,
                                                const T* __restrict__ P2, const T* __restrict__ sv,
@@ -311,8 +354,8 @@ __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArg
                                                T* __restrict__ outp, int ostride, int lane) {
   constexpr int VEC = 16 / sizeof(T);
   T acc[M][VEC];
-  stencil_compute<T, D3, M, ROW>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase, px, py, pz,
-                                 lane, acc);
+  stencil_compute<T, D3, M, ROW, PAD>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase, px, py,
+                                      pz, lane, acc);
 #pragma unroll
   for (int m = 0; m < M; ++m)
     if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * ostride, acc[m]);
@@ -407,7 +450,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   // ahead (one commit group per plane), so no consumer instruction waits on
   // a global load.
   constexpr int VR = (M * (D3 ? 27 : 9) + 31) / 32;  // value elements per lane and plane
-  constexpr int VS = VR * 32;                         // value slot (elements)
+  constexpr int VS0 = VR * 32;
+  constexpr int VS = VS0 > M * 4 * (D3 ? 9 : 3) ? VS0 : M * 4 * (D3 ? 9 : 3);  // value slot
   T* svb = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * 3 * VS;
   int* srp = reinterpret_cast<int*>(reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) +
                                     (size_t)NW * 3 * VS) + warp * 8 * 16;
@@ -442,10 +486,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       if (!wlive || jj >= nzl) return;
       const int v0 = srp[(jj & 7) * 16], v1 = srp[(jj & 7) * 16 + M];
       T* dst = svb + (jj % 3) * VS;
+      // the compute side takes the padded full-box path exactly when this holds
+      const bool pad = opa.full && valid != 0 && (v1 - v0 == M * (D3 ? 27 : 9) || a.dbg_fast);
 #pragma unroll
       for (int i = 0; i < VR; ++i) {
-        const int k = v0 + lane + 32 * i;
-        if (k < v1) cp_async_ca<sizeof(T)>(dst + lane + 32 * i, av + k);
+        const int t = lane + 32 * i;
+        if (v0 + t < v1) cp_async_ca<sizeof(T)>(dst + (pad ? pad_index<D3>(t) : t), av + v0 + t);
       }
     };
     issue_rp(0);
@@ -479,7 +525,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       }
       s_bar_wait(&full[s2], p2);
       const int rb = r0 + j * a.nxy;
-      stencil_points<T, D3, M, TL::ROW>(
+      stencil_points<T, D3, M, TL::ROW, true>(
           a, opa, planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
           planes + (size_t)s2 * a.plane_elems, svb + (j % 3) * VS, rp_j, valid, wy, wx * M, rb,
           x, y, z0 + j, outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
@@ -906,8 +952,9 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   sp.nty = (g.ny + sp.ty - 1) / sp.ty;
   sp.plane_bytes = (size_t)sp.cw * (sp.tx + 2) * sp.tyh * elem;
   // per warp: 3 value slots + 8 row-pointer slots (consumer cp.async ring)
-  const size_t vbytes =
-      (size_t)sp.nw * (3 * ((sp.M * (g.d3 ? 27 : 9) + 31) / 32) * 32 * elem + 8 * 16 * 4);
+  const size_t vslot = std::max<size_t>((sp.M * (g.d3 ? 27 : 9) + 31) / 32 * 32,
+                                        (size_t)sp.M * 4 * (g.d3 ? 9 : 3));
+  const size_t vbytes = (size_t)sp.nw * (3 * vslot * elem + 8 * 16 * 4);
   // CTAs per SM, then the deepest ring that fits (>= 3 planes in use)
   const int per_env = env_int("TFG_STENCIL_CTAS", 0);
   int per_sm = per_env > 0 ? std::min(per_env, sp.nw == 8 ? 2 : 4) : (sp.nw == 8 ? (g.d3 ? 1 : 2) : 3);
