@@ -64,16 +64,23 @@ __device__ __forceinline__ unsigned group_mask(int lpr) {
 // One CSR row times X, LPR lanes per row, each lane NCH x VEC columns.
 // Per-element order = ascending nonzeros, separate mul and add
 // (kernels.hpp:75-79).  XL(c, ch, out[VEC]) loads X row c, chunk ch.
-template <class T, int VEC, int LPR, int NCH, class XL, int UNR = 4>
-__device__ __forceinline__ void spmm_row(int kb, int ke,
-                                         const int* __restrict__ ci,
-                                         const T* __restrict__ av, int gl,
-                                         unsigned gmask, XL xl,
-                                         T (&acc)[NCH][VEC]) {
-#pragma unroll
-  for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[ch][e] = T(0);
+// acc += a * x per term: separately rounded mul and add (the reference's
+// order and rounding), or one fused multiply-add when FMA (GeMM-SpMM plans
+// whose first op is already tolerance-bound; never for SpMM-SpMM parity)
+template <class T, bool FMA>
+__device__ __forceinline__ T madd(T acc, T a, T x) {
+  if constexpr (FMA)
+    return fops<T>::fma(a, x, acc);
+  else
+    return fops<T>::add(acc, fops<T>::mul(a, x));
+}
+
+template <class T, int VEC, int LPR, int NCH, class XL, int UNR = 4, bool FMA = false>
+__device__ __forceinline__ void spmm_accum(int kb, int ke,
+                                           const int* __restrict__ ci,
+                                           const T* __restrict__ av, int gl,
+                                           unsigned gmask, XL xl,
+                                           T (&acc)[NCH][VEC]) {
   for (int k0 = kb; k0 < ke; k0 += LPR) {
     const int kk = k0 + gl;
     int c = 0;
@@ -103,7 +110,7 @@ __device__ __forceinline__ void spmm_row(int kb, int ke,
         for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
           for (int e = 0; e < VEC; ++e)
-            acc[ch][e] = fops<T>::add(acc[ch][e], fops<T>::mul(au[q], x[q][ch][e]));
+            acc[ch][e] = madd<T, FMA>(acc[ch][e], au[q], x[q][ch][e]);
     }
     for (; u < cnt; ++u) {
       const int cu = __shfl_sync(gmask, c, u, LPR);
@@ -115,9 +122,23 @@ __device__ __forceinline__ void spmm_row(int kb, int ke,
       for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int e = 0; e < VEC; ++e)
-          acc[ch][e] = fops<T>::add(acc[ch][e], fops<T>::mul(au, x[ch][e]));
+          acc[ch][e] = madd<T, FMA>(acc[ch][e], au, x[ch][e]);
     }
   }
+}
+
+// acc = row kb..ke times X, from 0 (spmm_row, kernels.hpp:71-80)
+template <class T, int VEC, int LPR, int NCH, class XL, int UNR = 4, bool FMA = false>
+__device__ __forceinline__ void spmm_row(int kb, int ke,
+                                         const int* __restrict__ ci,
+                                         const T* __restrict__ av, int gl,
+                                         unsigned gmask, XL xl,
+                                         T (&acc)[NCH][VEC]) {
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[ch][e] = T(0);
+  spmm_accum<T, VEC, LPR, NCH, XL, UNR, FMA>(kb, ke, ci, av, gl, gmask, xl, acc);
 }
 
 }  // namespace dev

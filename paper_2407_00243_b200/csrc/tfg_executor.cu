@@ -53,7 +53,8 @@ using namespace dev;
 // gathered, and X gathers are issued UNR at a time (predicated), so each
 // row costs about one dependent memory round trip.  Per-element order stays
 // ascending with separately rounded mul/add (kernels.hpp:75-79).
-template <class T, int VEC, int LPR, int NCH, int UNR, int MINB = 1, int STRIP = LPR>
+template <class T, int VEC, int LPR, int NCH, int UNR, int MINB = 1, int STRIP = LPR,
+          bool FMA = false>
 __global__ void __launch_bounds__(256, MINB)
     k_spmm_strip(int64_t nrows, const int* __restrict__ rows, int row0,
                  const int* __restrict__ rp, const int* __restrict__ ci,
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(256, MINB)
           for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
             for (int v = 0; v < VEC; ++v)
-              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au[u], x[u][ch][v]));
+              acc[ch][v] = madd<T, FMA>(acc[ch][v], au[u], x[u][ch][v]);
         }
     }
     if (row_done) {
@@ -1486,7 +1487,7 @@ __global__ void __launch_bounds__(256)
 
 // Vectorised long-row segments: LPR lanes per segment (16-byte gathers),
 // partial rows to scratch, then an ordered combine per long row.
-template <class T, int VEC, int LPR, int NCH, int UNR = 4, int MINB = 1>
+template <class T, int VEC, int LPR, int NCH, int UNR = 4, int MINB = 1, bool FMA = false>
 __global__ void __launch_bounds__(256, MINB)
     k_spmm_segments_vec(int64_t nseg, const int* __restrict__ seg_k0,
                         const int* __restrict__ seg_k1, const int* __restrict__ ci,
@@ -1500,7 +1501,7 @@ __global__ void __launch_bounds__(256, MINB)
     ldv<T, VEC>(x, X + (size_t)c * ldx + (ch * LPR + gl) * VEC);
   };
   T acc[NCH][VEC];
-  spmm_row<T, VEC, LPR, NCH, decltype(xl), UNR>(seg_k0[g], seg_k1[g], ci, av, gl, gmask, xl, acc);
+  spmm_row<T, VEC, LPR, NCH, decltype(xl), UNR, FMA>(seg_k0[g], seg_k1[g], ci, av, gl, gmask, xl, acc);
   T* o = partial + (size_t)g * ldx;
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
@@ -2191,6 +2192,17 @@ __global__ void k_gather_rows(const T* __restrict__ src, int cols,
     dst[e] = src[(size_t)rows[r] * cols + c];
   }
 }
+// D[rows[i], :] = 0 (empty rows of a row list), 16-byte stores
+__global__ void k_zero_rows(int64_t nrows, const int* __restrict__ rows, int row_bytes,
+                            unsigned char* __restrict__ out) {
+  const int per = row_bytes / 16;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nrows * per) return;
+  const int64_t i = t / per;
+  const int q = (int)(t - i * per);
+  reinterpret_cast<uint4*>(out + (size_t)rows[i] * row_bytes)[q] = make_uint4(0, 0, 0, 0);
+}
+
 template <class T>
 __global__ void k_scatter_rows(const T* __restrict__ src, int cols,
                                const int* __restrict__ rows, int64_t n,
@@ -2476,6 +2488,10 @@ struct SpmmWork {
   bool identity = false;  // short rows are exactly [row0, row0 + n_short)
   int row0 = 0;
   dbuf<int> short_rows, long_rows, seg_k0, seg_k1;
+  // empty rows of a non-stencil list: D rows zero-filled by one streaming
+  // kernel instead of costing a lane group's row iteration each
+  int64_t n_empty = 0;
+  dbuf<int> empty_rows;
   dbuf<int64_t> long_seg_off;
   dbuf<unsigned char> partial;
 
@@ -2539,6 +2555,18 @@ struct SpmmWork {
     TFG_CUDA(cudaStreamSynchronize(st));
   }
 
+  // side stream for the long rows (runs beside the short-row kernel)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  SpmmWork() = default;
+  SpmmWork(const SpmmWork&) = delete;
+  SpmmWork& operator=(const SpmmWork&) = delete;
+  ~SpmmWork() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
+
   void build(const std::vector<int>& rows, const std::vector<int>& rp, int cc,
              size_t elem, cudaStream_t st, const std::vector<int>* ci = nullptr,
              bool stencil_rows = false) {  // stencil_rows: the stencil kernel takes them
@@ -2563,9 +2591,16 @@ struct SpmmWork {
         seg_len = thr;
       }
     }
+    static const bool split_empty = [] {
+      const char* e = getenv("TFG_W1_EMPTY");
+      return !e || atoi(e) > 0;
+    }();
+    std::vector<int> em;
     for (int r : rows) {
       const int b = rp[r], e = rp[r + 1];
-      if (e - b <= long_thr) {
+      if (e == b && split_empty && !stencil_rows && ci && ((size_t)cc * elem) % 16 == 0) {
+        em.push_back(r);
+      } else if (e - b <= long_thr) {
         sh.push_back(r);
       } else {
         lg.push_back(r);
@@ -2575,6 +2610,11 @@ struct SpmmWork {
         }
         off.push_back((int64_t)k0.size());
       }
+    }
+    n_empty = (int64_t)em.size();
+    if (n_empty) {
+      empty_rows.alloc(em.size());
+      h2d(empty_rows.p, em.data(), em.size(), st);
     }
     n_short = (int64_t)sh.size();
     n_long = (int64_t)lg.size();
@@ -2630,6 +2670,15 @@ struct SpmmWork {
               "blocks=%d stage_cap=%d smem=%zu ci=%d\n",
               (long long)n_short, (long long)n_long, (int)identity, (int)skewed, (int)banded,
               band_R, band_blocks, stage_cap, band_smem, ci ? 1 : 0);
+    static const bool conc_on = [] {
+      const char* e = getenv("TFG_W1_CONCURRENT");
+      return !e || atoi(e) > 0;
+    }();
+    if (conc_on && n_long > 0 && n_short > 0 && !side) {
+      TFG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      TFG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      TFG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
     static const bool groups_on = [] {
       const char* e = getenv("TFG_SPMM_GROUPS");
       return e && atoi(e) > 0;
@@ -2642,9 +2691,11 @@ struct SpmmWork {
            long_seg_off.bytes() + partial.bytes() + g_rows.bytes() + ucol.bytes() +
            g_uoff.bytes() + umask.bytes() + g_poff.bytes() + gperm.bytes() + gval.bytes() +
            run_begin.bytes() + run_start.bytes() + run_len.bytes() + idx_off.bytes() +
-           lidx.bytes();
+           lidx.bytes() + empty_rows.bytes();
   }
-  int launches() const { return (n_short > 0) + 2 * (n_long > 0) + (grouped ? 1 : 0); }
+  int launches() const {
+    return (n_short > 0) + 2 * (n_long > 0) + (grouped ? 1 : 0) + (n_empty > 0);
+  }
 };
 
 // TFG_BAND_DIA=0 switches the stencil consumer off at execution time
@@ -2854,31 +2905,19 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
 }
 
 template <class T>
-static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
-                     const T* av, const T* X, int cc, T* out, cudaStream_t st) {
-  if (w.stencil) {
-    stencil_run(*w.stencil, rp, ci, av, out, st);
-    return;
-  }
-  spmm_dispatch_short<T>(w, rp, ci, av, X, cc, out, st);
-  if (w.n_long) {
-    T* partial = reinterpret_cast<T*>(w.partial.p);
-    constexpr int VEC = 16 / sizeof(T);
-    static const int seg_unr = [] {  // gathers in flight per lane group
-      const char* e = getenv("TFG_SEG_UNR");
-      return e ? atoi(e) : 8;  // 8: cfg5 wavefront 1 10.3 -> 9.1 ms (vs 4)
-    }();
-    const int L = cc % VEC == 0 ? cc / VEC : 0;
+static void spmm_long(const SpmmWork& w, const int* ci, const T* av, const T* X, int cc, T* out,
+                      cudaStream_t st) {
+  T* partial = reinterpret_cast<T*>(w.partial.p);
+  constexpr int VEC = 16 / sizeof(T);
+  static const int seg_unr = [] {  // gathers in flight per lane group
+    const char* e = getenv("TFG_SEG_UNR");
+    return e ? atoi(e) : 8;  // 8: cfg5 wavefront 1 10.3 -> 9.1 ms (vs 4)
+  }();
+  const int L = cc % VEC == 0 ? cc / VEC : 0;
 #define TFG_SEG(LPR, NCH)                                                                     \
   {                                                                                           \
     if (seg_unr == 2)                                                                         \
       k_spmm_segments_vec<T, VEC, LPR, NCH, 2, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
-          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
-    else if (seg_unr == 3)                                                                    \
-      k_spmm_segments_vec<T, VEC, LPR, NCH, 4, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
-          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
-    else if (seg_unr == 5)                                                                    \
-      k_spmm_segments_vec<T, VEC, LPR, NCH, 8, 4><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
           w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
     else if (seg_unr == 16)                                                                   \
       k_spmm_segments_vec<T, VEC, LPR, NCH, 16><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(   \
@@ -2895,17 +2934,45 @@ static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
     TFG_LAUNCH_CHECK();                                                                       \
     return;                                                                                   \
   }
-    if (L == 8) TFG_SEG(8, 1)
-    if (L == 16) TFG_SEG(16, 1)
-    if (L == 32) TFG_SEG(32, 1)
-    if (L == 64) TFG_SEG(32, 2)
+  if (L == 8) TFG_SEG(8, 1)
+  if (L == 16) TFG_SEG(16, 1)
+  if (L == 32) TFG_SEG(32, 1)
+  if (L == 64) TFG_SEG(32, 2)
 #undef TFG_SEG
-    k_spmm_segments<T><<<blocks_for(w.n_seg * 32), 256, 0, st>>>(
-        w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, cc, partial);
+  k_spmm_segments<T><<<blocks_for(w.n_seg * 32), 256, 0, st>>>(
+      w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, cc, partial);
+  TFG_LAUNCH_CHECK();
+  k_segment_combine<T><<<blocks_for(w.n_long * 32), 256, 0, st>>>(
+      w.n_long, w.long_rows.p, w.long_seg_off.p, partial, cc, out, cc);
+  TFG_LAUNCH_CHECK();
+}
+
+template <class T>
+static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
+                     const T* av, const T* X, int cc, T* out, cudaStream_t st) {
+  if (w.stencil) {
+    stencil_run(*w.stencil, rp, ci, av, out, st);
+    return;
+  }
+  // short and long (segmented) rows are independent: the long rows run on a
+  // side stream beside the short-row kernel (latency-bound gathers both)
+  const bool fork = w.side && w.n_long && w.n_short;
+  if (fork) {
+    TFG_CUDA(cudaEventRecord(w.ev_fork, st));
+    TFG_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
+  }
+  if (w.n_long) spmm_long<T>(w, ci, av, X, cc, out, fork ? w.side : st);
+  if (w.n_empty) {
+    const int rb = cc * (int)sizeof(T);
+    const int64_t thr = w.n_empty * (rb / 16);
+    k_zero_rows<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
+        w.n_empty, w.empty_rows.p, rb, reinterpret_cast<unsigned char*>(out));
     TFG_LAUNCH_CHECK();
-    k_segment_combine<T><<<blocks_for(w.n_long * 32), 256, 0, st>>>(
-        w.n_long, w.long_rows.p, w.long_seg_off.p, partial, cc, out, cc);
-    TFG_LAUNCH_CHECK();
+  }
+  spmm_dispatch_short<T>(w, rp, ci, av, X, cc, out, st);
+  if (fork) {
+    TFG_CUDA(cudaEventRecord(w.ev_join, w.side));
+    TFG_CUDA(cudaStreamWaitEvent(st, w.ev_join, 0));
   }
 }
 
@@ -3955,7 +4022,7 @@ tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
   return guard([&] {
     if (!pl || !buf || len < 1) throw invalid_argument("plan_kernels: null plan or buffer");
     auto spmm_kind = [](const SpmmWork& w) -> std::string {
-      if (w.n_short == 0 && w.n_long == 0) return "none";
+      if (w.n_short == 0 && w.n_long == 0 && !w.n_empty) return "none";
       std::string k;
       if (w.stencil)
         k = w.stencil->g.d3 ? "stencil3d" : "stencil2d";

@@ -481,8 +481,8 @@ class Plan:
 
     def kernels(self) -> dict:
         """Kernel chosen for each stage: {"first_op": ..., "fused": ..., "wave1": ...}."""
-        buf = C.create_string_buffer(256)
-        check(lib().tfg_plan_kernels(self._h, buf, 256))
+        buf = C.create_string_buffer(1024)
+        check(lib().tfg_plan_kernels(self._h, buf, 1024))
         return dict(kv.split("=", 1) for kv in buf.value.decode().split())
 
     def stats(self):
