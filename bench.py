@@ -1,12 +1,15 @@
 #!/usr/bin/env python
 """Benchmark of the fused D = A(BC) hot path (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
   python bench.py --impl reference ...     (the reference CPU executor)
 
 A "step" is one execution of the tile-fusion plan (wavefront 0 + wavefront
 1) over one synthetic problem resident in HBM.  Default workload = BASELINE
-configs[1] (cfg2: SpMM-SpMM fp64, 9-point stencil on 1024^2, cCol = 64).
+configs[4] (cfg5: GeMM-SpMM fp32, R-MAT 2^23 avg degree 32, bCol 256, cCol
+64), the largest configuration that fits one GPU and the one the metric's
+"at 1/2/4/8 B200" names; the other four configs are summarised in the same
+line ("configs") and are parity-test cases.
 Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
 events on the launching stream, the L2 flushed (256 MiB write) between steps
 outside the events; barrier + synchronize around the timed region; the max
@@ -38,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the workload (testing only)")
     ap.add_argument("--ct-size", type=int, default=2048)
     ap.add_argument("--cache-kb", type=float, default=1280.0)
@@ -46,20 +49,72 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--flush-mib", type=int, default=256)
+    ap.add_argument("--no-summary", action="store_true",
+                    help="skip the per-config summary of the other BASELINE configs")
     ap.add_argument("--quick", action="store_true",
                     help="timed loop only (no clock tail / profile / e2e / cpu legs): for ncu")
     return ap.parse_args()
 
 
 def peaks():
+    """HBM peak (the driver-measured copy bandwidth) and the compute peaks
+    measured on the box by tools/mma_probe.cu and tools/tc_probe.cu."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
-    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+        hbm, src = float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    else:
+        hbm, src = FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+    comp = {}
+    cp = os.path.join(ROOT, "profiles", "compute_peaks.json")
+    if os.path.exists(cp):
+        with open(cp) as f:
+            comp = json.load(f)
+    return hbm, src, comp
 
 
+def cpu_info():
+    """Host CPU model and physical core count (bench.cpp:177-180 binding label)."""
+    model, phys = "unknown", set()
+    try:
+        cur = {}
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if ":" not in line:
+                    if "physical id" in cur or "core id" in cur:
+                        phys.add((cur.get("physical id"), cur.get("core id")))
+                    cur = {}
+                    continue
+                k, v = [x.strip() for x in line.split(":", 1)]
+                cur[k] = v
+                if k == "model name":
+                    model = v
+        if cur:
+            phys.add((cur.get("physical id"), cur.get("core id")))
+    except OSError:
+        pass
+    logical = os.cpu_count() or 1
+    return {"cpu_model": model, "physical_cores": len(phys) or logical, "logical_cpus": logical}
+
+
+def schedule_config(w, args):
+    """The pinned SchedulerConfig both arms use (bench.cpp:135-150 with the
+    explicit budget): ct_size, p = 148 (one per SM), 1280 KB."""
+    return w.scheduler_config(num_workers=args.workers, ct_size=args.ct_size, cache_kb=args.cache_kb)
+
+
+def config_dict(args, w, cfg, tiles, fused_ratio, spill_rows=None):
+    """Config keys shared by both arms (same workload, same schedule)."""
+    return {"workload": f"{args.config}: {w.description}", "n": w.n, "nnz_a": w.a.nnz,
+            "b_cols": w.b_cols, "c_cols": w.c_cols, "flops_per_step": w.flops(),
+            "schedule": {**cfg.__dict__, "tiles": list(tiles), "fused_ratio": fused_ratio},
+            "bytes_min": w.bytes_min(),
+            "bytes_alg": w.bytes_alg(spill_rows) if spill_rows is not None else None,
+            "l2": f"flushed between timed steps ({args.flush_mib} MiB write, outside the events)"}
+
+
+# ---------------------------------------------------------------------------
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the run."""
@@ -122,12 +177,14 @@ def problem_bytes(w):
 def cpu_reference_time(w, args, workers, steps, warmup, budget_s=25.0):
     """Time the reference CPU executor (oracle/_ref, the unmodified reference
     compiled from its own sources) -- or the C port when _ref is absent --
-    on the host cores.  Returns (seconds list, kind, sample text, sched secs)."""
+    on the host cores, with the pinned SchedulerConfig (the same schedule
+    the GPU arm runs).  Returns (seconds list, kind, sample text, sched secs,
+    reference schedule)."""
     from oracle.oracle import (Oracle, RefProblem, Reference, SchedulerConfig as OCfg, have_reference,
                                ref_schedule_handle)
     from paper_2407_00243_b200 import Csr
 
-    cfg = w.scheduler_config(num_workers=workers, ct_size=args.ct_size, cache_kb=args.cache_kb)
+    cfg = schedule_config(w, args)
     ocfg = OCfg(**cfg.__dict__)
     a = (w.a.row_ptr, w.a.col_idx, w.a.values)
     b = (w.b.row_ptr, w.b.col_idx, w.b.values, w.b.n_cols) if isinstance(w.b, Csr) else w.b
@@ -150,8 +207,9 @@ def cpu_reference_time(w, args, workers, steps, warmup, budget_s=25.0):
                 break
         kind = "reference"
         what = (f"reference fused_{'gemm' if w.op == 'gemm-spmm' else 'spmm'}_spmm on the full "
-                f"{w.name} problem, workers={workers}, OMP_PROC_BIND=close; per-run steady_clock "
-                f"time includes the executor's own zeroed D1/D allocation (kernels.hpp:97-98)")
+                f"{w.name} problem, workers={workers}, OMP_PROC_BIND=close, schedule p={cfg.num_workers} "
+                f"(the GPU arm's); per-run steady_clock time includes the executor's own zeroed D1/D "
+                f"allocation (kernels.hpp:97-98)")
     else:
         orc = Oracle()
         t0 = time.perf_counter()
@@ -167,7 +225,15 @@ def cpu_reference_time(w, args, workers, steps, warmup, budget_s=25.0):
                 break
         kind = "port"
         what = f"C port (oracle/tf_oracle.c) fused executor on the full {w.name} problem, workers={workers}"
-    return times, kind, what, sched_s
+    return times, kind, what, sched_s, sched
+
+
+def _ref_tiles(sched):
+    return [int(len(sched.i_lo[0])), int(len(sched.i_lo[1]))]
+
+
+def _ref_fused_ratio(sched, n):
+    return float(len(sched.j_rows[0])) / (2.0 * n)
 
 
 def run_reference_arm(args, rank, world):
@@ -176,30 +242,219 @@ def run_reference_arm(args, rank, world):
     from paper_2407_00243_b200 import workloads as W
 
     w = W.make(args.config, scale=args.scale, device="cpu")
-    cores = os.cpu_count() or 1
-    times, kind, what, sched_s = cpu_reference_time(w, args, cores, args.steps, args.warmup,
-                                                    budget_s=240.0)
+    info = cpu_info()
+    cores = info["logical_cpus"]
+    times, kind, what, sched_s, sched = cpu_reference_time(w, args, cores, args.steps, args.warmup,
+                                                           budget_s=240.0)
     per = float(np.mean(times))
     value = w.flops() / per / 1e9
+    cfg = schedule_config(w, args)
+    config = config_dict(args, w, cfg, _ref_tiles(sched), _ref_fused_ratio(sched, w.n))
+    config["scheduler_seconds_cpu"] = sched_s
+    config["parallelism"] = f"host OpenMP, {cores} threads (rank 0 only)"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if w.dtype == np.float64 else "f32",
-            "data": "synthetic (seeded generator with the BASELINE config's shape and distributions)",
+            "data": "synthetic (seeded generator with the BASELINE config's shape and distributions; "
+                    "SuiteSparse corpus not available)",
             "impl": "reference",
-            "config": {"workload": f"{args.config}: {w.description}", "n": w.n, "nnz_a": w.a.nnz,
-                       "flops_per_step": w.flops(), "scheduler_seconds_cpu": sched_s},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "config": config,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, **info,
                              "sample": what + f"; {len(times)} timed runs after {args.warmup} warm-up"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
+def _timed(body, steps, warmup, stream, flush, dist=None, dev=None):
+    """W warm-ups, then exactly `steps` steps bracketed by CUDA events on
+    `stream`, the L2 flushed between steps outside the events; barrier +
+    synchronize on both sides; max over ranks.  Returns total ms."""
+    import torch
+
+    for _ in range(warmup):
+        flush.fill_(1.0)
+        body()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(float(k))
+        evs[k][0].record(stream)
+        body()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = float(sum(a.elapsed_time(b) for a, b in evs))
+    if dist:
+        t = torch.tensor([tot], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    return tot
+
+
+def _stage_profile(plan, out, stream, flush, reps=5):
+    stages = {}
+    for _ in range(reps):
+        flush.fill_(2.0)
+        for name, ms, by in plan.profile(out, stream):
+            stages.setdefault(name, []).append((ms, by))
+    return {k: (float(np.mean([m for m, _ in v])), int(v[0][1])) for k, v in stages.items()}
+
+
+def _traffic(config, stage):
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tp):
+        return None
+    rec = json.load(open(tp)).get(config, {}).get(stage)
+    return rec["dram_bytes"] if rec else None
+
+
+def compute_roofline(w, plan_kernels, step_ms, comp):
+    """The step's compute floor: dense GEMM FLOPs on the pipe the plan uses
+    (tcgen05 3xTF32: three TF32 MMAs per product; FP64 / FP32 FMA otherwise)
+    plus the SpMM FLOPs on the FP pipe (separately rounded mul + add: two
+    issues per product pair, i.e. half the FMA peak)."""
+    fp64 = np.dtype(w.dtype) == np.float64
+    fma = comp.get("dfma_tflops" if fp64 else "ffma_tflops")
+    if not fma:
+        return None
+    spmm = 2.0 * w.a.nnz * w.c_cols + (2.0 * w.b.nnz * w.c_cols if w.op == "spmm-spmm" else 0.0)
+    gemm = 2.0 * w.n * w.b_cols * w.c_cols if w.op == "gemm-spmm" else 0.0
+    t = spmm / (fma / 2 * 1e12)
+    pipe = f"{'FP64' if fp64 else 'FP32'} mul+add"
+    if gemm:
+        if "tcgen05" in plan_kernels.get("first_op", "") and comp.get("tcgen05_tf32_tflops"):
+            t += gemm / (comp["tcgen05_tf32_tflops"] / 3 * 1e12)
+            pipe += " + tcgen05 3xTF32 GEMM"
+        else:
+            t += gemm / (fma * 1e12)
+            pipe += f" + {'DFMA' if fp64 else 'FFMA'} GEMM"
+    return {"pipe": pipe, "floor_ms": t * 1e3, "frac": t * 1e3 / step_ms,
+            "peaks_tflops": {k: v for k, v in comp.items() if k.endswith("tflops")}}
+
+
+def measure_config(name, args, dev, stream, flush, steps=10, warmup=3):
+    """One BASELINE config on this GPU (summary entry of the bench line)."""
+    import torch
+
+    import paper_2407_00243_b200 as P
+    from paper_2407_00243_b200 import workloads as W
+
+    w = W.make(name)
+    cfg = schedule_config(w, args)
+    prob = P.DeviceProblem(w.a, w.b, w.c, w.dtype)
+    sched = P.build_schedule(prob.a, cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = P.Plan(prob, sched)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    out = torch.empty((w.n, w.c_cols), dtype=getattr(torch, w.dtype.name), device=dev)
+    tot = _timed(lambda: plan.execute(out, stream), steps, warmup, stream, flush)
+    ms = tot / steps
+    st = _stage_profile(plan, out, stream, flush, 3)
+    dom = max(st, key=lambda k: st[k][0])
+    hbm, _, comp = peaks()
+    step_bytes = sum(b for _, b in st.values())
+    tr = _traffic(name, dom)
+    kern = plan.kernels()
+    cr = compute_roofline(w, kern, ms, comp)
+    bytes_alg = w.bytes_alg(plan.spill_rows)
+    res = {"workload": w.description, "ms_per_step": ms, "gflops": w.flops() / (ms * 1e-3) / 1e9,
+           "stages_ms": {k: v[0] for k, v in st.items()}, "dominant_stage": dom,
+           "dominant_hbm_frac": st[dom][1] / (st[dom][0] * 1e-3) / 1e9 / hbm if st[dom][0] else None,
+           "step_hbm_frac": bytes_alg / (ms * 1e-3) / 1e9 / hbm,
+           "step_compute_frac": cr["frac"] if cr else None,
+           "dominant_dram_over_alg": (tr / st[dom][1]) if tr and st[dom][1] else None,
+           "kernels": kern, "fused_ratio": sched.fused_ratio(), "plan_seconds": plan_s,
+           "inspector_seconds_gpu": sched.inspect_seconds}
+    del plan, prob, sched, out
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
+def e2e_dropin(w, sched, steps, warmup):
+    """The reference-facing by-value call (fused_gemm_spmm / fused_spmm_spmm,
+    kernels.hpp:182-208) through the C-ABI tfg_run_host: host A, B, C in,
+    host D out; per call it uploads the operands, builds the executor plan,
+    runs it and downloads D.  Host operands are pinned once by the caller."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2407_00243_b200 as P
+    from paper_2407_00243_b200._lib import TfgProblem
+    from paper_2407_00243_b200.tilefuse import _dt_code, check, lib
+
+    def pin(x, dt):
+        t = torch.from_numpy(np.ascontiguousarray(x, dt))
+        return t.pin_memory()
+
+    dt = np.dtype(w.dtype)
+    keep = []
+    p = TfgProblem()
+    p.dtype = _dt_code(dt)
+    p.n = w.n
+    for name, arr, adt in (("d_a_row_ptr", w.a.row_ptr, np.int32), ("d_a_col_idx", w.a.col_idx, np.int32),
+                           ("d_a_val", w.a.values, dt)):
+        t = pin(arr, adt)
+        keep.append(t)
+        setattr(p, name, t.data_ptr())
+    p.a_nnz = w.a.nnz
+    if isinstance(w.b, P.Csr):
+        p.b_is_dense = 0
+        p.b_rows, p.b_cols = w.b.n_rows, w.b.n_cols
+        p.b_nnz = w.b.nnz
+        if w.b is w.a:
+            p.d_b_row_ptr, p.d_b_col_idx, p.d_b_val = p.d_a_row_ptr, p.d_a_col_idx, p.d_a_val
+        else:
+            for name, arr, adt in (("d_b_row_ptr", w.b.row_ptr, np.int32),
+                                   ("d_b_col_idx", w.b.col_idx, np.int32), ("d_b_val", w.b.values, dt)):
+                t = pin(arr, adt)
+                keep.append(t)
+                setattr(p, name, t.data_ptr())
+    else:
+        p.b_is_dense = 1
+        p.b_rows, p.b_cols = w.b.shape
+        t = pin(w.b, dt)
+        keep.append(t)
+        p.d_b_dense = t.data_ptr()
+    p.c_rows, p.c_cols = w.c.shape
+    t = pin(w.c, dt)
+    keep.append(t)
+    p.d_c = t.data_ptr()
+    hout = torch.empty((w.n, w.c_cols), dtype=getattr(torch, dt.name)).pin_memory()
+    h2d = sum(int(x.numel() * x.element_size()) for x in keep)
+    d2h = int(hout.numel() * hout.element_size())
+    times = []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        check(lib().tfg_run_host(C.byref(p), sched.handle, C.c_void_p(hout.data_ptr())))
+        if k >= warmup:
+            times.append(time.perf_counter() - t0)
+    ms = float(np.median(times)) * 1e3
+    return {"value": w.flops() / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
+            "path": ("drop-in by-value call per step: tfg_run_host (C-ABI behind "
+                     "tilefuse::fused_*_spmm, kernels.hpp:182-208) from pinned host A, B, C to host D; "
+                     "each call uploads the operands, allocates, builds the executor plan (schedule "
+                     "given, as the reference API takes it), executes and downloads D; host wall "
+                     "clock per call, median")}
+
+
 def run_ours(args, rank, world, dist):
     import torch
 
     import paper_2407_00243_b200 as P
+    from paper_2407_00243_b200 import report as R
     from paper_2407_00243_b200 import workloads as W
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
@@ -207,7 +462,7 @@ def run_ours(args, rank, world, dist):
     sampler = ClockSampler(dev.index if dev.index is not None else 0)
 
     w = W.make(args.config, scale=args.scale)
-    cfg = w.scheduler_config(num_workers=args.workers, ct_size=args.ct_size, cache_kb=args.cache_kb)
+    cfg = schedule_config(w, args)
     prob = P.DeviceProblem(w.a, w.b, w.c, w.dtype)
     torch.cuda.synchronize()
     sched = P.build_schedule(prob.a, cfg)  # GPU inspector, outside the timed region
@@ -216,7 +471,13 @@ def run_ours(args, rank, world, dist):
     out = torch.empty((w.n, w.c_cols), dtype=getattr(torch, w.dtype.name), device=dev)
     flush = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
-    plan = P.Plan(prob, sched) if rank == 0 else None
+    plan, plan_s = None, None
+    if rank == 0:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan = P.Plan(prob, sched)
+        torch.cuda.synchronize()
+        plan_s = time.perf_counter() - t0
     dplan, bounds, halo = None, None, None
     if world > 1:
         # row-block partition of the same global problem (strong scaling)
@@ -237,35 +498,7 @@ def run_ours(args, rank, world, dist):
         def step():
             plan.execute(out, stream)
 
-    def timed_loop(body, flush_between=True):
-        for _ in range(args.warmup):
-            if flush_between:
-                flush.fill_(1.0)
-            body()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        for k in range(args.steps):
-            if flush_between:
-                flush.fill_(float(k))
-            evs[k][0].record(stream)
-            body()
-            evs[k][1].record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        tot = float(sum(a.elapsed_time(b) for a, b in evs))
-        if dist:
-            t = torch.tensor([tot], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            tot = float(t.item())
-        return tot
-
-    total_ms = timed_loop(step)
+    total_ms = _timed(step, args.steps, args.warmup, stream, flush, dist, dev)
     mean_ms = total_ms / args.steps
     value = w.flops() * args.steps / (total_ms * 1e-3) / 1e9  # the global problem, all ranks
 
@@ -276,14 +509,11 @@ def run_ours(args, rank, world, dist):
                               "ms_per_step": mean_ms, "value": value}))
         return
 
-    # end to end: pinned host A,B,C -> HBM, execute, D -> pinned host, every step.
-    # Steps are pipelined over two device input/output buffer sets and three
-    # streams (H2D | compute | D2H), so step k+1's upload overlaps step k's
-    # download (PCIe is full duplex); every step still moves all its inputs
-    # and its result across PCIe inside the timed region.
-    e2e = None
+    # end to end (pipelined device-plan API): pinned host A,B,C -> HBM,
+    # execute, D -> pinned host, every step, two buffer sets and three streams
+    e2e_pipe = None
     if not args.no_e2e:
-        e2e = _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan)
+        e2e_pipe = _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan)
 
     if rank != 0:
         sampler.stop()
@@ -298,41 +528,84 @@ def run_ours(args, rank, world, dist):
     clocks = sampler.stop()
 
     # roofline of the dominant stage of the single-GPU plan (CUDA events per stage)
-    prof = []
-    for _ in range(5):
-        flush.fill_(2.0)
-        prof.append(plan.profile(out, stream))
-    stages = {}
-    for rec in prof:
-        for name, ms, by in rec:
-            stages.setdefault(name, []).append((ms, by))
-    stage_avg = {k: (float(np.mean([m for m, _ in v])), int(v[0][1])) for k, v in stages.items()}
+    stage_avg = _stage_profile(plan, out, stream, flush)
     dom = max(stage_avg, key=lambda k: stage_avg[k][0])
     dom_ms, dom_bytes = stage_avg[dom]
-    peak, peak_src = peaks()
+    peak, peak_src, comp = peaks()
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):  # committed ncu --set full capture of the same kernel
-        rec = json.load(open(tp)).get(args.config, {}).get(dom)
-        if rec:
-            traffic = rec["dram_bytes"]
+    traffic = _traffic(args.config, dom)
     step_bytes = sum(b for _, b in stage_avg.values())
     single_ms = sum(v[0] for v in stage_avg.values())
+    kern = plan.kernels()
+    cr = compute_roofline(w, kern, mean_ms, comp)
+    spill_rows = plan.spill_rows
+    bytes_alg = w.bytes_alg(spill_rows)
+    t_hbm = bytes_alg / (peak * 1e9) * 1e3
+
+    # the paper's own metric: GPU fused vs GPU unfused, scheduler amortisation
+    # (bench.cpp:244-316 run_rows; report rows as bench.cpp:460-513)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    uplan = P.Plan(prob, None)
+    torch.cuda.synchronize()
+    uplan_s = time.perf_counter() - t0
+    fused_med = R.median_seconds(lambda: plan.execute(out, stream), 7, 1)
+    unfused_med = R.median_seconds(lambda: uplan.execute(out, stream), 7, 1)
+    prec = "dp" if w.dtype == np.float64 else "sp"
+    rows = [R.Row(args.config, w.n, w.a.nnz, w.op, "fused", prec, w.b_cols, w.c_cols, cfg.num_workers,
+                  7, fused_med, w.flops() / fused_med / 1e9, sched.fused_ratio(), sched.inspect_seconds),
+            R.Row(args.config, w.n, w.a.nnz, w.op, "unfused", prec, w.b_cols, w.c_cols,
+                  cfg.num_workers, 7, unfused_med, w.flops() / unfused_med / 1e9)]
+    saved = unfused_med - fused_med
+    rows[0].runs_to_amortize = sched.inspect_seconds / saved if saved > 0 else float("inf")
+    report = json.loads(R.rows_to_json(rows))
+    report[0]["runs_to_amortize_incl_plan"] = ((sched.inspect_seconds + plan_s) / saved
+                                               if saved > 0 else "inf")
+    del uplan
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = e2e_dropin(w, sched, steps=3 if w.n > (1 << 21) else 5, warmup=1)
 
     cpu = None
+    info = cpu_info()
     if world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        times, kind, what, sched_s = cpu_reference_time(w, args, cores, 7, 1)
+        cores = info["logical_cpus"]
+        times, kind, what, sched_cpu_s, _ = cpu_reference_time(w, args, cores, 7, 1)
         med = float(np.median(times))
-        cpu = {"value": w.flops() / med / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+        cpu = {"value": w.flops() / med / 1e9, "unit": UNIT, "cores": cores, "kind": kind, **info,
                "sample": what + f"; median of {len(times)} runs after 1 warm-up",
-               "ms_per_run": med * 1e3, "scheduler_seconds": sched_s}
+               "ms_per_run": med * 1e3, "scheduler_seconds": sched_cpu_s}
+
+    summary = None
+    if world == 1 and not args.no_summary and args.scale == 1.0:
+        del prob, plan
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        summary = {}
+        for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+            if name != args.config:
+                summary[name] = measure_config(name, args, dev, stream, flush)
 
     parallelism = "single GPU"
     if world > 1:
         parallelism = (f"row-block partition x{world} at tile boundaries; D1 halo via one NCCL "
                        f"all_to_all per step (rank-0 halo rows {dplan.halo_rows})")
+    config = config_dict(args, w, cfg, sched.num_tiles_per_wave, sched.fused_ratio(), spill_rows)
+    config["schedule"].update({"tile_size": sched.tile_size,
+                               "inspector_seconds_gpu": sched.inspect_seconds,
+                               "inspector_seconds_gpu_cold": inspect_cold})
+    config.update({
+        "plan_seconds": plan_s, "plan_seconds_unfused": uplan_s,
+        "spill_rows": spill_rows, "bytes_alg_stages": step_bytes,
+        "step_hbm_frac_of_peak": (step_bytes / (single_ms * 1e-3) / 1e9) / peak,
+        "step_roofline": {"t_hbm_ms": t_hbm, "t_compute_ms": cr["floor_ms"] if cr else None,
+                          "bound": "hbm" if not cr or t_hbm >= cr["floor_ms"] else "compute",
+                          "frac": max(t_hbm, cr["floor_ms"] if cr else 0.0) / mean_ms},
+        "stages_ms": {k: v[0] for k, v in stage_avg.items()},
+        "kernels": kern, "parallelism": parallelism,
+        "report_rows": report,
+        "configs": summary})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
@@ -340,27 +613,16 @@ def run_ours(args, rank, world, dist):
         "dtype": "f64" if w.dtype == np.float64 else "f32",
         "data": "synthetic (seeded generator with the BASELINE config's shape and distributions; "
                 "SuiteSparse corpus not available)",
-        "config": {
-            "workload": f"{args.config}: {w.description}", "n": w.n, "nnz_a": w.a.nnz,
-            "b_cols": w.b_cols, "c_cols": w.c_cols, "flops_per_step": w.flops(),
-            "schedule": {**cfg.__dict__, "tile_size": sched.tile_size,
-                         "tiles": list(sched.num_tiles_per_wave),
-                         "fused_ratio": sched.fused_ratio(),
-                         "inspector_seconds_gpu": sched.inspect_seconds,
-                         "inspector_seconds_gpu_cold": inspect_cold},
-            "spill_rows": plan.spill_rows, "bytes_min": w.bytes_min(),
-            "bytes_alg": w.bytes_alg(plan.spill_rows), "bytes_alg_stages": step_bytes,
-            "step_hbm_frac_of_peak": (step_bytes / (single_ms * 1e-3) / 1e9) / peak,
-            "stages_ms": {k: v[0] for k, v in stage_avg.items()},
-            "kernels": plan.kernels(),
-            "l2": f"flushed between timed steps ({args.flush_mib} MiB write, outside the events)",
-            "parallelism": parallelism},
+        "config": config,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
-                     "peak_source": peak_src},
+                     "traffic_over_algorithmic": traffic / dom_bytes if traffic and dom_bytes else None,
+                     "peak_source": peak_src,
+                     "compute": cr},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_pipelined": e2e_pipe,
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
     }

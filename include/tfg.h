@@ -169,6 +169,19 @@ typedef struct {
 tfg_status tfg_plan_create(const tfg_problem *p, const tfg_schedule *s,
                            void *stream, tfg_plan **out);
 
+/* Plan options (tfg_plan_create_ex).  Default: every SpMM term of a
+ * grid-stencil row is one fused multiply-add (results within the north-star
+ * tolerance of the reference, 1e-12 / 1e-5 max-norm).  REFERENCE_BITS: the
+ * reference's separately rounded multiply and add in the same ascending
+ * order (kernels.hpp:75-79), so SpMM results are bit-identical to it. */
+#define TFG_PLAN_REFERENCE_BITS 1u
+
+/* tfg_plan_create with options; row_lo = 0, row_hi = -1 is the whole
+ * problem, a row block is a multi-GPU partition (tfg_plan_create_partition).
+ * Device operands must be 16-byte aligned (cudaMalloc guarantees 256). */
+tfg_status tfg_plan_create_ex(const tfg_problem *p, const tfg_schedule *s, uint32_t flags,
+                              int32_t row_lo, int32_t row_hi, void *stream, tfg_plan **out);
+
 /* Multi-GPU row-block partition: the plan of the rank owning
  * rows [row_lo, row_hi).  It runs the wavefront-0 tiles whose i_lo lies in
  * the block (the caller cuts at tile boundaries, so fused rows need no

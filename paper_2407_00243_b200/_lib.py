@@ -35,6 +35,9 @@ class TfgConfig(C.Structure):
     ]
 
 
+PLAN_REFERENCE_BITS = 1  # tfg.h TFG_PLAN_REFERENCE_BITS
+
+
 class TfgProblem(C.Structure):
     """tfg_problem == FusedProblem<T> (kernels.hpp:16-43) as pointers."""
 
@@ -81,6 +84,8 @@ SIGNATURES = [
                                         C.c_size_t]),
     ("tfg_plan_create", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
+    ("tfg_plan_create_ex", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_uint32, C.c_int32,
+                                     C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tfg_plan_create_partition", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_int32,
                                             C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tfg_plan_d1", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),

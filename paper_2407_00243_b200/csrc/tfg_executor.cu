@@ -27,6 +27,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <memory>
 #include <cstring>
@@ -148,107 +149,6 @@ __global__ void __launch_bounds__(256, MINB)
   }
 }
 
-// ---- row-group union SpMM ----------------------------------------------------
-// A warp owns a group of up to R rows of the row list.  The plan merged the
-// rows' column lists into one ascending list U of distinct columns, each with
-// a mask of the group rows that use it.  The warp walks U in order, gathers
-// every distinct X row ONCE (UNR gathers in flight) and adds it into the
-// accumulators of the rows in its mask, reading each row's values from the
-// unmodified CSR through a per-row running pointer.  Every row therefore
-// still sums its terms in ascending column order with separately rounded mul
-// and add (kernels.hpp:75-79: bit-identical to the reference), while the X
-// bytes pulled through L1 drop by the group's column sharing (about 2.4x for
-// a 9-point stencil at R = 8).
-template <class T, int VEC, int NCH, int R, int UNR, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-    k_spmm_group(int64_t ngroups, const int* __restrict__ g_rows,
-                 const int64_t* __restrict__ g_uoff, const int64_t* __restrict__ g_poff,
-                 const int* __restrict__ ucol, const uint8_t* __restrict__ umask,
-                 const T* __restrict__ gval, const T* __restrict__ X, int ldx,
-                 T* __restrict__ out, int ldo) {
-  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (g >= ngroups) return;
-  const int lane = threadIdx.x & 31;
-  const int my_row = lane < R ? __ldg(g_rows + g * R + lane) : -1;
-  T acc[R][NCH][VEC];
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[r][ch][v] = T(0);
-  const int64_t ub = g_uoff[g], ue = g_uoff[g + 1];
-  // value stream: pairs (u, row) in order; lane l holds pair pc0 + l
-  const int64_t pe = g_poff[g + 1];
-  int64_t pc0 = g_poff[g];
-  int pi = 0;  // index of the next pair within the current 32-value chunk
-  T vcur = pc0 + lane < pe ? __ldg(gval + pc0 + lane) : T(0);
-  T vnext = pc0 + 32 + lane < pe ? __ldg(gval + pc0 + 32 + lane) : T(0);
-  for (int64_t u0 = ub; u0 < ue; u0 += 32) {
-    int c = 0, m = 0;
-    if (u0 + lane < ue) {
-      c = __ldg(ucol + u0 + lane);
-      m = __ldg(umask + u0 + lane);
-    }
-    const int cnt = (int)min((int64_t)32, ue - u0);
-    for (int q0 = 0; q0 < cnt; q0 += UNR) {
-      int cu[UNR], mu[UNR];
-      T x[UNR][NCH][VEC];
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        cu[q] = __shfl_sync(0xffffffffu, c, (q0 + q) & 31);
-        mu[q] = q0 + q < cnt ? __shfl_sync(0xffffffffu, m, (q0 + q) & 31) : 0;
-      }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q)
-        if (mu[q]) {
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch)
-            ldv<T, VEC>(x[q][ch], X + (size_t)cu[q] * ldx + (ch * 32 + lane) * VEC);
-        }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (mu[q] & (1 << r)) {
-            const T a = __shfl_sync(0xffffffffu, vcur, pi);
-            if (++pi == 32) {
-              pi = 0;
-              pc0 += 32;
-              vcur = vnext;
-              vnext = pc0 + 32 + lane < pe ? __ldg(gval + pc0 + 32 + lane) : T(0);
-            }
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-              for (int v = 0; v < VEC; ++v)
-                acc[r][ch][v] = fops<T>::add(acc[r][ch][v], fops<T>::mul(a, x[q][ch][v]));
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int row = __shfl_sync(0xffffffffu, my_row, r);
-    if (row >= 0) {
-      T* o = out + (size_t)row * ldo;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * 32 + lane) * VEC, acc[r][ch]);
-    }
-  }
-}
-
-// gval[p] = av[gperm[p]]: refresh the group-ordered value stream from the
-// live CSR values (first kernel of every execution that uses groups).
-template <class T>
-__global__ void k_permute_values(int64_t np, const int* __restrict__ perm,
-                                 const T* __restrict__ av, T* __restrict__ gval) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
-       p += (int64_t)gridDim.x * blockDim.x)
-    gval[p] = __ldg(av + __ldg(perm + p));
-}
-
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
@@ -298,6 +198,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// the CTA's cp.async copies issued so far arrive on the barrier when complete
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 template <int BYTES>
 __device__ __forceinline__ void cp_async_small(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
@@ -314,268 +226,6 @@ struct DiaLines {
 constexpr int kBandMG = 4;  // rows per register-reuse mini-group
 constexpr size_t kBandSmemMax = 200 * 1024;
 
-template <class T, int VEC, int LPR, int NCH>
-__global__ void __launch_bounds__(256, 1)
-    k_spmm_band(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
-                const T* __restrict__ av, const int* __restrict__ run_begin,
-                const int* __restrict__ run_start, const int* __restrict__ run_len,
-                const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
-                int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
-                T* __restrict__ out, int ldo) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int cc = ldx;
-  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
-  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
-  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
-  const size_t bufbytes = xbytes + ibytes + vbytes;
-  __shared__ __align__(8) uint64_t mbar[2];
-  const int tid = threadIdx.x;
-  const int gl = tid & (LPR - 1);
-  const unsigned gmask = group_mask(LPR);
-  const int group = tid / LPR, ngroups = blockDim.x / LPR;
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  auto issue = [&](int b, int buf) {
-    unsigned char* base = smem_raw + (size_t)buf * bufbytes;
-    T* xs = reinterpret_cast<T*>(base);
-    uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
-    T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
-    const int r_lo = row0 + b * R;
-    const int r_hi = min(r_lo + R, row0 + nrows);
-    const int k0 = __ldg(rp + r_lo), k1 = __ldg(rp + r_hi);
-    if (tid == 0) {
-      const int rb = run_begin[b], re = run_begin[b + 1];
-      const int64_t i0 = idx_off[b], i1 = idx_off[b + 1];
-      unsigned total = (unsigned)((i1 - i0) * 2);
-      for (int q = rb; q < re; ++q) total += (unsigned)run_len[q] * cc * sizeof(T);
-      mbar_expect_tx(&mbar[buf], total);
-      int off = 0;
-      for (int q = rb; q < re; ++q) {
-        const int len = run_len[q];
-        const char* src = reinterpret_cast<const char*>(X + (size_t)run_start[q] * cc);
-        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
-        size_t left = (size_t)len * cc * sizeof(T);
-        while (left) {
-          const unsigned chunk = (unsigned)min(left, (size_t)32768);
-          bulk_g2s(dst, src, chunk, &mbar[buf]);
-          dst += chunk;
-          src += chunk;
-          left -= chunk;
-        }
-        off += len;
-      }
-      if (i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &mbar[buf]);
-    }
-    for (int k = k0 + tid; k < k1; k += blockDim.x) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
-    cp_async_commit();
-  };
-
-  int it = 0;
-  int b = blockIdx.x;
-  if (b < nblk) issue(b, 0);
-  for (; b < nblk; b += gridDim.x, ++it) {
-    const int buf = it & 1;
-    const int bn = b + gridDim.x;
-    if (bn < nblk)
-      issue(bn, buf ^ 1);
-    else
-      cp_async_commit();
-    mbar_wait(&mbar[buf], (unsigned)((it >> 1) & 1));
-    cp_async_wait<1>();
-    __syncthreads();
-    unsigned char* base = smem_raw + (size_t)buf * bufbytes;
-    const T* xs = reinterpret_cast<const T*>(base);
-    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
-    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
-    const int r_lo = row0 + b * R;
-    const int nr = min(R, row0 + nrows - r_lo);
-    const uint16_t* lrp = is;          // nr + 1 local offsets
-    const uint16_t* lsl = is + nr + 1; // slots
-    for (int r = group; r < nr; r += ngroups) {
-      const int eb = lrp[r], ee = lrp[r + 1];
-      T acc[NCH][VEC];
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-      for (int e0 = eb; e0 < ee; e0 += LPR) {
-        int sl = 0;
-        T a = T(0);
-        if (e0 + gl < ee) {
-          sl = lsl[e0 + gl];
-          a = vs[e0 + gl];
-        }
-        const int cnt = min(LPR, ee - e0);
-        for (int u = 0; u < cnt; ++u) {
-          const int su = __shfl_sync(gmask, sl, u, LPR);
-          const T au = __shfl_sync(gmask, a, u, LPR);
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            T x[VEC];
-            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v)
-              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
-          }
-        }
-      }
-      T* o = out + (size_t)(r_lo + r) * ldo;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-}
-
-// Warp-specialised band SpMM: warp 8 is the producer (one lane issues the
-// TMA bulk copies of a block's X-row runs and index record, all lanes copy
-// the block's live CSR values into the stage), warps 0-7 consume.  Stages
-// form a ring guarded by full/empty mbarriers, so consumers never meet a
-// CTA-wide barrier and up to STAGES blocks are in flight per CTA.
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-template <class T, int VEC, int LPR, int NCH, int STAGES>
-__global__ void __launch_bounds__(288, 1)
-    k_spmm_band2(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
-                 const T* __restrict__ av, const int* __restrict__ run_begin,
-                 const int* __restrict__ run_start, const int* __restrict__ run_len,
-                 const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
-                 int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
-                 T* __restrict__ out, int ldo, const DiaLines* __restrict__ = nullptr) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  const int cc = ldx;
-  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
-  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
-  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
-  const size_t bufbytes = xbytes + ibytes + vbytes;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NCONS = 8;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == NCONS) {
-    // ---------------- producer ----------------
-    int it = 0;
-    for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
-      unsigned char* base = smem_raw + (size_t)s * bufbytes;
-      T* xs = reinterpret_cast<T*>(base);
-      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
-      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
-      const int r_lo = row0 + b * R;
-      const int r_hi = min(r_lo + R, row0 + nrows);
-      const int k0 = __ldg(rp + r_lo), k1 = __ldg(rp + r_hi);
-      for (int k = k0 + lane; k < k1; k += 32) vs[k - k0] = __ldg(av + k);
-      __syncwarp();
-      if (lane == 0) {
-        const int rb = run_begin[b], re = run_begin[b + 1];
-        const int64_t i0 = idx_off[b], i1 = idx_off[b + 1];
-        unsigned total = (unsigned)((i1 - i0) * 2);
-        for (int q = rb; q < re; ++q) total += (unsigned)run_len[q] * cc * sizeof(T);
-        mbar_arrive_expect_tx(&full[s], total);  // also publishes the value stores
-        int off = 0;
-        for (int q = rb; q < re; ++q) {
-          const int len = run_len[q];
-          const char* src = reinterpret_cast<const char*>(X + (size_t)run_start[q] * cc);
-          char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
-          size_t left = (size_t)len * cc * sizeof(T);
-          while (left) {
-            const unsigned chunk = (unsigned)min(left, (size_t)32768);
-            bulk_g2s(dst, src, chunk, &full[s]);
-            dst += chunk;
-            src += chunk;
-            left -= chunk;
-          }
-          off += len;
-        }
-        if (i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &full[s]);
-      }
-    }
-    return;
-  }
-  // ---------------- consumers ----------------
-  const int gl = threadIdx.x & (LPR - 1);
-  const unsigned gmask = group_mask(LPR);
-  const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
-  int it = 0;
-  for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++it) {
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
-    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
-    const T* xs = reinterpret_cast<const T*>(base);
-    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
-    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
-    const int r_lo = row0 + b * R;
-    const int nr = min(R, row0 + nrows - r_lo);
-    const uint16_t* lrp = is;
-    const uint16_t* lsl = is + nr + 1;
-    for (int r = group; r < nr; r += ngroups) {
-      const int eb = lrp[r], ee = lrp[r + 1];
-      T acc[NCH][VEC];
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-      for (int e0 = eb; e0 < ee; e0 += LPR) {
-        int sl = 0;
-        T a = T(0);
-        if (e0 + gl < ee) {
-          sl = lsl[e0 + gl];
-          a = vs[e0 + gl];
-        }
-        const int cnt = min(LPR, ee - e0);
-#pragma unroll 4
-        for (int u = 0; u < cnt; ++u) {
-          const int su = __shfl_sync(gmask, sl, u, LPR);
-          const T au = __shfl_sync(gmask, a, u, LPR);
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            T x[VEC];
-            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v)
-              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
-          }
-        }
-      }
-      T* o = out + (size_t)(r_lo + r) * ldo;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-// Band SpMM v3: warp-specialised like v2, but the producer never blocks on
-// data: values are cp.async'ed and tracked by the stage's mbarrier
-// (cp.async.mbarrier.arrive), block metadata is prefetched lane-parallel for
-// 32 blocks at a time, each run's TMA bulk copy is issued by its own lane.
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// DIA (stencil) consumer: a warp takes a mini-group of 4 consecutive rows.
 // For a regular mini-group (every row has the global diagonal set) each
 // diagonal line's X rows are loaded once into a sliding register window and
 // applied to all 4 rows: row q, diagonal d of a line reads window slot q + d.
@@ -852,557 +502,6 @@ __global__ void __launch_bounds__(288, (DIA && NCH == 1) ? 2 : 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-}
-
-// ---- dependency-driven band sweep (SpMM-SpMM without fused tiles) ----------
-// The first op (D1 = B C) and wavefront 1 (D = A D1) as ONE persistent band
-// kernel over a single item list: first-op blocks in row order, each
-// wavefront-1 block placed after the first-op blocks that produce the D1 rows
-// it reads (plus a lag of two grid rounds).  First-op blocks are grouped in
-// chunks of C (C sized so any block's D1 row range spans <= 32 chunks);
-// consumers bump their chunk's counter once per warp after their D1 stores
-// are fenced.  The producer of a wavefront-1 block checks the chunks of its
-// D1 row range lane-parallel -- loads issued one item ahead, so the check is
-// off the critical path -- before its TMA copies of those rows, so D1
-// is read back from L2 while it is still resident instead of from HBM.  The
-// wavefront barrier of the reference (kernels.hpp:118-119) is relaxed to the
-// exact per-row dependencies; every D1 and D row is computed by the same
-// code and order as in the two-pass execution (bit-identical).  Items are
-// taken round-robin in list order by co-resident CTAs and dependencies only
-// point to earlier items, so every wait is on an item some CTA is already
-// processing.
-template <class T>
-struct BandSide {
-  int R, row0, nrows;
-  const int* rp;
-  const T* av;
-  const int* run_begin;
-  const int* run_start;
-  const int* run_len;
-  const int64_t* idx_off;
-  const uint16_t* lidx;
-  const T* X;
-  T* out;
-};
-
-__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p));
-  return v;
-}
-
-template <class T, int VEC, int LPR, int NCH, int STAGES, bool DIA = false>
-__global__ void __launch_bounds__(288, (DIA && NCH == 1) ? 2 : 1)
-    k_spmm_band_sweep(int nitems, const int* __restrict__ items, const int2* __restrict__ dep,
-                      int* chunk_done, int chunk_shift, int epoch, BandSide<T> s0,
-                      BandSide<T> s1, int stage_cap, int idx_cap, int val_cap, int cc,
-                      int dbg, const DiaLines* __restrict__ dl0p = nullptr,
-                      const DiaLines* __restrict__ dl1p = nullptr) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
-  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
-  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
-  const size_t bufbytes = xbytes + ibytes + vbytes;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NCONS = 8;
-  constexpr int kOpShift = 30;
-  constexpr int kBlkMask = (1 << kOpShift) - 1;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  const int G = gridDim.x;
-  const int nmine = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / G + 1 : 0;
-  if (warp == NCONS) {
-    // ---------------- producer ----------------
-    int m_k0 = 0, m_k1 = 0, m_rb = 0, m_re = 0, m_op = 0, m_b = 0;
-    int64_t m_i0 = 0, m_i1 = 0;
-    auto load_meta = [&](int base) {
-      const int itl = base + lane;
-      if (itl < nmine) {
-        const int code = __ldg(items + blockIdx.x + itl * G);
-        const int op = code >> kOpShift, b = code & kBlkMask;
-        const int R = op ? s1.R : s0.R, row0 = op ? s1.row0 : s0.row0;
-        const int nrows = op ? s1.nrows : s0.nrows;
-        const int* rp = op ? s1.rp : s0.rp;
-        const int* rbp = op ? s1.run_begin : s0.run_begin;
-        const int64_t* io = op ? s1.idx_off : s0.idx_off;
-        const int r_lo = row0 + b * R;
-        const int r_hi = min(r_lo + R, row0 + nrows);
-        m_k0 = __ldg(rp + r_lo);
-        m_k1 = __ldg(rp + r_hi);
-        m_rb = __ldg(rbp + b);
-        m_re = __ldg(rbp + b + 1);
-        m_i0 = __ldg(io + b);
-        m_i1 = __ldg(io + b + 1);
-        m_op = op;
-        m_b = b;
-      }
-    };
-    load_meta(0);
-    auto load_runs = [&](int it, int& rs, int& rl) {
-      const int rb = __shfl_sync(0xffffffffu, m_rb, it & 31);
-      const int re = __shfl_sync(0xffffffffu, m_re, it & 31);
-      const int op = __shfl_sync(0xffffffffu, m_op, it & 31);
-      rs = 0;
-      rl = 0;
-      if (rb + lane < re) {
-        rs = __ldg((op ? s1.run_start : s0.run_start) + rb + lane);
-        rl = __ldg((op ? s1.run_len : s0.run_len) + rb + lane);
-      }
-    };
-    int rs = 0, rl = 0;
-    if (nmine > 0) load_runs(0, rs, rl);
-    const int nb0 = s0.nrows > 0 ? (s0.nrows + s0.R - 1) / s0.R : 0;
-    // chunk c is complete when all its blocks' 8 consumer warps published
-    auto chunk_target = [&](int c) {
-      return 8 * epoch * min(1 << chunk_shift, nb0 - (c << chunk_shift));
-    };
-    // lane q: chunk (lo_chunk + q) of the item's range and its counter value
-    int pc = -1, pv = 0;
-    auto prefetch_deps = [&](int it2) {
-      pc = -1;
-      if (it2 >= nmine) return;
-      const int code = __ldg(items + blockIdx.x + it2 * G);
-      if (!(code >> kOpShift)) return;
-      const int2 d = __ldg(dep + (code & kBlkMask));
-      if (d.y < d.x) return;
-      const int c0 = d.x >> chunk_shift, c1 = d.y >> chunk_shift;
-      if (c0 + lane <= c1) {
-        pc = c0 + lane;
-        pv = ld_relaxed_gpu(chunk_done + pc);
-      }
-    };
-    prefetch_deps(0);
-    for (int it = 0; it < nmine; ++it) {
-      const int s = it % STAGES;
-      const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
-      const int k1 = __shfl_sync(0xffffffffu, m_k1, it & 31);
-      const int64_t i0 = __shfl_sync(0xffffffffu, m_i0, it & 31);
-      const int64_t i1 = __shfl_sync(0xffffffffu, m_i1, it & 31);
-      const int op = __shfl_sync(0xffffffffu, m_op, it & 31);
-      const int b = __shfl_sync(0xffffffffu, m_b, it & 31);
-      int off = rl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, off, o);
-        if (lane >= o) off += y;
-      }
-      const int total_rows = __shfl_sync(0xffffffffu, off, 31);
-      off -= rl;
-      const int my_rs = rs, my_rl = rl;
-      if (it + 1 < nmine) {
-        if (((it + 1) & 31) == 0) load_meta(it + 1);
-        load_runs(it + 1, rs, rl);
-      }
-      if (op && !(dbg & 1)) {  // wavefront-1 block: wait for the first-op chunks it reads
-        if (pc >= 0) {
-          const int tgt = chunk_target(pc);
-          while (pv < tgt) {
-            __nanosleep(64);
-            pv = ld_relaxed_gpu(chunk_done + pc);
-          }
-        }
-        __syncwarp();
-        // acquire the publishers' D1 stores, then order them before the TMA
-        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      }
-      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
-      unsigned char* base = smem_raw + (size_t)s * bufbytes;
-      T* xs = reinterpret_cast<T*>(base);
-      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
-      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
-      const T* av = op ? s1.av : s0.av;
-      for (int k = k0 + lane; k < k1; k += 32) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
-      cp_async_mbar_arrive(&full[s]);
-      __syncwarp();
-      if (lane == 0)
-        mbar_arrive_expect_tx(&full[s], (unsigned)((size_t)total_rows * cc * sizeof(T) +
-                                                   (size_t)(i1 - i0) * 2));
-      __syncwarp();
-      if (my_rl > 0) {
-        const T* X = op ? s1.X : s0.X;
-        const char* src = reinterpret_cast<const char*>(X + (size_t)my_rs * cc);
-        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
-        size_t left = (size_t)my_rl * cc * sizeof(T);
-        while (left) {
-          const unsigned chunk = (unsigned)min(left, (size_t)32768);
-          bulk_g2s(dst, src, chunk, &full[s]);
-          dst += chunk;
-          src += chunk;
-          left -= chunk;
-        }
-      }
-      if (lane == 0 && i1 > i0)
-        bulk_g2s(is, (op ? s1.lidx : s0.lidx) + i0, (unsigned)((i1 - i0) * 2), &full[s]);
-      prefetch_deps(it + 1);  // dependency loads of the next item in flight now
-    }
-    cp_async_wait<0>();
-    return;
-  }
-  // ---------------- consumers ----------------
-  const int gl = threadIdx.x & (LPR - 1);
-  const unsigned gmask = group_mask(LPR);
-  const int group = threadIdx.x / LPR, ngroups = (NCONS * 32) / LPR;
-  __shared__ DiaLines dl_s[2];
-  if constexpr (DIA) {
-    if (threadIdx.x == 0) {
-      dl_s[0] = *dl0p;
-      dl_s[1] = *dl1p;
-    }
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");  // consumer warps only
-  }
-  for (int it = 0; it < nmine; ++it) {
-    const int code = __ldg(items + blockIdx.x + it * G);
-    const int op = code >> kOpShift, b = code & kBlkMask;
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
-    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
-    const T* xs = reinterpret_cast<const T*>(base);
-    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
-    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
-    const int R = op ? s1.R : s0.R, row0 = op ? s1.row0 : s0.row0;
-    const int nrows = op ? s1.nrows : s0.nrows;
-    T* out = op ? s1.out : s0.out;
-    const int r_lo = row0 + b * R;
-    const int nr = min(R, row0 + nrows - r_lo);
-    const uint16_t* lrp = is;
-    const uint16_t* lsl = is + nr + 1;
-    if constexpr (DIA) {
-      band_block_dia<T, VEC, NCH, NCONS>(xs, vs, lrp, lsl, cc, nr, dl_s[op], warp, gl,
-                                         out + (size_t)r_lo * cc, cc);
-    } else
-    for (int r = group; r < nr; r += ngroups) {
-      const int eb = lrp[r], ee = lrp[r + 1];
-      T acc[NCH][VEC];
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-      for (int e0 = eb; e0 < ee; e0 += LPR) {
-        const int sl = e0 + gl < ee ? lsl[e0 + gl] : 0;
-        const int cnt = min(LPR, ee - e0);
-#pragma unroll 4
-        for (int u = 0; u < cnt; ++u) {
-          const int su = __shfl_sync(gmask, sl, u, LPR);
-          const T au = vs[e0 + u];
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            T x[VEC];
-            ldv<T, VEC>(x, xs + (size_t)su * cc + (ch * LPR + gl) * VEC);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v)
-              acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
-          }
-        }
-      }
-      T* o = out + (size_t)(r_lo + r) * cc;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
-    }
-    if (op == 0 && !(dbg & 2)) {  // publish: this warp's D1 rows are globally visible
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(chunk_done + (b >> chunk_shift), 1);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-template <class T, int VEC, int LPR, int NCH, int STAGES>
-__global__ void __launch_bounds__(288, 1)
-    k_spmm_band4(int nblk, int R, int row0, int nrows, const int* __restrict__ rp,
-                 const T* __restrict__ av, const int* __restrict__ run_begin,
-                 const int* __restrict__ run_start, const int* __restrict__ run_len,
-                 const int64_t* __restrict__ idx_off, const uint16_t* __restrict__ lidx,
-                 int stage_cap, int idx_cap, int val_cap, const T* __restrict__ X, int ldx,
-                 T* __restrict__ out, int ldo, const DiaLines* __restrict__ = nullptr) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  const int cc = ldx;
-  const size_t xbytes = (size_t)stage_cap * cc * sizeof(T);
-  const size_t ibytes = ((size_t)idx_cap * 2 + 15) / 16 * 16;
-  const size_t vbytes = ((size_t)val_cap * sizeof(T) + 15) / 16 * 16;
-  const size_t bufbytes = xbytes + ibytes + vbytes;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NCONS = 8;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  const int G = gridDim.x;
-  const int nmine = blockIdx.x < nblk ? (nblk - 1 - blockIdx.x) / G + 1 : 0;
-  if (warp == NCONS) {
-    // ---------------- producer ----------------
-    int m_k0 = 0, m_k1 = 0, m_rb = 0, m_re = 0;
-    int64_t m_i0 = 0, m_i1 = 0;
-    auto load_meta = [&](int base) {
-      const int itl = base + lane;
-      if (itl < nmine) {
-        const int b = blockIdx.x + itl * G;
-        const int r_lo = row0 + b * R;
-        const int r_hi = min(r_lo + R, row0 + nrows);
-        m_k0 = __ldg(rp + r_lo);
-        m_k1 = __ldg(rp + r_hi);
-        m_rb = __ldg(run_begin + b);
-        m_re = __ldg(run_begin + b + 1);
-        m_i0 = __ldg(idx_off + b);
-        m_i1 = __ldg(idx_off + b + 1);
-      }
-    };
-    load_meta(0);
-    // runs of the current block: lane q holds run q
-    auto load_runs = [&](int it, int& rs, int& rl) {
-      const int rb = __shfl_sync(0xffffffffu, m_rb, it & 31);
-      const int re = __shfl_sync(0xffffffffu, m_re, it & 31);
-      rs = 0;
-      rl = 0;
-      if (rb + lane < re) {
-        rs = __ldg(run_start + rb + lane);
-        rl = __ldg(run_len + rb + lane);
-      }
-    };
-    int rs = 0, rl = 0;
-    if (nmine > 0) load_runs(0, rs, rl);
-    for (int it = 0; it < nmine; ++it) {
-      const int s = it % STAGES;
-      const int k0 = __shfl_sync(0xffffffffu, m_k0, it & 31);
-      const int k1 = __shfl_sync(0xffffffffu, m_k1, it & 31);
-      const int64_t i0 = __shfl_sync(0xffffffffu, m_i0, it & 31);
-      const int64_t i1 = __shfl_sync(0xffffffffu, m_i1, it & 31);
-      // offsets of this block's runs in the stage (exclusive warp scan)
-      int off = rl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, off, o);
-        if (lane >= o) off += y;
-      }
-      const int total_rows = __shfl_sync(0xffffffffu, off, 31);
-      off -= rl;
-      const int my_rs = rs, my_rl = rl;
-      // prefetch the next block's metadata / runs while this one is issued
-      if (it + 1 < nmine) {
-        if (((it + 1) & 31) == 0) load_meta(it + 1);
-        load_runs(it + 1, rs, rl);
-      }
-      mbar_wait(&empty[s], (unsigned)(((it / STAGES) & 1) ^ 1));
-      unsigned char* base = smem_raw + (size_t)s * bufbytes;
-      T* xs = reinterpret_cast<T*>(base);
-      uint16_t* is = reinterpret_cast<uint16_t*>(base + xbytes);
-      T* vs = reinterpret_cast<T*>(base + xbytes + ibytes);
-      for (int k = k0 + lane; k < k1; k += 32) cp_async_small<sizeof(T)>(vs + (k - k0), av + k);
-      cp_async_mbar_arrive(&full[s]);
-      __syncwarp();
-      if (lane == 0)
-        mbar_arrive_expect_tx(&full[s], (unsigned)((size_t)total_rows * cc * sizeof(T) +
-                                                   (size_t)(i1 - i0) * 2));
-      __syncwarp();
-      if (my_rl > 0) {
-        const char* src = reinterpret_cast<const char*>(X + (size_t)my_rs * cc);
-        char* dst = reinterpret_cast<char*>(xs + (size_t)off * cc);
-        size_t left = (size_t)my_rl * cc * sizeof(T);
-        while (left) {
-          const unsigned chunk = (unsigned)min(left, (size_t)32768);
-          bulk_g2s(dst, src, chunk, &full[s]);
-          dst += chunk;
-          src += chunk;
-          left -= chunk;
-        }
-      }
-      if (lane == 0 && i1 > i0) bulk_g2s(is, lidx + i0, (unsigned)((i1 - i0) * 2), &full[s]);
-    }
-    cp_async_wait<0>();
-    return;
-  }
-  // ---------------- consumers: mini-groups of kBandMG rows -----------------
-  // Each warp takes a mini-group of consecutive rows and walks the group's
-  // ascending union of stage slots: every staged X row is read from shared
-  // memory once per mini-group and added into the accumulators of the rows
-  // in its mask.  Each row still sums its terms in ascending column order
-  // with its own values in CSR order (bit-identical to the reference).
-  static_assert(LPR == 32, "band4 uses full warps per mini-group");
-  constexpr int MG = kBandMG;
-  for (int it = 0; it < nmine; ++it) {
-    const int b = blockIdx.x + it * G;
-    const int s = it % STAGES;
-    mbar_wait(&full[s], (unsigned)((it / STAGES) & 1));
-    const unsigned char* base = smem_raw + (size_t)s * bufbytes;
-    const T* xs = reinterpret_cast<const T*>(base);
-    const uint16_t* is = reinterpret_cast<const uint16_t*>(base + xbytes);
-    const T* vs = reinterpret_cast<const T*>(base + xbytes + ibytes);
-    const int r_lo = row0 + b * R;
-    const int nr = min(R, row0 + nrows - r_lo);
-    const uint16_t* lrp = is;
-    const int nnz_b = lrp[nr];
-    const int nmg = (nr + MG - 1) / MG;
-    const uint16_t* mgoff = is + nr + 1 + nnz_b;
-    const uint16_t* uent = mgoff + nmg + 1;
-    for (int m = warp; m < nmg; m += NCONS) {
-      const int r0 = m * MG;
-      const int nrg = min(MG, nr - r0);
-      const int vb = lrp[r0], ve = lrp[r0 + nrg];
-      (void)ve;
-      int p[MG];
-#pragma unroll
-      for (int r = 0; r < MG; ++r) p[r] = r < nrg ? lrp[r0 + r] - vb : 0;
-      T acc[MG][NCH][VEC];
-#pragma unroll
-      for (int r = 0; r < MG; ++r)
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[r][ch][v] = T(0);
-      const int ub = mgoff[m], ue = mgoff[m + 1];
-      for (int u0 = ub; u0 < ue; u0 += 32) {
-        const int ent = u0 + lane < ue ? uent[u0 + lane] : 0;
-        const int cnt = min(32, ue - u0);
-        for (int u = 0; u < cnt; ++u) {
-          const int e = __shfl_sync(0xffffffffu, ent, u);
-          const int slot = e >> 4, mask = e & 15;
-          T x[NCH][VEC];
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch)
-            ldv<T, VEC>(x[ch], xs + (size_t)slot * cc + (ch * 32 + lane) * VEC);
-#pragma unroll
-          for (int r = 0; r < MG; ++r) {
-            if (mask & (1 << r)) {
-              const int idx = p[r]++;
-              const T a = vs[vb + idx];  // shared-memory broadcast
-#pragma unroll
-              for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-                for (int v = 0; v < VEC; ++v)
-                  acc[r][ch][v] = fops<T>::add(acc[r][ch][v], fops<T>::mul(a, x[ch][v]));
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < MG; ++r) {
-        if (r < nrg) {
-          T* o = out + (size_t)(r_lo + r0 + r) * ldo;
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * 32 + lane) * VEC, acc[r][ch]);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-// ---- ring-gather SpMM (skewed / random rows) -----------------------------------
-// For rows with no reusable structure (R-MAT) the gather is latency-bound and
-// the number of X rows in flight is capped by the registers used as landing
-// buffers.  Here each LPR-lane group walks a strip of rows as one entry
-// stream and lands gathered X rows in a DEPTH-slot shared-memory ring with
-// cp.async (16 B per lane), issuing DEPTH entries ahead of the consumer.
-// The consumer sums each row's entries in order (mul then add, bit-identical
-// to the reference).
-template <class T, int VEC, int LPR, int NCH, int DEPTH, int STRIP = LPR>
-__global__ void __launch_bounds__(256)
-    k_spmm_ring(int64_t nrows, const int* __restrict__ rows, int row0,
-                const int* __restrict__ rp, const int* __restrict__ ci,
-                const T* __restrict__ av, const T* __restrict__ X, int ldx,
-                T* __restrict__ out, int ldo) {
-  constexpr int SLOT = LPR * VEC * NCH;  // elements per gathered row
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int grp_in_cta = threadIdx.x / LPR;
-  T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)grp_in_cta * DEPTH * SLOT;
-  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
-  const int64_t base = g * STRIP;
-  if (base >= nrows) return;
-  const int gl = threadIdx.x & (LPR - 1);
-  const unsigned gmask = group_mask(LPR);
-  const int cnt = (int)(nrows - base < STRIP ? nrows - base : STRIP);
-  int my_r = 0, my_b = 0, my_e = 0;
-  if (gl < cnt) {
-    my_r = rows ? __ldg(rows + base + gl) : row0 + (int)(base + gl);
-    my_b = __ldg(rp + my_r);
-    my_e = __ldg(rp + my_r + 1);
-  }
-  // producer cursor
-  int pq = 0, pk = __shfl_sync(gmask, my_b, 0, LPR), pe = __shfl_sync(gmask, my_e, 0, LPR);
-  int pk0 = pk;
-  int pcol = pk + gl < pe ? __ldg(ci + pk + gl) : 0;
-  int issued = 0;
-  auto produce = [&]() {
-    // skip exhausted rows
-    while (pq < cnt && pk >= pe) {
-      ++pq;
-      if (pq < cnt) {
-        pk = __shfl_sync(gmask, my_b, pq, LPR);
-        pe = __shfl_sync(gmask, my_e, pq, LPR);
-        pk0 = pk;
-        pcol = pk + gl < pe ? __ldg(ci + pk + gl) : 0;
-      }
-    }
-    if (pq < cnt) {
-      if (pk - pk0 == LPR) {
-        pk0 = pk;
-        pcol = pk + gl < pe ? __ldg(ci + pk + gl) : 0;
-      }
-      const int c = __shfl_sync(gmask, pcol, pk - pk0, LPR);
-      T* dst = ring + (size_t)(issued % DEPTH) * SLOT;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int off = (ch * LPR + gl) * VEC;
-        cp_async16(dst + off, X + (size_t)c * ldx + off, 16);
-      }
-      ++pk;
-    }
-    cp_async_commit();  // one group per step keeps wait_group counting exact
-    ++issued;
-  };
-#pragma unroll 1
-  for (int d = 0; d < DEPTH - 1; ++d) produce();
-  // consumer cursor
-  int consumed = 0;
-  for (int q = 0; q < cnt; ++q) {
-    const int b = __shfl_sync(gmask, my_b, q, LPR), e = __shfl_sync(gmask, my_e, q, LPR);
-    T acc[NCH][VEC];
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[ch][v] = T(0);
-    for (int k0 = b; k0 < e; k0 += LPR) {
-      const T a = k0 + gl < e ? __ldg(av + k0 + gl) : T(0);
-      const int n_here = min(LPR, e - k0);
-      for (int u = 0; u < n_here; ++u) {
-        produce();
-        cp_async_wait<DEPTH - 1>();
-        __syncwarp(gmask);
-        const T au = __shfl_sync(gmask, a, u, LPR);
-        const T* src = ring + (size_t)(consumed % DEPTH) * SLOT;
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          T x[VEC];
-          ldv<T, VEC>(x, src + (ch * LPR + gl) * VEC);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v)
-            acc[ch][v] = fops<T>::add(acc[ch][v], fops<T>::mul(au, x[v]));
-        }
-        __syncwarp(gmask);  // slot may be refilled by the next produce()
-        ++consumed;
-      }
-    }
-    const int r = __shfl_sync(gmask, my_r, q, LPR);
-    T* o = out + (size_t)r * ldo;
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) stv<T, VEC>(o + (ch * LPR + gl) * VEC, acc[ch]);
-  }
-  cp_async_wait<0>();
 }
 
 // Generic SpMM (any column count): one warp per row, scalar columns.
@@ -2228,13 +1327,24 @@ inline int blocks_for(int64_t threads, int per_block = 256) {
 // ===========================================================================
 struct SpmmWork {
   int64_t n_short = 0, n_long = 0, n_seg = 0;
-  // row-group union layout of the short rows (used when it cuts X gathers)
-  static constexpr int kGroupR = 8;
   size_t elem_ = 8;
+  // side stream for the long rows (runs beside the short-row kernel)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  SpmmWork() = default;
+  SpmmWork(const SpmmWork&) = delete;
+  SpmmWork& operator=(const SpmmWork&) = delete;
+  ~SpmmWork() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
+  // reference-bits mode: grid-stencil rows with separately rounded mul and
+  // add (bit-identical to spmm_row); default one FMA per term (tfg.h)
+  bool exact = false;
   bool skewed = false;  // row lengths vary a lot: one row per lane group
-  // band-staged layout (k_spmm_band)
+  // band-staged layout (k_spmm_band3)
   bool banded = false;
-  bool band_union = false;  // records carry mini-group unions (k_spmm_band4)
   int band_R = 0, band_blocks = 0, stage_cap = 0, idx_cap = 0, val_cap = 0;
   size_t band_smem = 0;
   dbuf<int> run_begin, run_start, run_len;
@@ -2252,19 +1362,13 @@ struct SpmmWork {
   // runs; adopted only when it at least halves the X rows gathered.
   void build_band(int row0, int64_t nrows, const std::vector<int>& rp,
                   const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st) {
-    const size_t row_bytes = (size_t)cc * elem;
-    static const int env_kb = [] {
-      const char* e = getenv("TFG_BAND_KB");
-      return e ? atoi(e) : 0;
-    }();
     detect_dia(row0, nrows, rp, ci, cc, elem);
     // smallest stage budget that admits a band layout (more CTAs per SM); the
     // stencil consumer wants >= 8 mini-groups (R >= 32) per block
     for (int kb : {40, 64, 100}) {
-      if (dia && kb == 40 && env_kb == 0 && (size_t)cc * elem == 512) continue;
-      const int use = env_kb > 0 ? env_kb : kb;
-      build_band_budget(row0, nrows, rp, ci, cc, elem, st, (size_t)use * 1024);
-      if (banded || env_kb > 0) return;
+      if (dia && kb == 40 && (size_t)cc * elem == 512) continue;
+      build_band_budget(row0, nrows, rp, ci, cc, elem, st, (size_t)kb * 1024);
+      if (banded) return;
     }
   }
 
@@ -2274,11 +1378,7 @@ struct SpmmWork {
                   int cc, size_t elem) {
     dia = false;
     dia_offs.clear();
-    static const bool dia_on = [] {
-      const char* e = getenv("TFG_BAND_DIA");
-      return !e || atoi(e) > 0;
-    }();
-    if (!dia_on || (size_t)cc * elem != 512 && (size_t)cc * elem != 1024) return;
+    if ((size_t)cc * elem != 512 && (size_t)cc * elem != 1024) return;
     std::vector<int> offs;
     for (int64_t r = row0; r < row0 + nrows; ++r)
       for (int k = rp[r]; k < rp[r + 1]; ++k) {
@@ -2323,13 +1423,6 @@ struct SpmmWork {
                          const std::vector<int>& ci, int cc, size_t elem, cudaStream_t st,
                          size_t budget) {
     const size_t row_bytes = (size_t)cc * elem;
-    static const bool union_on = [] {
-      const char* e = getenv("TFG_BAND_UNION");  // opt-in: measured slower than band3
-      return e && atoi(e) > 0;
-    }();
-    const int L = cc / (16 / (int)elem);
-    const bool use_union = union_on && (L == 32 || L == 64);
-    band_union = use_union;
     int64_t nnz_total = (int64_t)rp[row0 + nrows] - rp[row0];
     if (nnz_total <= 0) return;
     for (int R : {256, 128, 64, 32, 16, 8, 4}) {
@@ -2375,35 +1468,11 @@ struct SpmmWork {
                      runs.begin() - 1;
           slots[k - k0] = run_off[q] + (c - runs[q].first);
         }
-        // mini-groups of kBandMG consecutive rows: ascending union of their
-        // slots with a row mask (the register-reuse consumer)
-        std::vector<int> mgoff{0}, uent;
-        if (use_union) {
-          std::vector<std::pair<int, int>> tmp;
-          for (int m0 = 0; m0 < nr; m0 += kBandMG) {
-            tmp.clear();
-            for (int r = m0; r < std::min(nr, m0 + kBandMG); ++r)
-              for (int k = rp[r_lo + r]; k < rp[r_lo + r + 1]; ++k)
-                tmp.emplace_back(slots[k - k0], r - m0);
-            std::sort(tmp.begin(), tmp.end());
-            for (size_t q = 0; q < tmp.size();) {
-              size_t e = q;
-              int mask = 0;
-              while (e < tmp.size() && tmp[e].first == tmp[q].first) mask |= 1 << tmp[e++].second;
-              uent.push_back((tmp[q].first << 4) | mask);
-              q = e;
-            }
-            mgoff.push_back((int)uent.size());
-          }
-        }
-        const int nmg = (nr + kBandMG - 1) / kBandMG;
-        const bool rec_dia = dia && !use_union && R <= 128 && R >= 32;
-        const int irec = ((nr + 1 + (k1 - k0) + (use_union ? nmg + 1 + (int)uent.size() : 0) +
-                           (rec_dia ? 2 : 0)) + 7) / 8 * 8;
+        const bool rec_dia = dia && R <= 128 && R >= 32;
+        const int irec = ((nr + 1 + (k1 - k0) + (rec_dia ? 2 : 0)) + 7) / 8 * 8;
         const size_t need = (size_t)staged * row_bytes + (size_t)irec * 2 +
                             ((size_t)(k1 - k0) * elem + 15) / 16 * 16;
-        if ((int)runs.size() > kBandRuns || staged > (use_union ? 4095 : 65535) || need > budget ||
-            (int)uent.size() > 65535) {
+        if ((int)runs.size() > kBandRuns || staged > 65535 || need > budget) {
           ok = false;
           break;
         }
@@ -2422,10 +1491,6 @@ struct SpmmWork {
         const size_t rec0 = li.size();
         for (int r = r_lo; r <= r_hi; ++r) li.push_back(rp[r] - k0);
         for (int v : slots) li.push_back(v);
-        if (use_union) {
-          for (int v : mgoff) li.push_back(v);
-          for (int v : uent) li.push_back(v);
-        }
         if (rec_dia) {
           uint32_t mask = 0;
           for (int g = 0; g < (nr + 3) / 4; ++g)
@@ -2447,7 +1512,7 @@ struct SpmmWork {
       band_R = R;
       band_blocks = nb;
       // the stencil consumer needs >= 8 mini-groups per block (one per warp)
-      if (!(dia && !use_union && R <= 128 && R >= 32)) dia = false;
+      if (!(dia && R <= 128 && R >= 32)) dia = false;
       if (dia) {
         dia_dev.alloc(1);
         h2d(dia_dev.p, &dia_lines, 1, st);
@@ -2478,13 +1543,6 @@ struct SpmmWork {
   // grid stencil: the plane-streaming kernel replaces everything above
   // (tfg_stencil.cu); set by the plan when every row is in the list
   std::unique_ptr<StencilPlan> stencil;
-  bool grouped = false;
-  int64_t n_groups = 0, n_ucols = 0;
-  int64_t n_pairs = 0;
-  dbuf<int> g_rows, ucol, gperm;
-  dbuf<int64_t> g_uoff, g_poff;
-  dbuf<uint8_t> umask;
-  dbuf<unsigned char> gval;
   bool identity = false;  // short rows are exactly [row0, row0 + n_short)
   int row0 = 0;
   dbuf<int> short_rows, long_rows, seg_k0, seg_k1;
@@ -2494,78 +1552,6 @@ struct SpmmWork {
   dbuf<int> empty_rows;
   dbuf<int64_t> long_seg_off;
   dbuf<unsigned char> partial;
-
-  // rows: host row list (ascending not required); rp: host row_ptr
-  // Merge the column lists of each group of kGroupR consecutive short rows.
-  // Uses the group layout only when it removes >= 25% of the X gathers.
-  void build_groups(const std::vector<int>& sh, const std::vector<int>& rp,
-                    const std::vector<int>& ci, cudaStream_t st) {
-    const int R = kGroupR;
-    const int64_t ng = ((int64_t)sh.size() + R - 1) / R;
-    std::vector<int> grows((size_t)ng * R, -1), uc, perm;
-    std::vector<uint8_t> um;
-    std::vector<int64_t> uoff{0}, poff{0};
-    int64_t nnz = 0;
-    struct E { int col, row, k; };
-    std::vector<E> tmp;
-    for (int64_t g = 0; g < ng; ++g) {
-      tmp.clear();
-      for (int r = 0; r < R && g * R + r < (int64_t)sh.size(); ++r) {
-        const int row = sh[g * R + r];
-        grows[g * R + r] = row;
-        for (int k = rp[row]; k < rp[row + 1]; ++k) tmp.push_back({ci[k], r, k});
-        nnz += rp[row + 1] - rp[row];
-      }
-      std::sort(tmp.begin(), tmp.end(), [](const E& x, const E& y) {
-        return x.col < y.col || (x.col == y.col && x.row < y.row);
-      });
-      for (size_t q = 0; q < tmp.size();) {
-        size_t e = q;
-        int mask = 0;
-        while (e < tmp.size() && tmp[e].col == tmp[q].col) {
-          mask |= 1 << tmp[e].row;
-          perm.push_back(tmp[e].k);  // pair order: column, then row
-          ++e;
-        }
-        uc.push_back(tmp[q].col);
-        um.push_back((uint8_t)mask);
-        q = e;
-      }
-      uoff.push_back((int64_t)uc.size());
-      poff.push_back((int64_t)perm.size());
-    }
-    if (nnz == 0 || (double)uc.size() > 0.75 * (double)nnz) return;
-    grouped = true;
-    n_groups = ng;
-    n_ucols = (int64_t)uc.size();
-    g_rows.alloc(grows.size());
-    h2d(g_rows.p, grows.data(), grows.size(), st);
-    g_uoff.alloc(uoff.size());
-    h2d(g_uoff.p, uoff.data(), uoff.size(), st);
-    ucol.alloc(uc.size() + 1);
-    h2d(ucol.p, uc.data(), uc.size(), st);
-    umask.alloc(um.size() + 1);
-    h2d(umask.p, um.data(), um.size(), st);
-    n_pairs = (int64_t)perm.size();
-    g_poff.alloc(poff.size());
-    h2d(g_poff.p, poff.data(), poff.size(), st);
-    gperm.alloc(perm.size() + 1);
-    h2d(gperm.p, perm.data(), perm.size(), st);
-    gval.alloc((perm.size() + 64) * elem_);
-    TFG_CUDA(cudaStreamSynchronize(st));
-  }
-
-  // side stream for the long rows (runs beside the short-row kernel)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  SpmmWork() = default;
-  SpmmWork(const SpmmWork&) = delete;
-  SpmmWork& operator=(const SpmmWork&) = delete;
-  ~SpmmWork() {
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (side) cudaStreamDestroy(side);
-  }
 
   void build(const std::vector<int>& rows, const std::vector<int>& rp, int cc,
              size_t elem, cudaStream_t st, const std::vector<int>* ci = nullptr,
@@ -2591,14 +1577,10 @@ struct SpmmWork {
         seg_len = thr;
       }
     }
-    static const bool split_empty = [] {
-      const char* e = getenv("TFG_W1_EMPTY");
-      return !e || atoi(e) > 0;
-    }();
     std::vector<int> em;
     for (int r : rows) {
       const int b = rp[r], e = rp[r + 1];
-      if (e == b && split_empty && !stencil_rows && ci && ((size_t)cc * elem) % 16 == 0) {
+      if (e == b && !stencil_rows && ((size_t)cc * elem) % 16 == 0) {
         em.push_back(r);
       } else if (e - b <= long_thr) {
         sh.push_back(r);
@@ -2657,11 +1639,7 @@ struct SpmmWork {
       skewed = mx > 8.0 * std::max(mean, 1.0) ||
                (int64_t)sh.size() < (int64_t)sm_count() * 32 * 32;
     }
-    static const bool band_on = [] {
-      const char* e = getenv("TFG_SPMM_BAND");
-      return !e || atoi(e) > 0;
-    }();
-    if (band_on && ci && identity && !stencil_rows && (cc % vec == 0) &&
+    if (ci && identity && !stencil_rows && (cc % vec == 0) &&
         (cc / vec == 8 || cc / vec == 16 || cc / vec == 32 || cc / vec == 64))
       build_band(row0, n_short, rp, *ci, cc, elem, st);
     if (getenv("TFG_DEBUG"))
@@ -2670,78 +1648,39 @@ struct SpmmWork {
               "blocks=%d stage_cap=%d smem=%zu ci=%d\n",
               (long long)n_short, (long long)n_long, (int)identity, (int)skewed, (int)banded,
               band_R, band_blocks, stage_cap, band_smem, ci ? 1 : 0);
-    static const bool conc_on = [] {
-      const char* e = getenv("TFG_W1_CONCURRENT");
-      return !e || atoi(e) > 0;
-    }();
-    if (conc_on && n_long > 0 && n_short > 0 && !side) {
+    if (n_long > 0 && n_short > 0 && !side) {
       TFG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
       TFG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       TFG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
-    static const bool groups_on = [] {
-      const char* e = getenv("TFG_SPMM_GROUPS");
-      return e && atoi(e) > 0;
-    }();
-    if (groups_on && ci && !stencil_rows && (cc == 32 * vec || cc == 64 * vec) && !sh.empty())
-      build_groups(sh, rp, *ci, st);
   }
   size_t bytes() const {
     return short_rows.bytes() + long_rows.bytes() + seg_k0.bytes() + seg_k1.bytes() +
-           long_seg_off.bytes() + partial.bytes() + g_rows.bytes() + ucol.bytes() +
-           g_uoff.bytes() + umask.bytes() + g_poff.bytes() + gperm.bytes() + gval.bytes() +
+           long_seg_off.bytes() + partial.bytes() +
            run_begin.bytes() + run_start.bytes() + run_len.bytes() + idx_off.bytes() +
            lidx.bytes() + empty_rows.bytes();
   }
   int launches() const {
-    return (n_short > 0) + 2 * (n_long > 0) + (grouped ? 1 : 0) + (n_empty > 0);
+    return (n_short > 0) + 2 * (n_long > 0) + (n_empty > 0);
   }
 };
-
-// TFG_BAND_DIA=0 switches the stencil consumer off at execution time
-static bool dia_on() {
-  const char* e = getenv("TFG_BAND_DIA_EXEC");
-  return !e || atoi(e) > 0;
-}
 
 template <class T>
 static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
                                 const T* av, const T* X, int cc, T* out,
                                 cudaStream_t st) {
   if (w.n_short == 0) return;
+  constexpr int VEC = 16 / sizeof(T);
   if (w.banded) {
-    constexpr int VEC = 16 / sizeof(T);
+    // band-staged blocks (k_spmm_band3): 2-stage ring, 8 consumer warps; the
+    // stencil (diagonal-line) consumer where every mini-group qualifies
     const int L = cc / VEC;
-    static const int ws = [] {
-      const char* e = getenv("TFG_BAND_WS");
-      return e ? atoi(e) : 2;
-    }();
-    static const int bv = [] {
-      const char* e = getenv("TFG_BAND_V");
-      return e ? atoi(e) : 3;
-    }();
-#define TFG_BAND2(LPR, NCH, S)                                                               \
-  if (ws == S) {                                                                             \
-    const size_t smem = w.band_smem / 2 * S;                                                 \
-    if constexpr (LPR == 32) {                                                               \
-      if (bv == 3 && w.dia && dia_on()) {                                                    \
-        auto kd = k_spmm_band3<T, VEC, LPR, NCH, S, true>;                                   \
-        TFG_CUDA(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                      (int)smem));                                           \
-        int occ = 1;                                                                         \
-        TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kd, 288, smem));        \
-        const int grid = (int)std::min<int64_t>(w.band_blocks, (int64_t)sm_count() * std::max(occ, 1)); \
-        kd<<<grid, 288, smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av,  \
-                                    w.run_begin.p, w.run_start.p, w.run_len.p, w.idx_off.p,   \
-                                    w.lidx.p, w.stage_cap, w.idx_cap, w.val_cap, X, cc, out, cc, \
-                                    w.dia_dev.p);                                             \
-        TFG_LAUNCH_CHECK();                                                                  \
-        return;                                                                              \
-      }                                                                                      \
-    }                                                                                        \
-    auto kern = bv == 3 ? k_spmm_band3<T, VEC, LPR, NCH, S> : k_spmm_band2<T, VEC, LPR, NCH, S>; \
+    const size_t smem = w.band_smem;
+#define TFG_BAND(LPR, NCH)                                                                   \
+  {                                                                                          \
+    auto kern = k_spmm_band3<T, VEC, LPR, NCH, 2>;                                           \
     if constexpr (LPR == 32)                                                                 \
-      if (w.band_union && w.band_R >= 8 * kBandMG) kern = k_spmm_band4<T, VEC, LPR, NCH, S>;  \
+      if (w.dia) kern = k_spmm_band3<T, VEC, LPR, NCH, 2, true>;                             \
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                   (int)smem));                                               \
     int occ = 1;                                                                             \
@@ -2750,27 +1689,7 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     kern<<<grid, 288, smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av,   \
                                   w.run_begin.p, w.run_start.p, w.run_len.p, w.idx_off.p,    \
                                   w.lidx.p, w.stage_cap, w.idx_cap, w.val_cap, X, cc, out, cc, \
-                                  nullptr);                                                  \
-    TFG_LAUNCH_CHECK();                                                                      \
-    return;                                                                                  \
-  }
-    if (L == 8) { TFG_BAND2(8, 1, 2) TFG_BAND2(8, 1, 3) TFG_BAND2(8, 1, 4) }
-    if (L == 16) { TFG_BAND2(16, 1, 2) TFG_BAND2(16, 1, 3) TFG_BAND2(16, 1, 4) }
-    if (L == 32) { TFG_BAND2(32, 1, 2) TFG_BAND2(32, 1, 3) TFG_BAND2(32, 1, 4) }
-    if (L == 64) { TFG_BAND2(32, 2, 2) TFG_BAND2(32, 2, 3) TFG_BAND2(32, 2, 4) }
-#undef TFG_BAND2
-#define TFG_BAND(LPR, NCH)                                                                   \
-  {                                                                                          \
-    auto kern = k_spmm_band<T, VEC, LPR, NCH>;                                               \
-    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                                  (int)w.band_smem));                                        \
-    int occ = 1;                                                                             \
-    TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, w.band_smem));   \
-    const int grid = (int)std::min<int64_t>(w.band_blocks, (int64_t)sm_count() * std::max(occ, 1)); \
-    kern<<<grid, 256, w.band_smem, st>>>(w.band_blocks, w.band_R, w.row0, (int)w.n_short, rp, av, \
-                                         w.run_begin.p, w.run_start.p, w.run_len.p,          \
-                                         w.idx_off.p, w.lidx.p, w.stage_cap, w.idx_cap,      \
-                                         w.val_cap, X, cc, out, cc);                         \
+                                  w.dia ? w.dia_dev.p : nullptr);                            \
     TFG_LAUNCH_CHECK();                                                                      \
     return;                                                                                  \
   }
@@ -2780,116 +1699,22 @@ static void spmm_dispatch_short(const SpmmWork& w, const int* rp, const int* ci,
     if (L == 64) TFG_BAND(32, 2)
 #undef TFG_BAND
   }
-  if (w.grouped) {
-    constexpr int VEC = 16 / sizeof(T);
-    T* gval = reinterpret_cast<T*>(w.gval.p);
-    k_permute_values<T><<<blocks_for(w.n_pairs), 256, 0, st>>>(w.n_pairs, w.gperm.p, av, gval);
-    TFG_LAUNCH_CHECK();
-    const int nb = blocks_for(w.n_groups * 32);
-    if (cc == 32 * VEC)
-      k_spmm_group<T, VEC, 1, SpmmWork::kGroupR, 4, 2><<<nb, 256, 0, st>>>(
-          w.n_groups, w.g_rows.p, w.g_uoff.p, w.g_poff.p, w.ucol.p, w.umask.p, gval, X, cc, out,
-          cc);
-    else
-      k_spmm_group<T, VEC, 2, SpmmWork::kGroupR, 4, 1><<<nb, 256, 0, st>>>(
-          w.n_groups, w.g_rows.p, w.g_uoff.p, w.g_poff.p, w.ucol.p, w.umask.p, gval, X, cc, out,
-          cc);
-    TFG_LAUNCH_CHECK();
-    return;
-  }
   const int* rows = w.identity ? nullptr : w.short_rows.p;
   const int row0 = w.identity ? w.row0 : 0;
   const int64_t n = w.n_short;
-  constexpr int VEC = 16 / sizeof(T);
-  static const int skv = [] {
-    const char* e = getenv("TFG_SKEW_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  static const int ring_depth = [] {
-    const char* e = getenv("TFG_RING");
-    return e ? atoi(e) : 0;  // opt-in: measured slower on R-MAT
-  }();
-  if (w.skewed && ring_depth > 0 && cc % VEC == 0 && (cc / VEC == 16 || cc / VEC == 32 || cc / VEC == 64)) {
-    const int L = cc / VEC;
-#define TFG_RING(LPR, NCH, D)                                                               \
-  if (ring_depth == D) {                                                                    \
-    auto kern = k_spmm_ring<T, VEC, LPR, NCH, D, 1>;                                        \
-    const size_t smem = (size_t)(256 / LPR) * D * LPR * VEC * NCH * sizeof(T);             \
-    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<blocks_for(n * LPR), 256, smem, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
-    TFG_LAUNCH_CHECK();                                                                     \
-    return;                                                                                 \
-  }
-    if (L == 16) { TFG_RING(16, 1, 8) TFG_RING(16, 1, 16) TFG_RING(16, 1, 32) }
-    if (L == 32) { TFG_RING(32, 1, 8) TFG_RING(32, 1, 16) TFG_RING(32, 1, 32) }
-    if (L == 64) { TFG_RING(32, 2, 8) TFG_RING(32, 2, 16) }
-#undef TFG_RING
-  }
-#define TFG_SPMM_CASE(LPR, NCH)                                                  \
-  if (w.skewed && skv == 6)                                                      \
-    k_spmm_strip<T, VEC, LPR, NCH, 4, 8, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else if (w.skewed && skv == 3)                                                 \
-    k_spmm_strip<T, VEC, LPR, NCH, 8, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else if (w.skewed && skv == 4 && LPR >= 8)                                     \
-    k_spmm_strip<T, VEC, (LPR >= 8 ? LPR / 2 : LPR), (LPR >= 8 ? NCH * 2 : NCH), 4, 4, 1> \
-        <<<blocks_for(n * (LPR / 2)), 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
-  else if (w.skewed && skv == 5 && LPR >= 8)                                     \
-    k_spmm_strip<T, VEC, (LPR >= 8 ? LPR / 2 : LPR), (LPR >= 8 ? NCH * 2 : NCH), 8, 4, 1> \
-        <<<blocks_for(n * (LPR / 2)), 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
-  else if (w.skewed && skv == 1)                                                 \
-    k_spmm_strip<T, VEC, LPR, NCH, 8, 3, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else if (w.skewed && skv == 2)                                                 \
-    k_spmm_strip<T, VEC, LPR, NCH, 8, 2, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else if (w.skewed && skv == 8)                                                 \
-    k_spmm_strip<T, VEC, LPR, NCH, 4, 4, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else if (w.skewed) /* 2 gathers in flight, full occupancy: cfg3 1.02 -> 0.76 ms */ \
-    k_spmm_strip<T, VEC, LPR, NCH, 2, 8, 1><<<blocks_for(n * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  else                                                                           \
+  // skewed lists: one row per lane group, 2 gathers in flight at full
+  // occupancy (cfg3 1.02 -> 0.76 ms); uniform lists: strips of LPR rows
+#define TFG_SPMM_CASE(LPR, NCH)                                                        \
+  if (w.skewed)                                                                        \
+    k_spmm_strip<T, VEC, LPR, NCH, 2, 8, 1><<<blocks_for(n * LPR), 256, 0, st>>>(       \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                                    \
+  else                                                                                 \
     k_spmm_strip<T, VEC, LPR, NCH, 4, 4><<<blocks_for((n + LPR - 1) / LPR * LPR), 256, 0, st>>>( \
-        n, rows, row0, rp, ci, av, X, cc, out, cc);                              \
-  TFG_LAUNCH_CHECK();                                                            \
+        n, rows, row0, rp, ci, av, X, cc, out, cc);                                    \
+  TFG_LAUNCH_CHECK();                                                                  \
   return;
-  if constexpr (sizeof(T) == 8) {
-    // experiment knob (TFG_SPMM_VARIANT=u*4+m): unroll {4,8,16}, min blocks {1,2,3,4}
-    static const int variant = [] {
-      const char* e = getenv("TFG_SPMM_VARIANT");
-      return e ? atoi(e) : -1;
-    }();
-    if (variant >= 0 && (cc == 64 || cc == 128)) {
-      const int nb = blocks_for((n + 31) / 32 * 32);
-#define TFG_V(U, M)                                                                      \
-  if (cc == 64)                                                                          \
-    k_spmm_strip<T, VEC, 32, 1, U, M><<<nb, 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
-  else                                                                                   \
-    k_spmm_strip<T, VEC, 32, 2, U, M><<<nb, 256, 0, st>>>(n, rows, row0, rp, ci, av, X, cc, out, cc); \
-  TFG_LAUNCH_CHECK();                                                                    \
-  return;
-      switch (variant) {
-        case 0: TFG_V(4, 1)
-        case 1: TFG_V(4, 2)
-        case 2: TFG_V(4, 3)
-        case 3: TFG_V(4, 4)
-        case 4: TFG_V(8, 1)
-        case 5: TFG_V(8, 2)
-        case 6: TFG_V(8, 3)
-        case 7: TFG_V(8, 4)
-        case 8: TFG_V(16, 1)
-        case 9: TFG_V(16, 2)
-        case 10: TFG_V(16, 3)
-        default: break;
-      }
-#undef TFG_V
-    }
-  }
   if (cc % VEC == 0) {
-    const int L = cc / VEC;
-    switch (L) {
+    switch (cc / VEC) {
       case 4: TFG_SPMM_CASE(4, 1)
       case 8: TFG_SPMM_CASE(8, 1)
       case 16: TFG_SPMM_CASE(16, 1)
@@ -2909,25 +1734,12 @@ static void spmm_long(const SpmmWork& w, const int* ci, const T* av, const T* X,
                       cudaStream_t st) {
   T* partial = reinterpret_cast<T*>(w.partial.p);
   constexpr int VEC = 16 / sizeof(T);
-  static const int seg_unr = [] {  // gathers in flight per lane group
-    const char* e = getenv("TFG_SEG_UNR");
-    return e ? atoi(e) : 8;  // 8: cfg5 wavefront 1 10.3 -> 9.1 ms (vs 4)
-  }();
   const int L = cc % VEC == 0 ? cc / VEC : 0;
 #define TFG_SEG(LPR, NCH)                                                                     \
   {                                                                                           \
-    if (seg_unr == 2)                                                                         \
-      k_spmm_segments_vec<T, VEC, LPR, NCH, 2, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>( \
-          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
-    else if (seg_unr == 16)                                                                   \
-      k_spmm_segments_vec<T, VEC, LPR, NCH, 16><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(   \
-          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
-    else if (seg_unr == 8)                                                                    \
-      k_spmm_segments_vec<T, VEC, LPR, NCH, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(    \
-          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
-    else                                                                                      \
-      k_spmm_segments_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(       \
-          w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                           \
+    /* 8 gathers in flight per lane group: cfg5 wavefront 1 10.3 -> 9.1 ms (vs 4) */          \
+    k_spmm_segments_vec<T, VEC, LPR, NCH, 8><<<blocks_for(w.n_seg * LPR), 256, 0, st>>>(      \
+        w.n_seg, w.seg_k0.p, w.seg_k1.p, ci, av, X, cc, partial);                             \
     TFG_LAUNCH_CHECK();                                                                       \
     k_segment_combine_vec<T, VEC, LPR, NCH><<<blocks_for(w.n_long * LPR), 256, 0, st>>>(      \
         w.n_long, w.long_rows.p, w.long_seg_off.p, partial, cc, out, cc);                     \
@@ -2951,7 +1763,7 @@ template <class T>
 static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
                      const T* av, const T* X, int cc, T* out, cudaStream_t st) {
   if (w.stencil) {
-    stencil_run(*w.stencil, rp, ci, av, out, st);
+    stencil_run(*w.stencil, rp, ci, av, out, st, w.exact);
     return;
   }
   // short and long (segmented) rows are independent: the long rows run on a
@@ -3011,31 +1823,18 @@ struct tfg_plan {
   int64_t n_wide = 0;
   // (c) wavefront 1 / unfused second op
   tfg::SpmmWork second;
-  // (a)+(c) as one dependency-driven band sweep (k_spmm_band_sweep)
-  bool sweep = false;
-  int sw_nitems = 0, sw_grid = 0, sw_scap = 0, sw_icap = 0, sw_vcap = 0;
-  size_t sw_smem = 0;
-  uint32_t sw_epoch = 0;
-  int sw_chunk_shift = 0;                    // first-op blocks per dependency chunk (log2)
-  tfg::dbuf<int> sw_items, sw_done;         // sw_done: per chunk, 8 * blocks * epoch when done
-  tfg::dbuf<int2> sw_dep;
   tfg::dbuf<uint8_t> spill;
   tfg::dbuf<unsigned char> d1;
   // accounting
   int64_t spill_rows = 0, fused_rows = 0;
   int64_t first_rows = 0, second_rows = 0, nnz_processed = 0;
   int launches = 0;
-  void* sweep_out = nullptr;   // D of the execution in flight (sweep launch argument)
   int row_lo = 0, row_hi = 0;  // row block of a partition plan (multi-GPU)
   // algorithmic (compulsory) HBM bytes per stage: (a) first op, (b) fused
   // tiles, (c) wavefront-1 SpMM -- each input byte read once, each output
   // byte written once (the roofline numerator)
   int64_t stage_bytes[3] = {0, 0, 0};
   int64_t d1_read_rows = 0;  // distinct D1 rows wavefront 1 reads
-  // SpMM-SpMM on a 2-D stencil pair: both passes in one kernel, D1 on chip
-  std::unique_ptr<tfg::StencilPlan> stencil2;
-  // SpMM-SpMM on a stencil pair: both passes in one dependency-driven sweep
-  std::unique_ptr<tfg::StencilSweep> stencil_sweep;
 };
 
 namespace tfg {
@@ -3046,100 +1845,21 @@ static constexpr size_t kFusedSmemCap = 200 * 1024;
 static constexpr int64_t kGroupMaxNnz = 96ll << 20;
 static constexpr size_t kFusedSmemMax = 227 * 1024;  // sm_100 opt-in max per CTA
 
-static int gemm_variant() {
-  static const int gv = [] {
-    const char* e = getenv("TFG_GEMM_VARIANT");
-    return e ? atoi(e) : 2;  // 2: 128x128 / 8x8 tiles for FP32 BN = 128 (measured best)
-  }();
-  return gv;
-}
-
-// FP64 first-op GEMM thread tile (BN = 64): 0 = 64x64 blocks of 4x4 (256
-// threads), 1 = 128x64 of 8x8 (128 threads), 2 = 128x64 of 8x4 (256
-// threads), 3 = as 1 with BK = 32, 4 = 64x64 of 8x4 (128 threads; cfg1
-// first op 0.062 (0) -> 0.056 (2) -> 0.047 ms: more, smaller blocks)
-static int gemm_variant_f64() {
-  static const int gv = [] {
-    const char* e = getenv("TFG_GEMM_F64");
-    return e ? atoi(e) : 4;
-  }();
-  return gv;
-}
+// FMA first-op GEMM tilings (measured best): FP32 BN =
+// 128 -> 128x128 blocks of 8x8 thread tiles, BN = 64 -> 128x64 of 8x4;
+// FP64 BN = 64 -> 64x64 blocks of 8x4 tiles, 128 threads (cfg1 first op
+// 0.062 ms with 4x4 tiles -> 0.047 ms: more, smaller blocks).
 
 // shared memory of the pipelined GEMM configuration a plan uses
 static size_t fused_gemm_smem(const tfg_plan& pl) {
   if (pl.elem == 4) {
-    if (pl.gemm_kind == 2 && gemm_variant() == 2) return GemmCfg<float, 128, 128, 32, 8, 8, 3>::SMEM;
-    return pl.gemm_kind == 2 ? GemmCfg<float, 64, 128, 32, 4, 8, 3>::SMEM
+    return pl.gemm_kind == 2 ? GemmCfg<float, 128, 128, 32, 8, 8, 3>::SMEM
                              : GemmCfg<float, 128, 64, 32, 8, 4, 3>::SMEM;
   }
   return pl.gemm_kind == 2 ? GemmCfg<double, 64, 128, 16, 4, 8, 3>::SMEM
                            : GemmCfg<double, 64, 64, 16, 4, 4, 3>::SMEM;
 }
 
-// Launch (or, with grid_only, size) the band sweep for a plan.
-template <class T>
-static int sweep_launch(tfg_plan& pl, cudaStream_t st, bool grid_only) {
-  constexpr int VEC = 16 / sizeof(T);
-  const int cc = pl.p.c_cols;
-  const int L = cc / VEC;
-  const SpmmWork& w0 = pl.fo_sparse;
-  const SpmmWork& w1 = pl.second;
-  auto side = [&](const SpmmWork& w, const int* rp, const void* av, const void* X, void* out) {
-    BandSide<T> b;
-    b.R = w.band_R;
-    b.row0 = w.row0;
-    b.nrows = (int)w.n_short;
-    b.rp = rp;
-    b.av = static_cast<const T*>(av);
-    b.run_begin = w.run_begin.p;
-    b.run_start = w.run_start.p;
-    b.run_len = w.run_len.p;
-    b.idx_off = w.idx_off.p;
-    b.lidx = w.lidx.p;
-    b.X = static_cast<const T*>(X);
-    b.out = static_cast<T*>(out);
-    return b;
-  };
-  int grid = 0;
-  static const int dbg = [] {  // timing experiments only: bit 0 no waits, bit 1 no publish
-    const char* e = getenv("TFG_SWEEP_DBG");
-    return e ? atoi(e) : 0;
-  }();
-  auto go = [&](auto kern) {
-    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)pl.sw_smem));
-    int occ = 1;
-    TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 288, pl.sw_smem));
-    grid = (int)std::min<int64_t>(pl.sw_nitems, (int64_t)sm_count() * std::max(occ, 1));
-    if (grid_only) return;
-    ++pl.sw_epoch;
-    if ((int64_t)(pl.sw_epoch + 1) * 8 * ((int64_t)1 << pl.sw_chunk_shift) > (int64_t)INT32_MAX) {
-      TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));  // counters restart
-      pl.sw_epoch = 1;
-    }
-    kern<<<grid, 288, pl.sw_smem, st>>>(
-        pl.sw_nitems, pl.sw_items.p, pl.sw_dep.p, pl.sw_done.p, pl.sw_chunk_shift,
-        (int)pl.sw_epoch,
-        side(w0, pl.p.d_b_row_ptr, pl.p.d_b_val, pl.p.d_c, pl.d1.p),
-        side(w1, pl.p.d_a_row_ptr, pl.p.d_a_val, pl.d1.p, pl.sweep_out), pl.sw_scap, pl.sw_icap,
-        pl.sw_vcap, cc, dbg, w0.dia_dev.p, w1.dia_dev.p);
-    TFG_LAUNCH_CHECK();
-  };
-  const bool dia = w0.dia && w1.dia && dia_on();
-  if (L == 8) go(k_spmm_band_sweep<T, VEC, 8, 1, 2>);
-  else if (L == 16) go(k_spmm_band_sweep<T, VEC, 16, 1, 2>);
-  else if (L == 32 && dia) go(k_spmm_band_sweep<T, VEC, 32, 1, 2, true>);
-  else if (L == 32) go(k_spmm_band_sweep<T, VEC, 32, 1, 2>);
-  else if (L == 64 && dia) go(k_spmm_band_sweep<T, VEC, 32, 2, 2, true>);
-  else if (L == 64) go(k_spmm_band_sweep<T, VEC, 32, 2, 2>);
-  else throw runtime_error("band sweep: unsupported column count");
-  return grid;
-}
-
-// Row-list SpMM over ALL rows of a grid-stencil CSR: switch it to the
-// plane-streaming kernel (tfg_stencil.cu).  X must hold n rows.
-// The grid geometry of an n x n CSR (host copies), or g.nx == 0.
 static StencilGeom probe_stencil(int64_t n, const std::vector<int>& rp,
                                  const std::vector<int>& ci) {
   StencilGeom g;
@@ -3178,7 +1898,7 @@ static void attach_stencil(SpmmWork& w, const StencilGeom& g, const void* X, int
 }
 
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
-                 tfg_plan& pl, int row_lo = 0, int row_hi = -1) {
+                 tfg_plan& pl, int row_lo = 0, int row_hi = -1, uint32_t flags = 0) {
   // problem.check() -- kernels.hpp:35-42; require_workers is the caller's.
   if (pr.dtype != TFG_F32 && pr.dtype != TFG_F64)
     throw invalid_argument("problem: unknown dtype");
@@ -3190,10 +1910,28 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     throw invalid_argument("problem: B and C need at least one column");
   if (s && s->n != pr.n)
     throw invalid_argument("schedule and problem disagree on n");
+  // the SpMM kernels read X rows with 16-byte vector loads (tfg.h: operands
+  // 16-byte aligned, as cudaMalloc returns them)
+  if (!pr.b_is_dense && (uintptr_t)pr.d_c % 16 != 0)
+    throw invalid_argument("problem: C must be 16-byte aligned");
+  if ((uintptr_t)pr.d_a_val % 16 != 0 || (!pr.b_is_dense && (uintptr_t)pr.d_b_val % 16 != 0))
+    throw invalid_argument("problem: CSR values must be 16-byte aligned");
 
   pl.p = pr;
   pl.elem = pr.dtype == TFG_F64 ? 8 : 4;
   pl.has_sched = s != nullptr;
+  pl.fo_sparse.exact = pl.second.exact = (flags & TFG_PLAN_REFERENCE_BITS) != 0;
+  // TFG_DEBUG: wall time of each plan-creation phase
+  const bool dbg_t = getenv("TFG_DEBUG") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!dbg_t) return;
+    TFG_CUDA(cudaStreamSynchronize(st));
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tfg] plan phase %-24s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   const int n = pr.n, cc = pr.c_cols, bc = pr.b_cols;
   if (row_hi < 0) row_hi = n;
   if (row_lo < 0 || row_hi > n || row_lo > row_hi)
@@ -3212,6 +1950,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   pl.nnz_processed = arp[n];
   pl.d1.alloc((size_t)n * cc * pl.elem);
   pl.spill.alloc(n);
+  phase("row_ptr + d1 alloc");
 
   std::vector<int> fo_rows;  // first-op rows handled by stage (a)
   std::vector<int> second_rows;
@@ -3229,13 +1968,12 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     else if (aligned && cc % 64 == 0)
       pl.gemm_kind = 1;  // BN = 64
     if (pl.gemm_kind)
-      pl.gemm_bm = (pl.elem == 4 && (pl.gemm_kind == 1 || gemm_variant() == 2)) ? 128 : 64;
-    if (pl.gemm_kind == 1 && pl.elem == 8 && gemm_variant_f64() >= 1 && gemm_variant_f64() <= 3)
-      pl.gemm_bm = 128;
+      pl.gemm_bm = pl.elem == 4 ? 128 : 64;
     if (pl.gemm_kind && pl.elem == 4 &&
         tc_prepare(pl.tc, static_cast<const float*>(pr.d_b_dense), n, bc, cc))
       pl.gemm_bm = 128;
   }
+  phase("gemm/tc prepare");
   if (!s) {
     for (int i = row_lo; i < row_hi; ++i) fo_rows.push_back(i);
     second_rows = fo_rows;
@@ -3288,6 +2026,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         w_max = std::max(w_max, ihi[v] - ilo[v]);
       }
     }
+    phase("schedule d2h + tile lists");
     pl.fused_rows = fused_here;
     pl.second_rows = fused_here + (int64_t)second_rows.size();
     pl.zero_d = !partial && pl.second_rows != n;
@@ -3344,7 +2083,6 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
           }
           int best_bn = pl.tc.bn;
           double best = 1e300;
-          const char* env_bn = getenv("TFG_TC_BN");
           for (int bnc = pl.tc.bn; bnc >= 32 && cc % bnc == 0; bnc /= 2) {
             const int capc = (int)std::min<size_t>(tc_stage_bytes_bn(pl.tc, bnc) / ((size_t)bnc * 4),
                                                    (size_t)max_need);
@@ -3355,8 +2093,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
             if (getenv("TFG_DEBUG"))
               fprintf(stderr, "[tfg] tc candidate bn %d cap %d wide-nnz %lld cost %.3g\n", bnc, capc,
                       (long long)wide_nnz, cost);
-            if (env_bn ? bnc == atoi(env_bn) : cost < best) {
-              best = env_bn ? -1.0 : cost;
+            if (cost < best) {
+              best = cost;
               best_bn = bnc;
             }
           }
@@ -3450,6 +2188,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         pl.fused_smem = (size_t)pl.w_cap * cs * pl.elem + c_bytes;
       }
     }
+    phase("fused tiles");
     // spill set S = columns of wavefront-1 rows
     TFG_CUDA(cudaMemsetAsync(pl.spill.p, 0, n, st));
     if (nj1) {
@@ -3467,6 +2206,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     pl.spill_rows = (int64_t)h;
   }
   if (!s) TFG_CUDA(cudaMemsetAsync(pl.spill.p, 1, n, st));
+  phase("spill set");
 
   // (a) first-op work
   if (pr.b_is_dense) {
@@ -3506,9 +2246,13 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     attach_stencil(pl.fo_sparse, gB, pr.d_c, cc, pl.elem);
   }
   // (c) second-op work (wavefront-1 rows, then the empty fused rows)
-  if (!zero_rows.empty()) {
-    second_rows.insert(second_rows.end(), zero_rows.begin(), zero_rows.end());
-    std::sort(second_rows.begin(), second_rows.end());
+  if (!zero_rows.empty()) {  // ascending union, O(n) (a sort of millions of rows costs 0.5 s)
+    std::vector<uint8_t> in(n, 0);
+    for (int r : second_rows) in[r] = 1;
+    for (int r : zero_rows) in[r] = 1;
+    second_rows.clear();
+    for (int r = 0; r < n; ++r)
+      if (in[r]) second_rows.push_back(r);
   }
   {
     std::vector<int> aci;
@@ -3525,6 +2269,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                     stencil_rows(second_rows, gA, cc, pl.elem));
     attach_stencil(pl.second, gA, pl.d1.p, cc, pl.elem);
   }
+  phase("first-op + wave-1 work");
 
   // ---- algorithmic bytes per stage ------------------------------------
   {
@@ -3594,123 +2339,15 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                           (int64_t)second_rows.size() * cc * el;
   }
 
-  // D = A (B C) for a 2-D stencil pair with every row in both passes: one
-  // fused kernel keeps D1 in shared memory (tfg_stencil.cu, k_spmm2_stencil)
-  pl.stencil2.reset();
-  if (!pr.b_is_dense && !partial && pl.fo_sparse.stencil && pl.second.stencil) {
-    auto sp = std::make_unique<StencilPlan>();
-    if (stencil2_prepare(*sp, pl.fo_sparse.stencil->g, pl.second.stencil->g, pr.d_c, cc,
-                         (int)pl.elem)) {
-      pl.stencil2 = std::move(sp);
-      // D1 is neither written to nor read from HBM
-      const int64_t el = (int64_t)pl.elem;
-      pl.stage_bytes[0] += pl.stage_bytes[2] - (int64_t)n * cc * el - pl.d1_read_rows * cc * el;
-      pl.stage_bytes[2] = 0;
-      if (getenv("TFG_DEBUG"))
-        fprintf(stderr, "[tfg] fused stencil: tile %d zc %d ns %d per_sm %d items %lld smem %zu\n",
-                pl.stencil2->tx, pl.stencil2->zc, pl.stencil2->ns, pl.stencil2->per_sm,
-                (long long)pl.stencil2->items, pl.stencil2->smem);
-    }
-  }
-  pl.stencil_sweep.reset();
-  if (!pl.stencil2 && !pr.b_is_dense && !partial && pl.fo_sparse.stencil && pl.second.stencil) {
-    auto sw = std::make_unique<StencilSweep>();
-    if (stencil_sweep_prepare(*sw, *pl.fo_sparse.stencil, *pl.second.stencil)) {
-      pl.stencil_sweep = std::move(sw);
-      // D1 is still written once; wavefront 1 reads it back from L2
-      const int64_t el = (int64_t)pl.elem;
-      pl.stage_bytes[0] += pl.stage_bytes[2] - pl.d1_read_rows * cc * el;
-      pl.stage_bytes[2] = 0;
-    }
-  }
-
-  // (a)+(c) as one dependency-driven band sweep: SpMM-SpMM, nothing fused,
-  // both passes band-staged over all rows
-  {
-    // opt-in: measured slower than two band passes on cfg2 (0.61-0.73 vs
-    // 0.56 ms) although it moves 1 GB less DRAM -- the band SpMM is bound by
-    // the shared-memory data path, not HBM
-    const char* sweep_env = getenv("TFG_SWEEP");
-    const bool sweep_on = sweep_env && atoi(sweep_env) > 0;
-    const SpmmWork& w0 = pl.fo_sparse;
-    const SpmmWork& w1 = pl.second;
-    if (sweep_on && !pr.b_is_dense && pl.n_ftiles == 0 && !partial && w0.banded && w1.banded &&
-        !w0.stencil && !w1.stencil && !pl.stencil2 &&
-        !w0.band_union && !w1.band_union && w0.n_long == 0 && w1.n_long == 0 && w0.row0 == 0 &&
-        w1.row0 == 0 && w0.n_short == n && w1.n_short == n) {
-      pl.sw_scap = std::max(w0.stage_cap, w1.stage_cap);
-      pl.sw_icap = std::max(w0.idx_cap, w1.idx_cap);
-      pl.sw_vcap = std::max(w0.val_cap, w1.val_cap);
-      const size_t buf = (size_t)pl.sw_scap * cc * pl.elem +
-                         ((size_t)pl.sw_icap * 2 + 15) / 16 * 16 +
-                         ((size_t)pl.sw_vcap * pl.elem + 15) / 16 * 16;
-      pl.sw_smem = 2 * buf;
-      if (pl.sw_smem <= kBandSmemMax) {
-        const int nb0 = w0.band_blocks, nb1 = w1.band_blocks;
-        pl.sw_nitems = nb0 + nb1;
-        pl.sw_grid = pl.elem == 8 ? sweep_launch<double>(pl, st, true)
-                                  : sweep_launch<float>(pl, st, true);
-        // item order: first-op block i at key i; wavefront-1 block k after the
-        // last first-op block it reads plus two grid rounds
-        // dependency chunks: any block's D1 range spans <= 32 of them
-        int max_span = 1;
-        for (int k = 0; k < nb1; ++k)
-          if (w1.blk_xhi[k] >= w1.blk_xlo[k])
-            max_span = std::max(max_span, w1.blk_xhi[k] / w0.band_R - w1.blk_xlo[k] / w0.band_R + 1);
-        int cs = 0;
-        while (((max_span + (1 << cs) - 1) >> cs) + 1 > 32) ++cs;
-        pl.sw_chunk_shift = cs;
-        const int64_t lag = 2 * (int64_t)pl.sw_grid + (1 << cs);
-        std::vector<int2> dep(nb1);
-        std::vector<std::pair<int64_t, int>> keyed;
-        keyed.reserve(pl.sw_nitems);
-        for (int i = 0; i < nb0; ++i) keyed.emplace_back(2 * (int64_t)i, i);
-        for (int k = 0; k < nb1; ++k) {
-          const int lo = w1.blk_xlo[k], hi = w1.blk_xhi[k];
-          int2 d;
-          if (hi < lo) {
-            d = make_int2(0, -1);
-          } else {
-            d = make_int2(lo / w0.band_R, std::min(hi / w0.band_R, nb0 - 1));
-          }
-          dep[k] = d;
-          // after the last block of the last chunk it waits for
-          const int64_t last = std::min<int64_t>(((int64_t)(std::max(d.y, 0) >> cs) + 1) << cs, nb0) - 1;
-          const int64_t key = 2 * (last + lag) + 1;
-          keyed.emplace_back(key, k | (1 << 30));
-        }
-        std::stable_sort(keyed.begin(), keyed.end(),
-                         [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& b) {
-                           return a.first < b.first;
-                         });
-        std::vector<int> items(keyed.size());
-        for (size_t q = 0; q < keyed.size(); ++q) items[q] = keyed[q].second;
-        pl.sw_items.alloc(items.size());
-        h2d(pl.sw_items.p, items.data(), items.size(), st);
-        pl.sw_dep.alloc(dep.size());
-        h2d(pl.sw_dep.p, dep.data(), dep.size(), st);
-        pl.sw_done.alloc(((int64_t)nb0 + (1 << cs) - 1) >> cs);
-        TFG_CUDA(cudaMemsetAsync(pl.sw_done.p, 0, pl.sw_done.bytes(), st));
-        TFG_CUDA(cudaStreamSynchronize(st));
-        pl.sweep = true;
-        pl.stage_bytes[0] += pl.stage_bytes[2];  // one kernel does both passes
-        pl.stage_bytes[2] = 0;
-      }
-    }
-  }
-
+  phase("algorithmic bytes");
   pl.launches = 0;
   if (pl.tc.on && (pl.n_fo_blocks > 0 || pl.n_ftiles > 0)) pl.launches += 1;  // C split
-  if (pl.sweep || pl.stencil2 || pl.stencil_sweep) {
-    pl.launches += 1;
-  } else {
-    if (pr.b_is_dense)
-      pl.launches += pl.n_fo_blocks > 0;
-    else
-      pl.launches += pl.fo_sparse.launches();
-    pl.launches += pl.n_ftiles > 0;
-    pl.launches += pl.second.launches();
-  }
+  if (pr.b_is_dense)
+    pl.launches += pl.n_fo_blocks > 0;
+  else
+    pl.launches += pl.fo_sparse.launches();
+  pl.launches += pl.n_ftiles > 0;
+  pl.launches += pl.second.launches();
   TFG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -3752,10 +2389,8 @@ static void launch_fused_v2_cfg(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
 template <class T>
 static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
-    if (pl.gemm_kind == 2 && gemm_variant() == 2)
+    if (pl.gemm_kind == 2)
       launch_fused_v2_cfg<T, 128, 128, 32, 8, 8, 32>(pl, D1, D, st);
-    else if (pl.gemm_kind == 2)
-      launch_fused_v2_cfg<T, 64, 128, 32, 4, 8, 32>(pl, D1, D, st);
     else
       launch_fused_v2_cfg<T, 128, 64, 32, 8, 4, 16>(pl, D1, D, st);
   } else {
@@ -3769,30 +2404,16 @@ static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
 template <class T>
 static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
                            cudaStream_t st) {
-  const int gv = gemm_variant();
   if constexpr (sizeof(T) == 4) {
-    if (pl.gemm_kind == 2 && gv == 2)
+    if (pl.gemm_kind == 2)
       launch_gemm_v2_cfg<T, 128, 128, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
-    else if (pl.gemm_kind == 2)
-      launch_gemm_v2_cfg<T, 64, 128, 32, 4, 8>(pl, B, bc, C, cc, D1, st);
-    else if (gv == 1)  // 8x8 thread tiles, 128 threads (blocks of 128 rows)
-      launch_gemm_v2_cfg<T, 128, 64, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
     else
       launch_gemm_v2_cfg<T, 128, 64, 32, 8, 4>(pl, B, bc, C, cc, D1, st);
   } else {
-    const int g64 = gemm_variant_f64();
     if (pl.gemm_kind == 2)
       launch_gemm_v2_cfg<T, 64, 128, 16, 4, 8>(pl, B, bc, C, cc, D1, st);
-    else if (g64 == 1)
-      launch_gemm_v2_cfg<T, 128, 64, 16, 8, 8>(pl, B, bc, C, cc, D1, st);
-    else if (g64 == 2)
-      launch_gemm_v2_cfg<T, 128, 64, 16, 8, 4>(pl, B, bc, C, cc, D1, st);
-    else if (g64 == 3)
-      launch_gemm_v2_cfg<T, 128, 64, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
-    else if (g64 == 4)
-      launch_gemm_v2_cfg<T, 64, 64, 16, 8, 4>(pl, B, bc, C, cc, D1, st);
     else
-      launch_gemm_v2_cfg<T, 64, 64, 16, 4, 4>(pl, B, bc, C, cc, D1, st);
+      launch_gemm_v2_cfg<T, 64, 64, 16, 8, 4>(pl, B, bc, C, cc, D1, st);
   }
 }
 
@@ -3806,28 +2427,6 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   if (part == 1) goto wave1;
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
-  if (pl.stencil2 && part < 0) {  // both passes in one kernel, D1 in shared memory
-    stencil2_run(*pl.stencil2, pr.d_b_row_ptr, pr.d_b_col_idx, pr.d_b_val, pr.d_a_row_ptr,
-                 pr.d_a_col_idx, pr.d_a_val, D, st);
-    for (int e = 1; e <= 3; ++e)
-      if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
-    return;
-  }
-  if (pl.stencil_sweep && part < 0) {  // both stencil passes, one dependency-driven kernel
-    stencil_sweep_run(*pl.stencil_sweep, *pl.fo_sparse.stencil, *pl.second.stencil,
-                      pr.d_b_row_ptr, pr.d_b_col_idx, pr.d_b_val, pr.d_a_row_ptr, pr.d_a_col_idx,
-                      pr.d_a_val, pl.d1.p, D, st);
-    for (int e = 1; e <= 3; ++e)
-      if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
-    return;
-  }
-  if (pl.sweep && part < 0) {  // both passes in one dependency-driven kernel
-    pl.sweep_out = D;
-    sweep_launch<T>(pl, st, false);
-    for (int e = 1; e <= 3; ++e)
-      if (ev) TFG_CUDA(cudaEventRecord(ev[e], st));
-    return;
-  }
   // (a)
   if constexpr (sizeof(T) == 4) {
     if (pl.tc.on && (pl.n_fo_blocks || pl.n_ftiles))
@@ -3959,6 +2558,23 @@ tfg_status tfg_plan_create(const tfg_problem* p, const tfg_schedule* s, void* st
   });
 }
 
+tfg_status tfg_plan_create_ex(const tfg_problem* p, const tfg_schedule* s, uint32_t flags,
+                              int32_t row_lo, int32_t row_hi, void* stream, tfg_plan** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!p) throw invalid_argument("plan_create: null problem");
+    if (flags & ~(uint32_t)TFG_PLAN_REFERENCE_BITS) throw invalid_argument("plan_create: unknown flags");
+    auto* pl = new tfg_plan;
+    try {
+      plan_create(*p, s, as_stream(stream), *pl, row_lo, row_hi < 0 ? -1 : row_hi, flags);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    *out = pl;
+  });
+}
+
 tfg_status tfg_plan_create_partition(const tfg_problem* p, const tfg_schedule* s,
                                      int32_t row_lo, int32_t row_hi, void* stream,
                                      tfg_plan** out) {
@@ -3987,6 +2603,7 @@ tfg_status tfg_plan_execute_stage(tfg_plan* pl, int32_t stage, void* d, void* st
   return guard([&] {
     if (!pl || !d) throw invalid_argument("plan_execute_stage: null plan or output");
     if (stage < 0 || stage > 1) throw invalid_argument("plan_execute_stage: stage 0 or 1");
+    if ((uintptr_t)d % 16 != 0) throw invalid_argument("plan_execute: D must be 16-byte aligned");
     plan_execute_part(*pl, d, as_stream(stream), stage);
   });
 }
@@ -3994,6 +2611,7 @@ tfg_status tfg_plan_execute_stage(tfg_plan* pl, int32_t stage, void* d, void* st
 tfg_status tfg_plan_execute(tfg_plan* pl, void* d, void* stream) {
   return guard([&] {
     if (!pl || !d) throw invalid_argument("plan_execute: null plan or output");
+    if ((uintptr_t)d % 16 != 0) throw invalid_argument("plan_execute: D must be 16-byte aligned");
     plan_execute(*pl, d, as_stream(stream));
   });
 }
@@ -4028,29 +2646,19 @@ tfg_status tfg_plan_kernels(const tfg_plan* pl, char* buf, int32_t len) {
         k = w.stencil->g.d3 ? "stencil3d" : "stencil2d";
       else if (w.banded)
         k = w.dia ? "band-dia" : "band";
-      else if (w.grouped)
-        k = "group";
       else
         k = w.skewed ? "strip-skewed" : "strip";
       if (w.n_long) k += "+segments";
       return k;
     };
     std::string fo;
-    if (pl->stencil2)
-      fo = "stencil2d-fused";
-    else if (pl->stencil_sweep)
-      fo = "stencil-sweep";
-    else if (pl->sweep)
-      fo = "sweep";
-    else if (pl->p.b_is_dense)
+    if (pl->p.b_is_dense)
       fo = pl->n_fo_blocks == 0 ? "none" : (pl->tc.on ? "tcgen05" : (pl->gemm_kind ? "gemm-v2" : "gemm"));
     else
       fo = spmm_kind(pl->fo_sparse);
     std::string fu = pl->n_ftiles == 0 ? "none"
                      : (pl->fused_v2 ? (pl->tc.on ? "tcgen05-tiles" : "gemm-tiles") : "tiles");
-    std::string w1 = pl->stencil2        ? "stencil2d-fused"
-                     : pl->stencil_sweep ? "stencil-sweep"
-                     : (pl->sweep ? "sweep" : spmm_kind(pl->second));
+    std::string w1 = spmm_kind(pl->second);
     const std::string s = "first_op=" + fo + " fused=" + fu + " wave1=" + w1;
     const size_t n = std::min(s.size(), (size_t)len - 1);
     memcpy(buf, s.data(), n);

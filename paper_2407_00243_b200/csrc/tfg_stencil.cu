@@ -38,15 +38,9 @@ struct StencilArgs {
   int zc, ns, slices, ntx, nty, cc;
   long long items;
   int plane_elems;
-  int plane2_elems;  // fused kernel: D1 plane (the ring planes hold C)
-  OpArgs op[2];      // [0]: the single SpMM (or B of the fused chain), [1]: A of the chain
+  OpArgs op;
   void* out;
-  void* out1;               // sweep: D (out = D1)
-  const int* sweep_items;   // sweep: op << 30 | item of op, in launch order
-  int* sweep_done;          // sweep: first-op items finished per z chunk (cumulative)
-  int sweep_target;         // sweep: counter value of a complete chunk this launch
-  int nzc;                  // z chunks per tile
-  int dbg_fast;             // timing experiment only: every group takes the fast path (wrong D)
+  int nzc;  // z chunks per tile
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
@@ -131,10 +125,14 @@ __device__ __forceinline__ void load_vals(const T* __restrict__ av, int v0, int 
   }
 }
 
-template <class T, int VEC>
+// acc += v * x: one fused multiply-add per element (default: within the
+// north-star tolerance, half the FP issue slots), or the reference's
+// separately rounded mul and add (EXACT: bit-identical to spmm_row)
+template <class T, int VEC, bool EXACT>
 __device__ __forceinline__ void axpy(T (&acc)[VEC], T v, const T (&x)[VEC]) {
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) acc[e] = fops<T>::add(acc[e], fops<T>::mul(v, x[e]));
+  for (int e = 0; e < VEC; ++e)
+    acc[e] = EXACT ? fops<T>::add(acc[e], fops<T>::mul(v, x[e])) : fops<T>::fma(v, x[e], acc[e]);
 }
 
 // One output plane z of a warp's M points.  P0/P1/P2: the shared-memory
@@ -167,7 +165,7 @@ __device__ __forceinline__ int pad_index(int t) {  // t = m * K + 3 l + j
   return m * (4 * (D3 ? 9 : 3)) + 4 * l + (r - 3 * l);
 }
 
-template <class T, bool D3, int M, int ROW, bool PAD = false>
+template <class T, bool D3, int M, int ROW, bool PAD, bool EXACT>
 __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpArgs& op,
                                                 const T* __restrict__ P0, const T* __restrict__ P1,
                                                 const T* __restrict__ P2, const T* __restrict__ sv,
@@ -183,7 +181,7 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
   // the window rows of points outside the tile are still in the plane
   // buffer (or the next shared-memory region), so the fast path computes all
   // M points and stores only the valid ones
-  const bool fast = op.full && valid != 0 && (vM - v0 == M * 3 * NL || a.dbg_fast);
+  const bool fast = op.full && valid != 0 && vM - v0 == M * 3 * NL;
 #pragma unroll
   for (int m = 0; m < M; ++m)
 #pragma unroll
@@ -213,9 +211,9 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
       for (int k = 0; k < M + 2; ++k) {
         T xr[VEC];
         ldv<T, VEC>(xr, base + k * CW);
-        if (k < M) axpy<T, VEC>(acc[k], vl[k][0], xr);
-        if (k >= 1 && k - 1 < M) axpy<T, VEC>(acc[k - 1], vl[k - 1][1], xr);
-        if (k >= 2) axpy<T, VEC>(acc[k - 2], vl[k - 2][2], xr);
+        if (k < M) axpy<T, VEC, EXACT>(acc[k], vl[k][0], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC, EXACT>(acc[k - 1], vl[k - 1][1], xr);
+        if (k >= 2) axpy<T, VEC, EXACT>(acc[k - 2], vl[k - 2][2], xr);
       }
     }
     return;
@@ -234,9 +232,9 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
       for (int k = 0; k < M + 2; ++k) {
         T xr[VEC];
         ldv<T, VEC>(xr, base + k * CW);
-        if (k < M) axpy<T, VEC>(acc[k], sv[k * K + 3 * l], xr);
-        if (k >= 1 && k - 1 < M) axpy<T, VEC>(acc[k - 1], sv[(k - 1) * K + 3 * l + 1], xr);
-        if (k >= 2) axpy<T, VEC>(acc[k - 2], sv[(k - 2) * K + 3 * l + 2], xr);
+        if (k < M) axpy<T, VEC, EXACT>(acc[k], sv[k * K + 3 * l], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC, EXACT>(acc[k - 1], sv[(k - 1) * K + 3 * l + 1], xr);
+        if (k >= 2) axpy<T, VEC, EXACT>(acc[k - 2], sv[(k - 2) * K + 3 * l + 2], xr);
       }
     }
     return;
@@ -306,7 +304,7 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
         for (int j = 0; j < 3; ++j) {
           const int m = k - j;
           if (m < 0 || m >= M) continue;
-          if ((pr >> (3 * m + j)) & 1u) axpy<T, VEC>(acc[m], vl[m][j], xr);
+          if ((pr >> (3 * m + j)) & 1u) axpy<T, VEC, EXACT>(acc[m], vl[m][j], xr);
         }
       }
     }
@@ -339,13 +337,13 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
         const int yy = D3 ? wy + 1 + dy : 0;
         T xr[VEC];
         ldv<T, VEC>(xr, P + (yy * ROW + col0 + m + 1 + o) * CW + lane * VEC);
-        axpy<T, VEC>(acc[m], sv[k - v0], xr);
+        axpy<T, VEC, EXACT>(acc[m], sv[k - v0], xr);
       }
     }
   }
 }
 
-template <class T, bool D3, int M, int ROW, bool PAD = false>
+template <class T, bool D3, int M, int ROW, bool PAD, bool EXACT>
 __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArgs& op,
                                                const T* __restrict__ P0, const T* __restrict__ P1,
                                                const T* __restrict__ P2, const T* __restrict__ sv,
@@ -354,46 +352,16 @@ __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArg
                                                T* __restrict__ outp, int ostride, int lane) {
   constexpr int VEC = 16 / sizeof(T);
   T acc[M][VEC];
-  stencil_compute<T, D3, M, ROW, PAD>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase, px, py,
-                                      pz, lane, acc);
+  stencil_compute<T, D3, M, ROW, PAD, EXACT>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase,
+                                             px, py, pz, lane, acc);
 #pragma unroll
   for (int m = 0; m < M; ++m)
     if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * ostride, acc[m]);
 }
 
-__device__ __forceinline__ int ld_relaxed_gpu_s(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Work item `it` of the launch: in a sweep, items[it] = op << 30 | item of op
-// (op 0: first op X = C -> D1, op 1: second op X = D1 -> D); otherwise op 0.
-template <bool SWEEP>
-__device__ __forceinline__ void item_of(const StencilArgs& a, long long it, int& op,
-                                        long long& sub) {
-  if constexpr (SWEEP) {
-    const int code = __ldg(a.sweep_items + it);
-    op = code >> 30;
-    sub = code & ((1 << 30) - 1);
-  } else {
-    op = 0;
-    sub = it;
-  }
-}
-
-// SWEEP: both SpMM passes of D = A (B C) as one persistent kernel over an
-// item list in which every second-op item follows the first-op z-chunks it
-// reads (its own and both neighbours) by a lag of a few chunk rows, so the
-// D1 planes it loads are still in L2.  A CTA publishes a finished first-op
-// item with a per-chunk counter (barrier of its compute warps, gpu-scope
-// fence, atomic add); the producer of a second-op item waits for the
-// counters of its chunks before its TMA copies of D1.  Same rows, same
-// order, same bits as two launches.
-template <class T, bool D3, int NW, int M, int MINB, bool SWEEP = false>
+template <class T, bool D3, int NW, int M, int MINB, bool EXACT>
 __global__ void __launch_bounds__((NW + 1) * 32, MINB)
-    k_spmm_stencil(const __grid_constant__ CUtensorMap xmap,
-                   const __grid_constant__ CUtensorMap xmap1, const StencilArgs a) {
+    k_spmm_stencil(const __grid_constant__ CUtensorMap xmap, const StencilArgs a) {
   using TL = Tile<D3, NW, M>;
   constexpr int CW = (int)(kSliceBytes / sizeof(T));
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -415,24 +383,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     if (lane == 0) {
       uint32_t g = 0;
       for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
-        int op;
-        long long sub;
-        item_of<SWEEP>(a, it, op, sub);
         int cs, itx, ity, izc;
-        decode_item(a, sub, cs, itx, ity, izc);
+        decode_item(a, it, cs, itx, ity, izc);
         const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
         const int c1 = itx * TL::TX - 1;
         const int c2 = D3 ? ity * TL::TY - 1 : 0;
-        if constexpr (SWEEP) {
-          if (op == 1) {  // D1 planes of chunks izc - 1 .. izc + 1 must be published
-            const int clo = max(izc - 1, 0), chi = min(izc + 1, a.nzc - 1);
-            for (int ch = clo; ch <= chi; ++ch)
-              while (ld_relaxed_gpu_s(a.sweep_done + ch) < a.sweep_target) __nanosleep(128);
-            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-            asm volatile("fence.proxy.async.global;\n" ::: "memory");
-          }
-        }
-        const CUtensorMap* map = (SWEEP && op) ? &xmap1 : &xmap;
+        const CUtensorMap* map = &xmap;
         for (int p = z0 - 1; p <= z1; ++p, ++g) {
           const int s = (int)(g % ns);
           const uint32_t k = g / ns;
@@ -458,15 +414,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   const int wy = D3 ? warp : 0, wx = D3 ? 0 : warp;
   int s0 = 0;        // ring slot of the current item's plane z-1
   uint32_t p0 = 0;   // its full-barrier phase parity
+  const OpArgs& opa = a.op;
+  const T* __restrict__ av = static_cast<const T*>(opa.av);
+  T* const outb = static_cast<T*>(a.out);
   for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
-    int op;
-    long long sub;
-    item_of<SWEEP>(a, it, op, sub);
-    const OpArgs& opa = a.op[op];
-    const T* __restrict__ av = static_cast<const T*>(opa.av);
-    T* const outb = static_cast<T*>(op ? a.out1 : a.out);
     int cs, itx, ity, izc;
-    decode_item(a, sub, cs, itx, ity, izc);
+    decode_item(a, it, cs, itx, ity, izc);
     const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
     const int nzl = z1 - z0;
     const int x = itx * TL::TX + wx * M;
@@ -487,7 +440,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       const int v0 = srp[(jj & 7) * 16], v1 = srp[(jj & 7) * 16 + M];
       T* dst = svb + (jj % 3) * VS;
       // the compute side takes the padded full-box path exactly when this holds
-      const bool pad = opa.full && valid != 0 && (v1 - v0 == M * (D3 ? 27 : 9) || a.dbg_fast);
+      const bool pad = opa.full && valid != 0 && v1 - v0 == M * (D3 ? 27 : 9);
 #pragma unroll
       for (int i = 0; i < VR; ++i) {
         const int t = lane + 32 * i;
@@ -525,7 +478,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       }
       s_bar_wait(&full[s2], p2);
       const int rb = r0 + j * a.nxy;
-      stencil_points<T, D3, M, TL::ROW, true>(
+      stencil_points<T, D3, M, TL::ROW, true, EXACT>(
           a, opa, planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
           planes + (size_t)s2 * a.plane_elems, svb + (j % 3) * VS, rp_j, valid, wy, wx * M, rb,
           x, y, z0 + j, outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
@@ -548,262 +501,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       }
     }
     cp_async_wait<0>();
-    if constexpr (SWEEP) {
-      if (op == 0) {  // publish: this item's D1 rows are visible at gpu scope
-        asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicAdd(a.sweep_done + izc, 1);
-        }
-      }
-    }
-  }
-}
-
-// ---- fused SpMM-SpMM on a 2-D stencil pair: D = A (B C), D1 in registers ----
-// The paper's tile fusion (kernels.hpp:88-126, fused_run) taken to the point
-// where D1 = B C never leaves the SM.  A CTA owns TX = 4 * NW consecutive
-// points of a grid line and walks the sliding axis; every warp owns 4 of
-// them and keeps the D1 rows its points read -- its 4 points plus one on
-// each side (recomputed by the neighbour too), for planes d - 1, d, d + 1 --
-// in registers.  Per step u a warp
-//   (A) computes D1 plane d = z0 - 1 + u for its 6 points from three TMA-fed
-//       C planes (tile + two-point halo) in shared memory;
-//   (B) computes D plane d - 1 of its 4 points from the three D1 planes in
-//       registers and stores it.
-// Warps never exchange D1, so there is no barrier beyond the C-plane ring.
-// Every D1 and D row is summed in the reference order (bit-identical to the
-// two-pass execution); D1 never touches HBM, so the step moves |A| + |B| +
-// |C| + |D| bytes instead of adding 2 |D1|.
-template <class T, int N>
-__device__ __forceinline__ void pick_row(const T (&Da)[N][16 / sizeof(T)],
-                                         const T (&Db)[N][16 / sizeof(T)],
-                                         const T (&Dc)[N][16 / sizeof(T)], int pl, int i,
-                                         T (&x)[16 / sizeof(T)]) {
-  constexpr int VEC = 16 / sizeof(T);
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) x[e] = T(0);
-#pragma unroll
-  for (int q = 0; q < N; ++q)
-    if (q == i)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) x[e] = pl == 0 ? Da[q][e] : (pl == 1 ? Db[q][e] : Dc[q][e]);
-}
-
-// D rows of a warp's M points from D1 rows (point m's neighbour dx is row
-// m + 1 + dx) of planes d - 1 (Da), d (Db), d + 1 (Dc) held in registers.
-template <class T, int M>
-__device__ __forceinline__ void stencil_regs(const StencilArgs& a, const OpArgs& op,
-                                             const T (&Da)[M + 2][16 / sizeof(T)],
-                                             const T (&Db)[M + 2][16 / sizeof(T)],
-                                             const T (&Dc)[M + 2][16 / sizeof(T)],
-                                             const T* __restrict__ sv, int rpl, unsigned valid,
-                                             int rbase, T* __restrict__ outp, int ostride) {
-  constexpr int VEC = 16 / sizeof(T);
-  const int v0 = __shfl_sync(0xffffffffu, rpl, 0);
-  const int vM = __shfl_sync(0xffffffffu, rpl, M);
-  T acc[M][VEC];
-#pragma unroll
-  for (int m = 0; m < M; ++m)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[m][e] = T(0);
-  if (op.full && valid != 0 && vM - v0 == M * 9) {
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-#pragma unroll
-      for (int k = 0; k < M + 2; ++k) {
-        const T(&x)[VEC] = l == 0 ? Da[k] : (l == 1 ? Db[k] : Dc[k]);
-        if (k < M) axpy<T, VEC>(acc[k], sv[k * 9 + 3 * l], x);
-        if (k >= 1 && k - 1 < M) axpy<T, VEC>(acc[k - 1], sv[(k - 1) * 9 + 3 * l + 1], x);
-        if (k >= 2) axpy<T, VEC>(acc[k - 2], sv[(k - 2) * 9 + 3 * l + 2], x);
-      }
-    }
-  } else {
-    int vb[M + 1];
-#pragma unroll
-    for (int m = 0; m <= M; ++m) vb[m] = __shfl_sync(0xffffffffu, rpl, m);
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      if (!((valid >> m) & 1u)) continue;
-      const int r = rbase + m;
-      for (int k = vb[m]; k < vb[m + 1]; ++k) {  // the row's own CSR order
-        int o = __ldg(op.ci + k) - r;
-        const int dz = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
-        o -= dz * a.nx;
-        T x[VEC];
-        pick_row<T, M + 2>(Da, Db, Dc, dz + 1, m + 1 + o, x);
-        axpy<T, VEC>(acc[m], sv[k - v0], x);
-      }
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < M; ++m)
-    if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * ostride, acc[m]);
-}
-
-template <class T, int NW, int MINB>
-__global__ void __launch_bounds__((NW + 1) * 32, MINB)
-    k_spmm2_stencil(const __grid_constant__ CUtensorMap cmap, const StencilArgs a) {
-  constexpr int M = 4;            // D points per warp
-  constexpr int MA = M + 2;       // D1 points per warp
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int CW = (int)(kSliceBytes / sizeof(T));
-  constexpr int TX = M * NW;      // D points per tile
-  constexpr int ROWC = TX + 4;    // C plane rows (two-point halo)
-  constexpr int VS = ((MA * 9 + 31) / 32) * 32;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[kMaxNS], empty[kMaxNS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ns = a.ns;
-  T* cpl = reinterpret_cast<T*>(smem_raw);
-  T* wbase = cpl + (size_t)ns * a.plane_elems;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ns; ++s) {
-      s_bar_init(&full[s], 1);
-      s_bar_init(&empty[s], NW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  const uint32_t plane_bytes = (uint32_t)a.plane_elems * sizeof(T);
-  if (warp == NW) {
-    // ---------------- producer: C planes z0 - 2 .. z1 + 1 of each item ----------------
-    if (lane == 0) {
-      uint32_t g = 0;
-      for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
-        int cs, itx, ity, izc;
-        decode_item(a, it, cs, itx, ity, izc);
-        const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
-        for (int p = z0 - 2; p <= z1 + 1; ++p, ++g) {
-          const int s = (int)(g % ns);
-          const uint32_t k = g / ns;
-          if (k > 0) s_bar_wait(&empty[s], (k - 1) & 1u);
-          s_bar_expect(&full[s], plane_bytes);
-          tma_4d(cpl + (size_t)s * a.plane_elems, &cmap, cs * CW, itx * TX - 2, 0, p, &full[s]);
-        }
-      }
-    }
-    return;
-  }
-  // ---------------- consumers ----------------
-  // per warp: value / row-pointer cp.async rings of the first op (B, D1
-  // points) and of the second op (A, D points)
-  T* svA = wbase + (size_t)warp * 6 * VS;
-  T* svB = svA + 3 * VS;
-  int* srpA = reinterpret_cast<int*>(wbase + (size_t)NW * 6 * VS) + warp * 2 * 8 * 16;
-  int* srpB = srpA + 8 * 16;
-  const T* __restrict__ avA = static_cast<const T*>(a.op[0].av);
-  const T* __restrict__ avB = static_cast<const T*>(a.op[1].av);
-  T D0[MA][VEC], D1r[MA][VEC], D2[MA][VEC];  // D1 planes, rotated by the unrolled loop
-  int s0 = 0;       // ring slot of the item's C plane z0 - 2
-  uint32_t p0 = 0;  // its full-barrier parity
-  for (long long it = blockIdx.x; it < a.items; it += gridDim.x) {
-    int cs, itx, ity, izc;
-    decode_item(a, it, cs, itx, ity, izc);
-    const int z0 = a.zb + izc * a.zc, z1 = min(z0 + a.zc, a.ze);
-    const int nzl = z1 - z0;
-    const int xB = itx * TX + warp * M;  // D point 0 of this warp
-    const int xA = xB - 1;               // D1 point 0
-    unsigned validA = 0, validB = 0;
-#pragma unroll
-    for (int m = 0; m < MA; ++m)
-      if (xA + m >= 0 && xA + m < a.nx) validA |= 1u << m;
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-      if (xB + m < a.nx) validB |= 1u << m;
-    // first-op stream: D1 plane d = z0 - 1 + u; second-op stream: D plane z0 + b
-    auto liveA = [&](int u) { return validA && u <= nzl + 1 && z0 - 1 + u >= 0 && z0 - 1 + u < a.nz; };
-    auto liveB = [&](int b) { return validB && b < nzl; };
-    auto rowA = [&](int u) { return (z0 - 1 + u) * a.nx + xA; };
-    auto rowB = [&](int b) { return (z0 + b) * a.nx + xB; };
-    auto issue_rp = [&](int* srp, const int* rp, bool live, int row, int jj, int cnt) {
-      if (live && lane <= cnt)
-        cp_async_ca<4>(srp + (jj & 7) * 16 + lane, rp + max(0, min(row + lane, a.n)));
-    };
-    auto issue_vals = [&](T* sv, const int* srp, const T* av, bool live, int jj, int cnt) {
-      if (!live) return;
-      const int v0 = srp[(jj & 7) * 16], v1 = srp[(jj & 7) * 16 + cnt];
-      T* dst = sv + (jj % 3) * VS;
-#pragma unroll
-      for (int i = 0; i < VS / 32; ++i) {
-        const int k = v0 + lane + 32 * i;
-        if (k < v1) cp_async_ca<sizeof(T)>(dst + lane + 32 * i, av + k);
-      }
-    };
-    issue_rp(srpA, a.op[0].rp, liveA(0), rowA(0), 0, MA);
-    issue_rp(srpA, a.op[0].rp, liveA(1), rowA(1), 1, MA);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    issue_vals(svA, srpA, avA, liveA(0), 0, MA);
-    issue_rp(srpA, a.op[0].rp, liveA(2), rowA(2), 2, MA);
-    issue_rp(srpB, a.op[1].rp, liveB(0), rowB(0), 0, M);
-    cp_async_commit();
-    issue_vals(svA, srpA, avA, liveA(1), 1, MA);
-    issue_rp(srpA, a.op[0].rp, liveA(3), rowA(3), 3, MA);
-    issue_rp(srpB, a.op[1].rp, liveB(1), rowB(1), 1, M);
-    cp_async_commit();
-    // one step: D1 plane into Dn; D plane from (Dp, Dq, Dn) = planes d-2, d-1, d
-    auto step = [&](int u, T(&Dp)[MA][VEC], T(&Dq)[MA][VEC], T(&Dn)[MA][VEC]) {
-      cp_async_wait<1>();  // group of step u - 2
-      __syncwarp();
-      issue_vals(svA, srpA, avA, liveA(u + 2), u + 2, MA);
-      issue_rp(srpA, a.op[0].rp, liveA(u + 4), rowA(u + 4), u + 4, MA);
-      issue_vals(svB, srpB, avB, liveB(u), u, M);
-      issue_rp(srpB, a.op[1].rp, liveB(u + 2), rowB(u + 2), u + 2, M);
-      cp_async_commit();
-      // C ring positions of item planes u, u + 1, u + 2
-      int s1 = s0 + 1, s2;
-      uint32_t p1 = p0, p2;
-      if (s1 == ns) s1 = 0, p1 ^= 1u;
-      s2 = s1 + 1;
-      p2 = p1;
-      if (s2 == ns) s2 = 0, p2 ^= 1u;
-      if (u == 0) {
-        s_bar_wait(&full[s0], p0);
-        s_bar_wait(&full[s1], p1);
-      }
-      s_bar_wait(&full[s2], p2);
-      if (liveA(u)) {  // (A) D1 plane z0 - 1 + u of the warp's 6 points
-        const int rp_u = lane <= MA ? srpA[(u & 7) * 16 + lane] : 0;
-        stencil_compute<T, false, MA, ROWC>(
-            a, a.op[0], cpl + (size_t)s0 * a.plane_elems, cpl + (size_t)s1 * a.plane_elems,
-            cpl + (size_t)s2 * a.plane_elems, svA + (u % 3) * VS, rp_u, validA, 0, warp * M,
-            rowA(u), xA, 0, z0 - 1 + u, lane, Dn);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        s_bar_arrive(&empty[s0]);
-        if (u == nzl + 1) {
-          s_bar_arrive(&empty[s1]);
-          s_bar_arrive(&empty[s2]);
-        }
-      }
-      if (u >= 2 && liveB(u - 2)) {  // (B) D plane z0 + u - 2
-        const int b = u - 2;
-        const int rp_b = lane <= M ? srpB[(b & 7) * 16 + lane] : 0;
-        const int rb = rowB(b);
-        stencil_regs<T, M>(a, a.op[1], Dp, Dq, Dn, svB + (b % 3) * VS, rp_b, validB, rb,
-                           static_cast<T*>(a.out) + (size_t)rb * a.cc + (size_t)cs * CW +
-                               lane * VEC,
-                           a.cc);
-      }
-      if (u == nzl + 1) {  // next item starts after item plane nzl + 3
-        s0 = s2 + 1;
-        p0 = p2;
-        if (s0 == ns) s0 = 0, p0 ^= 1u;
-      } else {
-        s0 = s1;
-        p0 = p1;
-      }
-    };
-    for (int u = 0; u <= nzl + 1; u += 3) {
-      step(u, D1r, D2, D0);
-      if (u + 1 <= nzl + 1) step(u + 1, D2, D0, D1r);
-      if (u + 2 <= nzl + 1) step(u + 2, D0, D1r, D2);
-    }
-    cp_async_wait<0>();
-    __syncwarp();
   }
 }
 
@@ -836,6 +533,9 @@ bool check_geom(int n, const std::vector<int>& rp, const std::vector<int>& ci, i
   for (int r = 0; r < n; ++r) {
     const int x = r % nx, y = (int)((r / nx) % ny), z = (int)(r / nxy);
     for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      // the kernel finds a neighbour's value by its rank in the row, so the
+      // columns must be strictly increasing (no duplicates, sorted)
+      if (k > rp[r] && ci[k] <= ci[k - 1]) return false;
       int64_t o = (int64_t)ci[k] - r;
       int dz, dy = 0;
       if (ny > 1) {
@@ -1006,43 +706,51 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   return true;
 }
 
-template <class T, bool D3, int NW, int MINB>
+template <class T, bool D3, int NW, int MINB, bool EXACT>
 static void stencil_launch(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
-  auto kern = k_spmm_stencil<T, D3, NW, 4, MINB>;
+  auto kern = k_spmm_stencil<T, D3, NW, 4, MINB, EXACT>;
   TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
-  kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, sp.xmap, a);
+  kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, a);
   TFG_LAUNCH_CHECK();
 }
 
 // register budget cut for the resident CTAs per SM the plan chose
-template <class T, bool D3>
+template <class T, bool D3, bool EXACT>
 static void stencil_launch_d(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
   const int r = sp.per_sm;
   if (sp.nw == 8) {
     if (r >= 2)
-      stencil_launch<T, D3, 8, 2>(sp, a, st);
+      stencil_launch<T, D3, 8, 2, EXACT>(sp, a, st);
     else
-      stencil_launch<T, D3, 8, 1>(sp, a, st);
+      stencil_launch<T, D3, 8, 1, EXACT>(sp, a, st);
   } else {
     if (r >= 4)
-      stencil_launch<T, D3, 4, 4>(sp, a, st);
+      stencil_launch<T, D3, 4, 4, EXACT>(sp, a, st);
     else if (r == 3)
-      stencil_launch<T, D3, 4, 3>(sp, a, st);
+      stencil_launch<T, D3, 4, 3, EXACT>(sp, a, st);
     else
-      stencil_launch<T, D3, 4, 2>(sp, a, st);
+      stencil_launch<T, D3, 4, 2, EXACT>(sp, a, st);
   }
 }
 
 template <class T>
-static void stencil_launch_t(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
-  if (sp.g.d3)
-    stencil_launch_d<T, true>(sp, a, st);
-  else
-    stencil_launch_d<T, false>(sp, a, st);
+static void stencil_launch_t(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st,
+                             bool exact) {
+  if (sp.g.d3) {
+    if (exact)
+      stencil_launch_d<T, true, true>(sp, a, st);
+    else
+      stencil_launch_d<T, true, false>(sp, a, st);
+  } else {
+    if (exact)
+      stencil_launch_d<T, false, true>(sp, a, st);
+    else
+      stencil_launch_d<T, false, false>(sp, a, st);
+  }
 }
 
 void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void* av, void* out,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool exact) {
   StencilArgs a{};
   const StencilGeom& g = sp.g;
   a.n = g.nx * g.ny * g.nz;
@@ -1061,270 +769,21 @@ void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void
   a.cc = sp.cc;
   a.items = sp.items;
   a.nzc = sp.nzc;
-  a.dbg_fast = env_int("TFG_STENCIL_DBG_FAST", 0);
   a.plane_elems = (int)(sp.plane_bytes / sp.elem);
-  a.op[0].K = g.K;
-  a.op[0].full = g.K == (g.d3 ? 27 : 9);
-  memcpy(a.op[0].rank, g.rank, sizeof(g.rank));
-  a.op[0].used = 0;
+  a.op.K = g.K;
+  a.op.full = g.K == (g.d3 ? 27 : 9);
+  memcpy(a.op.rank, g.rank, sizeof(g.rank));
+  a.op.used = 0;
   for (int q = 0; q < 27; ++q)
-    if (g.rank[q] >= 0) a.op[0].used |= 1u << q;
-  a.op[0].rp = rp;
-  a.op[0].ci = ci;
-  a.op[0].av = av;
+    if (g.rank[q] >= 0) a.op.used |= 1u << q;
+  a.op.rp = rp;
+  a.op.ci = ci;
+  a.op.av = av;
   a.out = out;
   if (sp.elem == 8)
-    stencil_launch_t<double>(sp, a, st);
+    stencil_launch_t<double>(sp, a, st, exact);
   else
-    stencil_launch_t<float>(sp, a, st);
-}
-
-bool stencil2_prepare(StencilPlan& sp, const StencilGeom& gb, const StencilGeom& ga,
-                      const void* C, int cc, int elem) {
-  sp.on = false;
-  // opt-in: measured 0.77 ms per cfg2 step against 0.42 ms for two stencil
-  // passes -- the D1 registers cap the CTA at 8 resident warps per SM and
-  // the kernel is latency-bound (IPC 0.97); DESIGN.md section 7
-  if (!stencil_env_enabled() || env_int("TFG_STENCIL_FUSE", 0) == 0) return false;
-  if (gb.d3 || ga.d3 || gb.nx == 0 || gb.nx != ga.nx || gb.nz != ga.nz) return false;
-  if ((size_t)cc * elem % kSliceBytes != 0 || (uintptr_t)C % 16 != 0) return false;
-  auto enc = encode_tiled();
-  if (!enc) return false;
-  sp.g = gb;
-  sp.elem = elem;
-  sp.cc = cc;
-  sp.M = 4;
-  const int nw_env = env_int("TFG_STENCIL2_NW", 0);
-  sp.nw = nw_env == 8 ? 8 : 4;
-  sp.cw = (int)(kSliceBytes / elem);
-  sp.slices = (int)((size_t)cc * elem / kSliceBytes);
-  sp.tx = 4 * sp.nw;
-  sp.ty = 1;
-  sp.tyh = 1;
-  sp.ntx = (gb.nx + sp.tx - 1) / sp.tx;
-  sp.nty = 1;
-  sp.plane_bytes = (size_t)sp.cw * (sp.tx + 4) * elem;   // C plane
-  sp.plane2_bytes = 0;  // D1 lives in registers
-  const size_t fixed = (size_t)sp.nw * (6 * ((6 * 9 + 31) / 32) * 32 * elem + 2 * 8 * 16 * 4);
-  const int per_env = env_int("TFG_STENCIL2_CTAS", 0);
-  int per_sm = per_env > 0 ? std::min(per_env, 3) : (sp.nw == 8 ? 1 : 3);
-  int ns = 0;
-  for (; per_sm >= 1; --per_sm) {
-    const size_t budget = kSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
-    ns = budget > fixed ? (int)std::min<size_t>(kMaxNS, (budget - fixed) / sp.plane_bytes) : 0;
-    if (ns >= 3) break;
-  }
-  if (per_sm < 1 || ns < 3) return false;
-  const int ns_env = env_int("TFG_STENCIL_NS", 0);
-  if (ns_env >= 3) ns = std::min(ns, ns_env);
-  sp.ns = ns;
-  sp.smem = ns * sp.plane_bytes + fixed;
-  sp.per_sm = per_sm;
-  sp.grid = sm_count() * per_sm;
-  const int64_t tiles = (int64_t)sp.ntx * sp.slices;
-  const int zc_env = env_int("TFG_STENCIL2_ZC", 0);
-  int best = gb.nz;
-  double best_cost = 1e300;
-  for (int zc = std::min(8, gb.nz); zc <= std::min(32, std::max(1, gb.nz)); ++zc) {
-    const int64_t items = tiles * ((gb.nz + zc - 1) / zc);
-    const double cost = (double)((items + sp.grid - 1) / sp.grid) * (zc + 4);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = zc;
-    }
-  }
-  sp.zc = zc_env > 0 ? zc_env : best;
-  sp.nzc = (gb.nz + sp.zc - 1) / sp.zc;
-  sp.items = tiles * sp.nzc;
-  sp.grid = (int)std::min<int64_t>(sp.grid, sp.items);
-  cuuint64_t dims[4] = {(cuuint64_t)cc, (cuuint64_t)gb.nx, 1, (cuuint64_t)gb.nz};
-  cuuint64_t strides[3] = {(cuuint64_t)cc * elem, (cuuint64_t)cc * elem * gb.nx,
-                           (cuuint64_t)cc * elem * gb.nx};
-  cuuint32_t box[4] = {(cuuint32_t)sp.cw, (cuuint32_t)(sp.tx + 4), 1, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  if (enc(&sp.xmap, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-          4, const_cast<void*>(C), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
-  sp.g2 = ga;
-  sp.on = true;
-  return true;
-}
-
-template <class T, int NW, int MINB>
-static void stencil2_launch(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
-  auto kern = k_spmm2_stencil<T, NW, MINB>;
-  TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
-  kern<<<sp.grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, a);
-  TFG_LAUNCH_CHECK();
-}
-
-template <class T>
-static void stencil2_launch_t(const StencilPlan& sp, const StencilArgs& a, cudaStream_t st) {
-  if (sp.nw == 8)
-    stencil2_launch<T, 8, 1>(sp, a, st);
-  else if (sp.per_sm >= 3)
-    stencil2_launch<T, 4, 3>(sp, a, st);
-  else
-    stencil2_launch<T, 4, 2>(sp, a, st);
-}
-
-static void fill_op(OpArgs& o, const StencilGeom& g, const int* rp, const int* ci, const void* av) {
-  o.used = 0;
-  for (int q = 0; q < 27; ++q)
-    if (g.rank[q] >= 0) o.used |= 1u << q;
-  o.K = g.K;
-  o.full = g.K == (g.d3 ? 27 : 9);
-  memcpy(o.rank, g.rank, sizeof(g.rank));
-  o.rp = rp;
-  o.ci = ci;
-  o.av = av;
-}
-
-void stencil2_run(const StencilPlan& sp, const int* b_rp, const int* b_ci, const void* b_av,
-                  const int* a_rp, const int* a_ci, const void* a_av, void* out,
-                  cudaStream_t st) {
-  StencilArgs a{};
-  const StencilGeom& g = sp.g;
-  a.n = g.nx * g.nz;
-  a.nx = g.nx;
-  a.ny = 1;
-  a.nz = g.nz;
-  a.nxy = g.nx;
-  a.zb = 0;
-  a.ze = g.nz;
-  a.zc = sp.zc;
-  a.ns = sp.ns;
-  a.slices = sp.slices;
-  a.ntx = sp.ntx;
-  a.nty = 1;
-  a.cc = sp.cc;
-  a.items = sp.items;
-  a.plane_elems = (int)(sp.plane_bytes / sp.elem);
-  a.plane2_elems = (int)(sp.plane2_bytes / sp.elem);
-  fill_op(a.op[0], sp.g, b_rp, b_ci, b_av);
-  fill_op(a.op[1], sp.g2, a_rp, a_ci, a_av);
-  a.out = out;
-  if (sp.elem == 8)
-    stencil2_launch_t<double>(sp, a, st);
-  else
-    stencil2_launch_t<float>(sp, a, st);
-}
-
-// ---- both passes as one dependency-driven sweep (k_spmm_stencil<..., true>) ----
-bool stencil_sweep_prepare(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1) {
-  sw.on = false;
-  // opt-in: on cfg2 0.42 ms per step at a lag of 16-24 chunk rows, equal to
-  // two passes; shorter lags stall on the dependencies (lag 3: 0.77 ms) and
-  // longer ones let D1 fall out of L2 before it is read
-  if (env_int("TFG_STENCIL_SWEEP", 0) == 0 || !p0.on || !p1.on) return false;
-  const StencilGeom &g0 = p0.g, &g1 = p1.g;
-  if (g0.nx != g1.nx || g0.ny != g1.ny || g0.nz != g1.nz || g0.d3 != g1.d3) return false;
-  if (p0.zb != 0 || p0.ze != g0.nz || p1.zb != 0 || p1.ze != g1.nz) return false;
-  if (p0.nw != p1.nw || p0.M != p1.M || p0.tx != p1.tx || p0.ty != p1.ty || p0.zc != p1.zc ||
-      p0.ns != p1.ns || p0.slices != p1.slices || p0.smem != p1.smem || p0.elem != p1.elem)
-    return false;
-  const int64_t ipc = (int64_t)p0.ntx * p0.nty * p0.slices;  // items per z chunk
-  const int nzc = p0.nzc;
-  const int lag = std::max(1, env_int("TFG_STENCIL_SWEEP_LAG", 16));
-  std::vector<int> items;
-  items.reserve((size_t)(2 * ipc * nzc));
-  for (int c = 0; c < nzc + lag; ++c) {
-    if (c < nzc)
-      for (int64_t q = 0; q < ipc; ++q) items.push_back((int)(c * ipc + q));
-    if (c - lag >= 0)
-      for (int64_t q = 0; q < ipc; ++q) items.push_back((int)((1 << 30) | ((c - lag) * ipc + q)));
-  }
-  if ((int64_t)items.size() >= (1 << 30)) return false;
-  sw.items.alloc(items.size());
-  h2d(sw.items.p, items.data(), items.size(), 0);
-  sw.done.alloc(nzc);
-  TFG_CUDA(cudaMemset(sw.done.p, 0, sw.done.bytes()));
-  TFG_CUDA(cudaDeviceSynchronize());
-  sw.nitems = (int64_t)items.size();
-  sw.ipc = ipc;
-  sw.epoch = 0;
-  sw.on = true;
-  return true;
-}
-
-template <class T, bool D3, int NW, int MINB>
-static void sweep_launch_k(const StencilPlan& sp, const StencilPlan& sp1, const StencilArgs& a,
-                           cudaStream_t st) {
-  auto kern = k_spmm_stencil<T, D3, NW, 4, MINB, true>;
-  TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem));
-  int occ = 0;
-  TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NW + 1) * 32, sp.smem));
-  // every CTA must be resident: items wait on earlier items of other CTAs
-  const int grid = (int)std::min<int64_t>(a.items, (int64_t)sm_count() * std::max(occ, 1));
-  kern<<<grid, (NW + 1) * 32, sp.smem, st>>>(sp.xmap, sp1.xmap, a);
-  TFG_LAUNCH_CHECK();
-}
-
-template <class T, bool D3>
-static void sweep_launch_d(const StencilPlan& sp, const StencilPlan& sp1, const StencilArgs& a,
-                           cudaStream_t st) {
-  const int r = sp.per_sm;
-  if (sp.nw == 8) {
-    if (r >= 2)
-      sweep_launch_k<T, D3, 8, 2>(sp, sp1, a, st);
-    else
-      sweep_launch_k<T, D3, 8, 1>(sp, sp1, a, st);
-  } else {
-    if (r >= 4)
-      sweep_launch_k<T, D3, 4, 4>(sp, sp1, a, st);
-    else if (r == 3)
-      sweep_launch_k<T, D3, 4, 3>(sp, sp1, a, st);
-    else
-      sweep_launch_k<T, D3, 4, 2>(sp, sp1, a, st);
-  }
-}
-
-void stencil_sweep_run(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1,
-                       const int* b_rp, const int* b_ci, const void* b_av, const int* a_rp,
-                       const int* a_ci, const void* a_av, void* d1, void* out, cudaStream_t st) {
-  ++sw.epoch;
-  if ((int64_t)(sw.epoch + 1) * sw.ipc > (int64_t)INT32_MAX) {  // counters restart
-    TFG_CUDA(cudaMemsetAsync(sw.done.p, 0, sw.done.bytes(), st));
-    sw.epoch = 1;
-  }
-  StencilArgs a{};
-  const StencilGeom& g = p0.g;
-  a.n = g.nx * g.ny * g.nz;
-  a.nx = g.nx;
-  a.ny = g.ny;
-  a.nz = g.nz;
-  a.nxy = g.nx * g.ny;
-  a.zb = 0;
-  a.ze = g.nz;
-  a.zc = p0.zc;
-  a.ns = p0.ns;
-  a.slices = p0.slices;
-  a.ntx = p0.ntx;
-  a.nty = p0.nty;
-  a.cc = p0.cc;
-  a.items = sw.nitems;
-  a.nzc = p0.nzc;
-  a.plane_elems = (int)(p0.plane_bytes / p0.elem);
-  fill_op(a.op[0], p0.g, b_rp, b_ci, b_av);
-  fill_op(a.op[1], p1.g, a_rp, a_ci, a_av);
-  a.out = d1;
-  a.out1 = out;
-  a.sweep_items = sw.items.p;
-  a.sweep_done = sw.done.p;
-  a.sweep_target = (int)(sw.epoch * sw.ipc);
-  if (p0.elem == 8) {
-    if (g.d3)
-      sweep_launch_d<double, true>(p0, p1, a, st);
-    else
-      sweep_launch_d<double, false>(p0, p1, a, st);
-  } else {
-    if (g.d3)
-      sweep_launch_d<float, true>(p0, p1, a, st);
-    else
-      sweep_launch_d<float, false>(p0, p1, a, st);
-  }
+    stencil_launch_t<float>(sp, a, st, exact);
 }
 
 }  // namespace tfg

@@ -69,34 +69,11 @@ bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& c
 // Planes [zb, ze) only (a row-block partition; -1: the whole grid).
 bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int cc, int elem,
                      int zb = 0, int ze = -1);
-// out[r, :] = sum_k av[k] * X[ci[k], :] over every row r of the matrix.
+// out[r, :] = sum_k av[k] * X[ci[k], :] over every row r of the matrix, in
+// ascending k; exact: separately rounded mul and add (the reference's bits),
+// else one fused multiply-add per term.
 void stencil_run(const StencilPlan& sp, const int* rp, const int* ci, const void* av, void* out,
-                 cudaStream_t st);
+                 cudaStream_t st, bool exact);
 int stencil_env_enabled();  // TFG_STENCIL (default 1)
-
-// Both SpMM passes of D = A (B C) (p0: B with X = C into D1, p1: A with X =
-// D1 into D) as one persistent dependency-driven kernel: second-op items
-// follow the first-op z chunks they read, so D1 is read back from L2.
-// Opt-in: TFG_STENCIL_SWEEP=1 (lag in chunk rows: TFG_STENCIL_SWEEP_LAG).
-struct StencilSweep {
-  bool on = false;
-  int64_t nitems = 0, ipc = 0;
-  uint32_t epoch = 0;
-  dbuf<int> items;  // op << 30 | item of op, launch order
-  dbuf<int> done;   // per z chunk: first-op items finished (cumulative over launches)
-};
-bool stencil_sweep_prepare(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1);
-void stencil_sweep_run(StencilSweep& sw, const StencilPlan& p0, const StencilPlan& p1,
-                       const int* b_rp, const int* b_ci, const void* b_av, const int* a_rp,
-                       const int* a_ci, const void* a_av, void* d1, void* out, cudaStream_t st);
-
-// Fused D = A (B C) for a pair of 2-D stencils on the same grid (gb: B, ga:
-// A), D1 kept on chip (registers).  false: not eligible or not enabled (the
-// plan keeps two stencil passes).  Opt-in: TFG_STENCIL_FUSE=1.
-bool stencil2_prepare(StencilPlan& sp, const StencilGeom& gb, const StencilGeom& ga,
-                      const void* C, int cc, int elem);
-void stencil2_run(const StencilPlan& sp, const int* b_rp, const int* b_ci, const void* b_av,
-                  const int* a_rp, const int* a_ci, const void* a_av, void* out,
-                  cudaStream_t st);
 
 }  // namespace tfg

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
                const int* __restrict__ slot, const uint8_t* __restrict__ spill, int stage_cap,
                int cc, const int* __restrict__ fx_aoff, const int64_t* __restrict__ fx_off,
                const int* __restrict__ fx_idx, const float* __restrict__ av, float* D1,
-               float* __restrict__ D, int dbg) {
+               float* __restrict__ D) {
   using R = Roles<CONV, EPI>;
   constexpr int kConv = R::kConv, kEpi = R::kEpi, kMmaWarp = R::kMmaWarp, kEpi0 = R::kEpi0;
   constexpr int VEC = 4;
@@ -325,13 +325,7 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
               x[4 * u + 3] = f.w;
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              if (dbg & 1) {
-                h[hv][i] = l[hv][i] = x[i];
-              } else {
-                split_tf32(x[i], h[hv][i], l[hv][i]);
-              }
-            }
+            for (int i = 0; i < 16; ++i) split_tf32(x[i], h[hv][i], l[hv][i]);
           }
           // the slot is refilled by the TMA (async proxy): order these generic
           // reads before that write, then release the slot
@@ -372,7 +366,6 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
                            cl = ch + (uint32_t)(BN * kKC * 4);
 #pragma unroll
             for (int ks = 0; ks < kKC / 8; ++ks) {
-              if ((dbg & 2) && (kc | ks)) break;
               const uint32_t o = (uint32_t)ks * 32;  // 8 tf32 = 32 bytes of the swizzled row
               mma_tf32_ts(d, al + ks * 8, sw128_desc(ch + o), kIdesc, (kc | ks) != 0);
               mma_tf32_ts(d, ah + ks * 8, sw128_desc(cl + o), kIdesc, 1);
@@ -411,13 +404,13 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
         for (int c0 = g * 16; c0 < BN; c0 += 16 * kEpiGroups) {
           float x[16];
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
-          if (sp && !(dbg & 8)) {
+          if (sp) {
             float4* o = reinterpret_cast<float4*>(D1 + (size_t)row * cc + n0 + c0);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
           }
-          if (sl >= 0 && !(dbg & 8)) {
+          if (sl >= 0) {
             float4* o = reinterpret_cast<float4*>(stage + (size_t)sl * BN + c0);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -429,7 +422,7 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
       }
       if (first_op) continue;
       const int64_t jb = t_joff[v], je = t_joff[v + 1];
-      if (je == jb || (dbg & 4)) continue;
+      if (je == jb) continue;
       named_sync();  // staged / spilled rows visible
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
@@ -562,10 +555,6 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
   (void)n;
   (void)bc;
   if (!ntiles) return;
-  static const int dbg = [] {
-    const char* e = getenv("TFG_TC_DBG");  // timing experiments only: skips work
-    return e ? atoi(e) : 0;
-  }();
   auto launch = [&](auto kern, int threads) {
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.smem));
     // all column slices of a tile run concurrently so B blocks are read from
@@ -574,7 +563,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
         std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, tc.smem, st>>>(
         tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
-        tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D, dbg);
+        tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D);
   };
   const bool fused = joff != nullptr;
   using F = Roles<4, 16>;

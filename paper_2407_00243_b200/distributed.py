@@ -132,7 +132,7 @@ class DistributedPlan:
 class GpuEngine:
     """libtfg partition plan on the current CUDA device."""
 
-    def __init__(self, problem, sched, lo, hi, stream=None):
+    def __init__(self, problem, sched, lo, hi, stream=None, reference_bits=False):
         import ctypes as C
 
         import torch
@@ -145,8 +145,11 @@ class GpuEngine:
         self.torch_dtype = getattr(torch, problem.dtype.name)
         self._p = problem.c_struct()
         h = C.c_void_p()
-        check(lib().tfg_plan_create_partition(C.byref(self._p), sched.handle, int(lo), int(hi),
-                                              _stream_ptr(stream), C.byref(h)))
+        from ._lib import PLAN_REFERENCE_BITS
+
+        check(lib().tfg_plan_create_ex(C.byref(self._p), sched.handle,
+                                       PLAN_REFERENCE_BITS if reference_bits else 0, int(lo),
+                                       int(hi), _stream_ptr(stream), C.byref(h)))
         self._h = h
         d1 = C.c_void_p()
         check(lib().tfg_plan_d1(h, C.byref(d1)))

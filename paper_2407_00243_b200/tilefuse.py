@@ -466,12 +466,19 @@ class DeviceProblem:
 class Plan:
     """Executor plan: schedule bound to a device problem (tfg_plan)."""
 
-    def __init__(self, problem: DeviceProblem, sched: Schedule | None, stream=None):
+    def __init__(self, problem: DeviceProblem, sched: Schedule | None, stream=None,
+                 reference_bits: bool = False):
+        """reference_bits: grid-stencil SpMM rows use the reference's separately
+        rounded multiply and add (bit-identical); default one FMA per term
+        (within the north-star tolerance).  tfg.h TFG_PLAN_REFERENCE_BITS."""
+        from ._lib import PLAN_REFERENCE_BITS
+
         self.problem = problem
         self._p = problem.c_struct()
         h = C.c_void_p()
-        check(lib().tfg_plan_create(C.byref(self._p), sched.handle if sched else None,
-                                    _stream_ptr(stream), C.byref(h)))
+        flags = PLAN_REFERENCE_BITS if reference_bits else 0
+        check(lib().tfg_plan_create_ex(C.byref(self._p), sched.handle if sched else None, flags,
+                                       0, -1, _stream_ptr(stream), C.byref(h)))
         self._h = h
         sp, fr = C.c_int64(), C.c_int64()
         la, sb = C.c_int32(), C.c_int64()

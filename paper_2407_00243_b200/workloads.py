@@ -180,30 +180,69 @@ def band_plus_random(n: int, half: int, extra: int, rng: np.random.Generator,
     return _csr_from_sorted(n, r, c, v, dtype)
 
 
+_M64 = (1 << 64) - 1
+
+
+def _i64(c: int) -> int:
+    """A uint64 constant as the int64 with the same bits."""
+    c &= _M64
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def _srl(x, k: int):
+    """Logical right shift of int64 bit patterns."""
+    return (x >> k) & ((1 << (64 - k)) - 1)
+
+
+def _mix64(x):
+    """splitmix64 finaliser on int64 tensors (wrapping arithmetic)."""
+    x = x ^ _srl(x, 30)
+    x = x * _i64(0xBF58476D1CE4E5B9)
+    x = x ^ _srl(x, 27)
+    x = x * _i64(0x94D049BB133111EB)
+    return x ^ _srl(x, 31)
+
+
+def _uniform(seed: int, idx, level: int):
+    """U[0,1) for draw `idx` at recursion level `level`: a counter-based hash,
+    so CPU and GPU produce identical bits (both arms of bench.py, and the
+    tests, see the same matrix whatever device generated it)."""
+    import torch
+
+    base = _i64(seed * 0xD1B54A32D192ED03 + level * 0x8CB92BA72F3D8DD7 + 0x9E3779B97F4A7C15)
+    x = _mix64(idx * _i64(0x9E3779B97F4A7C15) + base)
+    return _srl(x, 11).to(torch.float64) * (1.0 / (1 << 53))
+
+
 def rmat_pattern(scale: int, draws: int, seed: int, abc=(0.57, 0.19, 0.19), device=None):
     """Symmetrised, deduplicated R-MAT edge set without self loops, as sorted
-    (rows, cols) int64 numpy arrays.  Uses torch (on `device`, default CUDA
-    when available) for speed; deterministic per (seed, device type)."""
+    (rows, cols) int64 numpy arrays.  Each draw descends `scale` levels; at
+    level l it picks quadrant a / b / c / d from a counter-based uniform
+    (`_uniform`), so the result is identical on CPU and CUDA.  torch (on
+    `device`, default CUDA when available) only supplies the speed."""
     import torch
 
     if device is None:
         device = "cuda" if torch.cuda.is_available() else "cpu"
     a, b, c = abc
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
     n = 1 << scale
-    r = torch.zeros(draws, dtype=torch.int64, device=device)
-    col = torch.zeros(draws, dtype=torch.int64, device=device)
-    for _ in range(scale):
-        u = torch.rand(draws, generator=g, device=device)
-        rb = (u >= a + b).to(torch.int64)
-        cb = (((u >= a) & (u < a + b)) | (u >= a + b + c)).to(torch.int64)
-        r = r * 2 + rb
-        col = col * 2 + cb
-    keep = r != col
-    r, col = r[keep], col[keep]
-    key = torch.cat([r * n + col, col * n + r])
-    key = torch.unique(key)
+    chunk = 1 << 24
+    keys = []
+    for d0 in range(0, draws, chunk):
+        idx = torch.arange(d0, min(draws, d0 + chunk), dtype=torch.int64, device=device)
+        r = torch.zeros_like(idx)
+        col = torch.zeros_like(idx)
+        for lev in range(scale):
+            u = _uniform(seed, idx, lev)
+            rb = (u >= a + b).to(torch.int64)
+            cb = (((u >= a) & (u < a + b)) | (u >= a + b + c)).to(torch.int64)
+            r = r * 2 + rb
+            col = col * 2 + cb
+        keep = r != col
+        r, col = r[keep], col[keep]
+        keys.append(torch.cat([r * n + col, col * n + r]))
+        del idx, r, col
+    key = torch.unique(torch.cat(keys))
     rows = (key // n).cpu().numpy()
     cols = (key % n).cpu().numpy()
     return n, rows, cols

@@ -169,30 +169,3 @@ def test_poisoned_scratch_and_output(cuda, name, scale):
     got = plan.execute(out).cpu().numpy()
     assert not np.isnan(got).any()
     assert np.array_equal(got, want)
-
-
-def test_band_sweep_bit_exact(cuda, monkeypatch):
-    """The opt-in dependency-driven band sweep (TFG_SWEEP=1: first op and
-    wavefront 1 in one kernel with per-chunk completion counters) computes
-    the same D bits as the two-pass execution, on repeated executions (the
-    counters carry an epoch)."""
-    import torch
-
-    from paper_2407_00243_b200 import workloads as W
-
-    for name, scale in (("cfg2", 1 / 4), ("cfg4", 1 / 8)):
-        w = W.make(name, scale=scale)
-        s = P.build_schedule(w.a, w.scheduler_config())
-        prob = P.DeviceProblem(w.a, w.b, w.c, w.dtype)
-        monkeypatch.setenv("TFG_SWEEP", "0")
-        want = P.Plan(prob, s).execute().cpu().numpy()
-        monkeypatch.setenv("TFG_SWEEP", "1")
-        monkeypatch.setenv("TFG_STENCIL", "0")  # the stencil kernel takes stencils by default
-        plan = P.Plan(prob, s)
-        monkeypatch.setenv("TFG_STENCIL", "1")
-        assert plan.launches == 1, name  # both passes in the one sweep kernel
-        out = torch.full((w.n, w.c_cols), float("nan"), dtype=getattr(torch, w.dtype.name),
-                         device="cuda")
-        for _ in range(3):
-            out.fill_(float("nan"))
-            assert np.array_equal(plan.execute(out).cpu().numpy(), want), name

@@ -217,7 +217,8 @@ def test_baseline_configs(cuda, oracle, name):
     cfg = w.scheduler_config()
     s = P.build_schedule(w.a, cfg)
     prob = P.DeviceProblem(w.a, w.b, w.c, w.dtype)
-    got = P.Plan(prob, s).execute().cpu().numpy()
+    got = P.Plan(prob, s).execute().cpu().numpy()  # default: FMA stencil terms
+    exact = P.Plan(prob, s, reference_bits=True).execute().cpu().numpy()
     ocfg = SchedulerConfig(**cfg.__dict__)
     osched = oracle.build_schedule(w.n, w.n, w.a.row_ptr, w.a.col_idx, ocfg)
     ob = w.b if not isinstance(w.b, P.Csr) else (w.b.row_ptr, w.b.col_idx, w.b.values, w.b.n_cols)
@@ -225,5 +226,6 @@ def test_baseline_configs(cuda, oracle, name):
                       workers=os.cpu_count() or 1)
     size = np.dtype(w.dtype).itemsize
     assert max_rel_err(got, want) <= TOL[size]
+    assert max_rel_err(exact, want) <= TOL[size]
     if w.op == "spmm-spmm":
-        assert np.array_equal(got, want)
+        assert np.array_equal(exact, want)

@@ -25,7 +25,7 @@ def test_emulated_ranks_match_oracle(cuda, oracle, name, world):
     sched = P.build_schedule(prob.a, cfg)
     flat = sched.export()
     bounds = PD.tile_boundaries(flat, w.n, world)
-    engines = [PD.GpuEngine(prob, sched, *bounds[r]) for r in range(world)]
+    engines = [PD.GpuEngine(prob, sched, *bounds[r], reference_bits=True) for r in range(world)]
     halos = [PD.halo_plan(w.a.row_ptr, w.a.col_idx, flat, bounds, r) for r in range(world)]
     outs = [torch.full((w.n, w.c_cols), float("nan"), dtype=engines[0].torch_dtype, device="cuda")
             for _ in range(world)]
