@@ -63,15 +63,15 @@ void tfg_config_default(tfg_config *cfg);
 tfg_status tfg_device_info(int32_t *built_arch, int32_t *sm_count);
 
 /* ---------------------------------------------------------------------
- * Inspector (replaces scheduler.hpp:266-310 / scheduler.cpp:124-252)
+ * Inspector (replaces scheduler.hpp:67-111 / scheduler.cpp:124-252)
  * ------------------------------------------------------------------- */
 
-/* choose_tile_size -- scheduler.hpp:266, scheduler.cpp:124-129.
+/* choose_tile_size -- scheduler.hpp:67, scheduler.cpp:124-129.
  * Host arithmetic on three scalars.  EINVAL if any input < 1. */
 tfg_status tfg_choose_tile_size(int32_t n, int32_t num_workers,
                                 int32_t ct_size, int32_t *out);
 
-/* build_schedule -- scheduler.hpp:300-301, scheduler.cpp:212-245.
+/* build_schedule -- scheduler.hpp:101-102, scheduler.cpp:212-245.
  * GPU inspector over a device-resident CSR pattern (row_ptr n_rows+1,
  * col_idx nnz; columns strictly increasing per row).  Produces a schedule
  * bit-identical to the reference's (tile order, i ranges, j lists and
@@ -119,13 +119,13 @@ tfg_status tfg_schedule_import(int32_t n, int32_t tile_size,
 
 void tfg_schedule_destroy(tfg_schedule *s);
 
-/* fused_ratio -- scheduler.hpp:304, scheduler.cpp:247-252 (Eq. 2). */
+/* fused_ratio -- scheduler.hpp:105, scheduler.cpp:247-252 (Eq. 2). */
 double tfg_fused_ratio(const tfg_schedule *s);
 
-/* validate_schedule -- scheduler.hpp:308-310, scheduler.cpp:254-390.
+/* validate_schedule -- scheduler.hpp:109-111, scheduler.cpp:254-390.
  * Host-side checker over host CSR pattern + a schedule (the verify path,
  * not the hot path).  *pass = 1 when no violation; the first message goes
- * to msg (may be NULL). */
+ * to msg (may be NULL); tfg_validate_messages returns all of them. */
 tfg_status tfg_validate_schedule(int32_t n_rows, int32_t n_cols,
                                  const int32_t *h_row_ptr,
                                  const int32_t *h_col_idx,
@@ -133,6 +133,36 @@ tfg_status tfg_validate_schedule(int32_t n_rows, int32_t n_cols,
                                  int32_t *pass, int64_t *n_violations,
                                  int64_t *over_budget_width1, char *msg,
                                  size_t msg_cap);
+
+/* Every violation message of the calling thread's last
+ * tfg_validate_schedule, newline separated (ValidationReport::violations,
+ * scheduler.hpp:60-65).  *needed = bytes including the terminator. */
+tfg_status tfg_validate_messages(char *buf, size_t cap, size_t *needed);
+
+/* tile_cost -- scheduler.hpp:86-87, scheduler.cpp:196-200 (Eq. 3 over the
+ * tile's j rows; distinct columns anywhere in the matrix).  Host pattern;
+ * runs the inspector's cost kernel on the device. */
+tfg_status tfg_tile_cost(int32_t n, const int32_t *h_row_ptr, const int32_t *h_col_idx,
+                         int32_t i_lo, int32_t i_hi, const int32_t *h_j_rows, int64_t n_j,
+                         const tfg_config *cfg, double *cost);
+
+/* split_tile -- scheduler.hpp:89-97, scheduler.cpp:66-93 / :202-210: the
+ * inspector's split kernel on one tile whose j rows read only columns in
+ * [i_lo, i_hi) (the tiles step 1 produces; EINVAL otherwise).  Pieces in DFS
+ * pre-order (cost-bounded or width 1), j rows per piece by h_j_off; demoted
+ * rows ascending.  Buffers: pieces <= i_hi - i_lo, j / demoted <= n_j. */
+tfg_status tfg_split_tile(int32_t n, const int32_t *h_row_ptr, const int32_t *h_col_idx,
+                          int32_t i_lo, int32_t i_hi, const int32_t *h_j_rows, int64_t n_j,
+                          const tfg_config *cfg, int64_t *n_pieces, int32_t *h_lo,
+                          int32_t *h_hi, double *h_cost, int64_t *h_j_off, int32_t *h_j_out,
+                          int64_t *n_demoted, int32_t *h_demoted);
+
+/* balance -- scheduler.hpp:80-82, scheduler.cpp:163-194: greedy contiguous
+ * chunking of a weight list (the inspector's k_balance).  h_chunk_start
+ * [num_chunks + 1]: chunk c is items [start[c], start[c + 1]); trailing
+ * chunks may be empty.  EINVAL when num_chunks < 1. */
+tfg_status tfg_balance(int64_t n_items, const int64_t *h_weights, int64_t num_chunks,
+                       int64_t *h_chunk_start);
 
 /* ---------------------------------------------------------------------
  * Executor (replaces kernels.hpp:182-236: fused_gemm_spmm,
@@ -259,28 +289,61 @@ tfg_status tfg_spmm_rows_host(int32_t dtype, int32_t a_rows, int32_t a_cols,
                               const int32_t *h_rows, int64_t n_rows, void *h_d);
 
 /* ---------------------------------------------------------------------
- * Multi-GPU row-block partition helpers: halo pack / unpack of
- * D1 rows around the NCCL exchange.  rows: device int32 list.
+ * Multi-GPU row-block partition.  The reference has no
+ * distributed mode; its wavefront barrier (kernels.hpp:102-120) is where the
+ * one exchange step sits: wavefront 0 is communication-free when the cuts
+ * fall on tile boundaries (the dependence closure, scheduler.cpp:336-351),
+ * and before wavefront 1 each rank needs the D1 rows its wavefront-1 rows
+ * read from other blocks.  One process per GPU; the caller owns the NCCL
+ * communicator (any NCCL already loaded in the process is used, else
+ * libnccl.so.2).
  * ------------------------------------------------------------------- */
+typedef struct tfg_halo tfg_halo;
+#define TFG_HALO_AUTO 0      /* cost model picks EXCHANGE or RECOMPUTE          */
+#define TFG_HALO_EXCHANGE 1  /* NCCL send/recv of the D1 halo rows              */
+#define TFG_HALO_RECOMPUTE 2 /* GeMM-SpMM: halo D1 rows recomputed from local B */
+
+/* NCCL communicator helpers (same NCCL library the exchange calls). */
+tfg_status tfg_nccl_unique_id(void *id_out, size_t cap /* >= 128 */);
+tfg_status tfg_nccl_comm_init(int32_t nranks, const void *id, int32_t rank, void **comm);
+tfg_status tfg_nccl_comm_destroy(void *comm);
+
+/* Row-block cuts for `world` ranks at wavefront-0 tile starts, balanced by
+ * estimated bytes per row (first op + wavefront-1 gathers), written to
+ * h_bounds[world + 1].  h_row_ptr: A's host row_ptr. */
+tfg_status tfg_partition_bounds(const tfg_schedule *s, const int32_t *h_row_ptr,
+                                int32_t b_cols, int32_t c_cols, int32_t dtype,
+                                int32_t b_is_dense, int32_t world, int32_t *h_bounds);
+
+/* The halo of rank `rank`'s partition plan (tfg_plan_create_partition /
+ * _ex with its row block): per-peer recv / send D1 row lists computed on the
+ * device from the replicated pattern and schedule; with EXCHANGE the
+ * wavefront-1 rows that read only local D1 are split off so they run while
+ * NCCL moves the halo.  mode: TFG_HALO_*; AUTO compares the NVLink time of
+ * the halo rows with recomputing them from B (GeMM-SpMM only). */
+tfg_status tfg_halo_create(tfg_plan *plan, const tfg_schedule *s, const int32_t *h_bounds,
+                           int32_t world, int32_t rank, int32_t mode, void *stream,
+                           tfg_halo **out);
+tfg_status tfg_halo_info(const tfg_halo *h, int32_t *mode, int64_t *recv_rows,
+                         int64_t *send_rows, double *t_exchange_us, double *t_recompute_us);
+void tfg_halo_destroy(tfg_halo *h);
+
+/* One step of the partitioned product on this rank into d_d (global row
+ * indexing; this rank's rows written): wavefront 0; then the halo (grouped
+ * ncclSend/ncclRecv on an internal stream, overlapped with the local-only
+ * wavefront-1 rows) or its recomputation; then the remaining wavefront-1
+ * rows.  nccl_comm: ncclComm_t (may be NULL for RECOMPUTE or world 1). */
+tfg_status tfg_plan_execute_dist(tfg_plan *plan, tfg_halo *halo, void *nccl_comm, void *d_d,
+                                 void *stream);
+
+/* Halo pack / unpack of D1 rows around a caller-driven exchange.  rows:
+ * device int32 list. */
 tfg_status tfg_gather_rows(int32_t dtype, const void *d_src, int32_t cols,
                            const int32_t *d_rows, int64_t n_rows,
                            void *d_dst, void *stream);
 tfg_status tfg_scatter_rows(int32_t dtype, const void *d_src, int32_t cols,
                             const int32_t *d_rows, int64_t n_rows,
                             void *d_dst, void *stream);
-
-/* ---------------------------------------------------------------------
- * Host generators the reference's Python module exposes
- * (generate.hpp:15-94; bindings.cpp:111-114).  malloc'd outputs, release
- * with tfg_free.  Deterministic for (n, density, seed).
- * ------------------------------------------------------------------- */
-tfg_status tfg_gen_random_sparse(int32_t n, double density, uint64_t seed,
-                                 int32_t **row_ptr, int32_t **col_idx,
-                                 double **values);
-tfg_status tfg_gen_banded(int32_t n, int32_t half_bandwidth,
-                          int32_t **row_ptr, int32_t **col_idx,
-                          double **values);
-void tfg_free(void *p);
 
 #ifdef __cplusplus
 }

@@ -1,7 +1,9 @@
 // tilefuse/scheduler.hpp -- drop-in inspector API over libtfg (tfg.h).
 //
 // Keeps the reference's names, types and signatures
-// (include/tilefuse/scheduler.hpp:15-111).  build_schedule runs the sm_100a
+// (include/tilefuse/scheduler.hpp:15-111): choose_tile_size,
+// step1_coarse_fuse, balance, tile_cost, split_tile, build_schedule,
+// fused_ratio and validate_schedule all run the GPU inspector's kernels.  build_schedule runs the sm_100a
 // GPU inspector and returns the same FusedSchedule, bit for bit, as the
 // reference's CPU inspector for the same SchedulerConfig.  Link with
 // -ltfg (paper_2407_00243_b200/libtfg.so).
@@ -9,6 +11,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <algorithm>
 #include <limits>
 #include <stdexcept>
 #include <string>
@@ -198,6 +201,72 @@ inline IntermediateSchedule step1_coarse_fuse(const SparsityView& a, index_t til
   return out;
 }
 
+// scheduler.cpp:163-194 -- the inspector's k_balance on the list's weights
+// (weight of an item = row_weight[row]).
+inline std::vector<std::vector<index_t>> balance(const std::vector<index_t>& rows,
+                                                 const std::vector<index_t>& row_weight,
+                                                 std::size_t num_chunks) {
+  std::vector<int64_t> w(rows.size());
+  for (std::size_t q = 0; q < rows.size(); ++q) {
+    const auto r = static_cast<std::size_t>(rows[q]);
+    if (r >= row_weight.size()) throw std::invalid_argument("balance: row without a weight");
+    w[q] = row_weight[r];
+  }
+  std::vector<int64_t> start(num_chunks + 1, 0);
+  detail::tfg_check(tfg_balance(static_cast<int64_t>(rows.size()), w.empty() ? nullptr : w.data(),
+                                static_cast<int64_t>(num_chunks), start.data()));
+  std::vector<std::vector<index_t>> out(num_chunks);
+  for (std::size_t c = 0; c < num_chunks; ++c)
+    out[c].assign(rows.begin() + start[c], rows.begin() + start[c + 1]);
+  return out;
+}
+
+// scheduler.cpp:196-200 (Eq. 3) -- the inspector's cost kernel on one tile.
+inline double tile_cost(const SparsityView& a, const FusedTile& tile, const SchedulerConfig& cfg) {
+  const tfg_config c = detail::to_c(cfg);
+  double cost = 0.0;
+  const int32_t dummy = 0;
+  detail::tfg_check(tfg_tile_cost(a.n_rows, a.row_ptr.data(),
+                                  a.col_idx.empty() ? &dummy : a.col_idx.data(), tile.i_lo,
+                                  tile.i_hi, tile.j_rows.empty() ? &dummy : tile.j_rows.data(),
+                                  static_cast<int64_t>(tile.j_rows.size()), &c, &cost));
+  return cost;
+}
+
+struct SplitResult {
+  std::vector<FusedTile> pieces;      // cost-bounded or width 1, DFS pre-order
+  std::vector<index_t> demoted_rows;  // rows evicted while splitting (ascending)
+};
+
+// scheduler.cpp:66-93 / :202-210 -- the inspector's split kernel on one tile
+// (a tile step 1 produces: its j rows read only columns inside it).
+inline SplitResult split_tile(const SparsityView& a, FusedTile tile, const SchedulerConfig& cfg) {
+  const tfg_config c = detail::to_c(cfg);
+  const auto w = static_cast<std::size_t>(std::max<index_t>(tile.i_hi - tile.i_lo, 1));
+  const std::size_t nj = tile.j_rows.size();
+  std::vector<int32_t> lo(w), hi(w), jout(nj + 1), dem(nj + 1);
+  std::vector<double> cost(w);
+  std::vector<int64_t> joff(w + 1);
+  int64_t np = 0, nd = 0;
+  const int32_t dummy = 0;
+  detail::tfg_check(tfg_split_tile(a.n_rows, a.row_ptr.data(),
+                                   a.col_idx.empty() ? &dummy : a.col_idx.data(), tile.i_lo,
+                                   tile.i_hi, nj ? tile.j_rows.data() : &dummy,
+                                   static_cast<int64_t>(nj), &c, &np, lo.data(), hi.data(),
+                                   cost.data(), joff.data(), jout.data(), &nd, dem.data()));
+  SplitResult r;
+  for (int64_t q = 0; q < np; ++q) {
+    FusedTile p;
+    p.i_lo = lo[q];
+    p.i_hi = hi[q];
+    p.cost = cost[q];
+    p.j_rows.assign(jout.begin() + joff[q], jout.begin() + joff[q + 1]);
+    r.pieces.push_back(std::move(p));
+  }
+  r.demoted_rows.assign(dem.begin(), dem.begin() + nd);
+  return r;
+}
+
 // scheduler.cpp:247-252 (Eq. 2)
 inline double fused_ratio(const FusedSchedule& sched) {
   if (sched.n < 1 || sched.wavefronts.empty()) return 0.0;
@@ -206,7 +275,8 @@ inline double fused_ratio(const FusedSchedule& sched) {
   return static_cast<double>(fused) / (2.0 * static_cast<double>(sched.n));
 }
 
-// scheduler.cpp:254-390 (verify path; reports the first violation).
+// scheduler.cpp:254-390 (verify path; every violation, in the reference's
+// check order).
 inline ValidationReport validate_schedule(const SparsityView& a, const FusedSchedule& sched,
                                           const SchedulerConfig& cfg) {
   ValidationReport rep;
@@ -227,7 +297,19 @@ inline ValidationReport validate_schedule(const SparsityView& a, const FusedSche
                                           &pass, &nv, &ob, msg, sizeof msg));
   rep.pass = pass != 0;
   rep.over_budget_width1 = static_cast<std::size_t>(ob);
-  if (!rep.pass) rep.violations.emplace_back(msg);
+  if (!rep.pass) {
+    std::size_t need = 0;
+    detail::tfg_check(tfg_validate_messages(nullptr, 0, &need));
+    std::string all(need, '\0');
+    detail::tfg_check(tfg_validate_messages(&all[0], need, &need));
+    all.resize(need ? need - 1 : 0);
+    std::size_t b = 0;
+    while (b <= all.size()) {
+      const std::size_t e = std::min(all.find('\n', b), all.size());
+      if (e > b) rep.violations.push_back(all.substr(b, e - b));
+      b = e + 1;
+    }
+  }
   return rep;
 }
 

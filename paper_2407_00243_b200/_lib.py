@@ -82,6 +82,13 @@ SIGNATURES = [
     ("tfg_validate_schedule", C.c_int, [C.c_int32, C.c_int32, i32p, i32p, C.c_void_p,
                                         C.POINTER(TfgConfig), i32p, i64p, i64p, C.c_char_p,
                                         C.c_size_t]),
+    ("tfg_validate_messages", C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("tfg_tile_cost", C.c_int, [C.c_int32, i32p, i32p, C.c_int32, C.c_int32, i32p, C.c_int64,
+                                C.POINTER(TfgConfig), C.POINTER(C.c_double)]),
+    ("tfg_split_tile", C.c_int, [C.c_int32, i32p, i32p, C.c_int32, C.c_int32, i32p, C.c_int64,
+                                 C.POINTER(TfgConfig), i64p, i32p, i32p, C.POINTER(C.c_double),
+                                 i64p, i32p, i64p, i32p]),
+    ("tfg_balance", C.c_int, [C.c_int64, i64p, C.c_int64, i64p]),
     ("tfg_plan_create", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
     ("tfg_plan_create_ex", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_uint32, C.c_int32,
@@ -105,11 +112,7 @@ SIGNATURES = [
                                   C.c_void_p, C.c_void_p]),
     ("tfg_scatter_rows", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
                                    C.c_void_p, C.c_void_p]),
-    ("tfg_gen_random_sparse", C.c_int, [C.c_int32, C.c_double, C.c_uint64, C.POINTER(i32p),
-                                        C.POINTER(i32p), C.POINTER(f64p)]),
-    ("tfg_gen_banded", C.c_int, [C.c_int32, C.c_int32, C.POINTER(i32p), C.POINTER(i32p),
-                                 C.POINTER(f64p)]),
-    ("tfg_free", None, [C.c_void_p]),
+
 ]
 
 _lib = None

@@ -23,11 +23,21 @@ void plan_execute(tfg_plan& pl, void* d, cudaStream_t st, cudaEvent_t* ev);
 size_t plan_scratch_bytes(const tfg_plan& pl);
 void gather_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
                  void* dst, cudaStream_t st);
+double tile_cost_device(int n, const int* rp, const int* ci, int i_lo, int i_hi,
+                        const int* jrows, int nj, const tfg_config& cfg, cudaStream_t st);
+void split_tile_device(int n, const int* rp, const int* ci, int i_lo, int i_hi, const int* jrows,
+                       int nj, const tfg_config& cfg, cudaStream_t st, std::vector<int>& lo,
+                       std::vector<int>& hi, std::vector<double>& cost,
+                       std::vector<int64_t>& joff, std::vector<int>& jout,
+                       std::vector<int>& demoted);
+void balance_device(int64_t U, const int64_t* h_w, int64_t num_chunks, int64_t* h_starts,
+                    cudaStream_t st);
 void scatter_rows(int dtype, const void* src, int cols, const int* rows, int64_t n,
                   void* dst, cudaStream_t st);
 
 namespace {
 thread_local std::string g_last_error;
+thread_local std::string g_violations;  // all messages of the last tfg_validate_schedule
 }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
@@ -371,6 +381,10 @@ tfg_status tfg_validate_schedule(int32_t n_rows, int32_t n_cols, const int32_t* 
     *pass = v.empty() ? 1 : 0;
     if (nviol) *nviol = (int64_t)v.size();
     if (ob1) *ob1 = over;
+    // every violation, newline separated (scheduler.cpp:258-261 keeps them all)
+    std::string all;
+    for (size_t q = 0; q < v.size(); ++q) all += (q ? "\n" : "") + v[q];
+    g_violations = all;
     if (msg && cap) {
       msg[0] = 0;
       if (!v.empty()) {
@@ -381,74 +395,88 @@ tfg_status tfg_validate_schedule(int32_t n_rows, int32_t n_cols, const int32_t* 
   });
 }
 
-// ---- host generators (generate.hpp:15-94), std::mt19937_64 as the reference
-static void export_csr(const std::vector<int32_t>& rp, const std::vector<int32_t>& ci,
-                       const std::vector<double>& v, int32_t** orp, int32_t** oci,
-                       double** ov) {
-  *orp = (int32_t*)std::malloc((rp.size() + 1) * sizeof(int32_t));
-  *oci = (int32_t*)std::malloc((ci.size() + 1) * sizeof(int32_t));
-  *ov = (double*)std::malloc((v.size() + 1) * sizeof(double));
-  std::memcpy(*orp, rp.data(), rp.size() * sizeof(int32_t));
-  if (!ci.empty()) std::memcpy(*oci, ci.data(), ci.size() * sizeof(int32_t));
-  if (!v.empty()) std::memcpy(*ov, v.data(), v.size() * sizeof(double));
-}
-
-tfg_status tfg_gen_random_sparse(int32_t n, double density, uint64_t seed, int32_t** orp,
-                                 int32_t** oci, double** ov) {
+tfg_status tfg_validate_messages(char* buf, size_t cap, size_t* needed) {
   return guard([&] {
-    if (n < 1) throw invalid_argument("gen_random_sparse: n must be >= 1");
-    if (!(density > 0.0) || density > 1.0)
-      throw invalid_argument("gen_random_sparse: density must be in (0,1]");
-    std::mt19937_64 rng(seed);
-    auto unit_open = [&] { return ((double)(rng() >> 11) + 0.5) * 0x1.0p-53; };
-    auto value = [&] { return 0.1 + 0.9 * (double)(rng() >> 11) * 0x1.0p-53; };
-    std::vector<int32_t> rp{0}, ci;
-    std::vector<double> v;
-    const bool full = density >= 1.0;
-    const double log_skip = full ? 0.0 : std::log1p(-density);
-    for (int32_t r = 0; r < n; ++r) {
-      const size_t start = ci.size();
-      if (full) {
-        for (int32_t c = 0; c < n; ++c) {
-          ci.push_back(c);
-          v.push_back(value());
-        }
-      } else {
-        int64_t c = -1;
-        for (;;) {
-          c += 1 + (int64_t)std::floor(std::log(unit_open()) / log_skip);
-          if (c >= n) break;
-          ci.push_back((int32_t)c);
-          v.push_back(value());
-        }
-      }
-      if (ci.size() == start) {
-        ci.push_back(r);
-        v.push_back(value());
-      }
-      rp.push_back((int32_t)ci.size());
+    if (needed) *needed = g_violations.size() + 1;
+    if (buf && cap) {
+      const size_t k = std::min(cap - 1, g_violations.size());
+      std::memcpy(buf, g_violations.data(), k);
+      buf[k] = 0;
     }
-    export_csr(rp, ci, v, orp, oci, ov);
   });
 }
 
-tfg_status tfg_gen_banded(int32_t n, int32_t hb, int32_t** orp, int32_t** oci, double** ov) {
+// ---- single inspector steps (scheduler.hpp:80-97) ------------------------
+namespace {
+struct HostPattern {  // a host CSR pattern on the device for one call
+  dbuf<int32_t> rp, ci, jr;
+  HostPattern(int32_t n, const int32_t* h_rp, const int32_t* h_ci, const int32_t* h_j, int64_t nj,
+              cudaStream_t st)
+      : rp(n + 1), ci(std::max<int64_t>(h_rp[n], 1)), jr(std::max<int64_t>(nj, 1)) {
+    h2d(rp.p, h_rp, n + 1, st);
+    h2d(ci.p, h_ci, h_rp[n], st);
+    h2d(jr.p, h_j, nj, st);
+  }
+};
+void check_tile_args(int32_t n, const int32_t* h_rp, const int32_t* h_j, int64_t nj,
+                     const tfg_config* cfg, const char* who) {
+  if (!h_rp || !cfg || (nj > 0 && !h_j)) throw invalid_argument(std::string(who) + ": null argument");
+  if (n < 1) throw invalid_argument(std::string(who) + ": matrix must be nonempty");
+  for (int64_t q = 0; q < nj; ++q)
+    if (h_j[q] < 0 || h_j[q] >= n) throw invalid_argument(std::string(who) + ": j row out of range");
+}
+}  // namespace
+
+tfg_status tfg_tile_cost(int32_t n, const int32_t* h_row_ptr, const int32_t* h_col_idx,
+                         int32_t i_lo, int32_t i_hi, const int32_t* h_j_rows, int64_t n_j,
+                         const tfg_config* cfg, double* cost) {
   return guard([&] {
-    if (n < 1) throw invalid_argument("gen_banded: n must be >= 1");
-    if (hb < 0 || hb >= n) throw invalid_argument("gen_banded: need 0 <= half_bandwidth < n");
-    std::vector<int32_t> rp{0}, ci;
-    std::vector<double> v;
-    for (int32_t r = 0; r < n; ++r) {
-      for (int32_t c = std::max(0, r - hb); c <= std::min(n - 1, r + hb); ++c) {
-        ci.push_back(c);
-        v.push_back(1.0);
-      }
-      rp.push_back((int32_t)ci.size());
-    }
-    export_csr(rp, ci, v, orp, oci, ov);
+    check_tile_args(n, h_row_ptr, h_j_rows, n_j, cfg, "tile_cost");
+    cudaStream_t st = nullptr;
+    HostPattern hp(n, h_row_ptr, h_col_idx, h_j_rows, n_j, st);
+    *cost = tile_cost_device(n, hp.rp.p, hp.ci.p, i_lo, i_hi, hp.jr.p, (int)n_j, *cfg, st);
   });
 }
 
-void tfg_free(void* p) { std::free(p); }
+tfg_status tfg_split_tile(int32_t n, const int32_t* h_row_ptr, const int32_t* h_col_idx,
+                          int32_t i_lo, int32_t i_hi, const int32_t* h_j_rows, int64_t n_j,
+                          const tfg_config* cfg, int64_t* n_pieces, int32_t* h_lo, int32_t* h_hi,
+                          double* h_cost, int64_t* h_j_off, int32_t* h_j_out, int64_t* n_demoted,
+                          int32_t* h_demoted) {
+  return guard([&] {
+    check_tile_args(n, h_row_ptr, h_j_rows, n_j, cfg, "split_tile");
+    for (int64_t q = 0; q < n_j; ++q) {  // j rows of a step-1 tile: columns inside it
+      const int j = h_j_rows[q];
+      for (int k = h_row_ptr[j]; k < h_row_ptr[j + 1]; ++k)
+        if (h_col_idx[k] < i_lo || h_col_idx[k] >= i_hi)
+          throw invalid_argument("split_tile: a j row reads outside the tile's i range");
+    }
+    cudaStream_t st = nullptr;
+    HostPattern hp(n, h_row_ptr, h_col_idx, h_j_rows, n_j, st);
+    std::vector<int> lo, hi, jout, dem;
+    std::vector<double> cost;
+    std::vector<int64_t> joff;
+    split_tile_device(n, hp.rp.p, hp.ci.p, i_lo, i_hi, hp.jr.p, (int)n_j, *cfg, st, lo, hi, cost,
+                      joff, jout, dem);
+    *n_pieces = (int64_t)lo.size();
+    *n_demoted = (int64_t)dem.size();
+    if (h_lo) std::copy(lo.begin(), lo.end(), h_lo);
+    if (h_hi) std::copy(hi.begin(), hi.end(), h_hi);
+    if (h_cost) std::copy(cost.begin(), cost.end(), h_cost);
+    if (h_j_off) std::copy(joff.begin(), joff.end(), h_j_off);
+    if (h_j_out) std::copy(jout.begin(), jout.end(), h_j_out);
+    if (h_demoted) std::copy(dem.begin(), dem.end(), h_demoted);
+  });
+}
+
+tfg_status tfg_balance(int64_t n_items, const int64_t* h_weights, int64_t num_chunks,
+                       int64_t* h_chunk_start) {
+  return guard([&] {
+    if (num_chunks < 1) throw invalid_argument("balance: num_chunks must be >= 1");
+    if (n_items < 0 || (n_items > 0 && !h_weights) || !h_chunk_start)
+      throw invalid_argument("balance: null argument");
+    balance_device(n_items, h_weights, num_chunks, h_chunk_start, nullptr);
+  });
+}
 
 }  // extern "C"

@@ -38,6 +38,7 @@
 #include "tfg_device.cuh"
 #include "tfg_tc.cuh"
 #include "tfg_stencil.cuh"
+#include "tfg_nccl.cuh"
 
 namespace tfg {
 namespace {
@@ -1291,6 +1292,35 @@ __global__ void k_gather_rows(const T* __restrict__ src, int cols,
     dst[e] = src[(size_t)rows[r] * cols + c];
   }
 }
+// Multi-GPU halo: bit q of mask[c] is set when a wavefront-1 row owned by
+// rank q (row block [bounds[q], bounds[q+1])) reads column c.
+__global__ void k_mark_readers(int64_t nrows, const int* __restrict__ rows,
+                               const int* __restrict__ rp, const int* __restrict__ ci,
+                               const int* __restrict__ bounds, int world,
+                               unsigned* __restrict__ mask) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  const int j = rows[w];
+  int q = 0;
+  while (q + 1 < world && j >= bounds[q + 1]) ++q;
+  for (int k = rp[j] + lane; k < rp[j + 1]; k += 32) atomicOr(mask + ci[k], 1u << q);
+}
+
+// flag[i] = 1 when row rows[i] reads a column outside [lo, hi)
+__global__ void k_reads_remote(int64_t nrows, const int* __restrict__ rows,
+                               const int* __restrict__ rp, const int* __restrict__ ci, int lo,
+                               int hi, uint8_t* __restrict__ flag) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  const int j = rows[w];
+  bool remote = false;
+  for (int k = rp[j] + lane; k < rp[j + 1] && !remote; k += 32) remote = ci[k] < lo || ci[k] >= hi;
+  remote = __any_sync(0xffffffffu, remote);
+  if (lane == 0) flag[w] = remote;
+}
+
 // D[rows[i], :] = 0 (empty rows of a row list), 16-byte stores
 __global__ void k_zero_rows(int64_t nrows, const int* __restrict__ rows, int row_bytes,
                             unsigned char* __restrict__ out) {
@@ -1830,11 +1860,36 @@ struct tfg_plan {
   int64_t first_rows = 0, second_rows = 0, nnz_processed = 0;
   int launches = 0;
   int row_lo = 0, row_hi = 0;  // row block of a partition plan (multi-GPU)
+  std::vector<int> w1_rows;    // partition plans: the wavefront-1 row list (tfg_halo_create)
   // algorithmic (compulsory) HBM bytes per stage: (a) first op, (b) fused
   // tiles, (c) wavefront-1 SpMM -- each input byte read once, each output
   // byte written once (the roofline numerator)
   int64_t stage_bytes[3] = {0, 0, 0};
   int64_t d1_read_rows = 0;  // distinct D1 rows wavefront 1 reads
+};
+
+// Multi-GPU halo of one rank's partition plan (tfg_halo_create).
+struct tfg_halo {
+  int world = 1, rank = 0;
+  int mode = TFG_HALO_EXCHANGE;
+  int64_t n_recv = 0, n_send = 0;
+  std::vector<int64_t> recv_off, send_off;  // per peer, rows (world + 1)
+  tfg::dbuf<int> recv_rows, send_rows;      // global D1 rows, grouped by peer
+  tfg::dbuf<unsigned char> recv_buf, send_buf;
+  // recompute mode: first-op row blocks covering the halo rows
+  int64_t n_rblk = 0;
+  tfg::dbuf<int> r_r0, r_cnt, r_ihi;
+  // wavefront 1 split: rows reading only local D1 run during the exchange
+  bool split = false;
+  tfg::SpmmWork interior, boundary;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
+  double t_exchange_us = 0, t_recompute_us = 0;  // the cost model's estimates
+  ~tfg_halo() {
+    if (ev_packed) cudaEventDestroy(ev_packed);
+    if (ev_recv) cudaEventDestroy(ev_recv);
+    if (comm) cudaStreamDestroy(comm);
+  }
 };
 
 namespace tfg {
@@ -2267,6 +2322,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     const StencilGeom gA = same ? gB : probe_stencil(n, arp, aci);
     pl.second.build(second_rows, arp, cc, pl.elem, st, aci.empty() ? nullptr : &aci,
                     stencil_rows(second_rows, gA, cc, pl.elem));
+    if (partial) pl.w1_rows = second_rows;
     attach_stencil(pl.second, gA, pl.d1.p, cc, pl.elem);
   }
   phase("first-op + wave-1 work");
@@ -2352,8 +2408,8 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
 }
 
 template <class T, int BM, int BN, int BK, int TM, int TN>
-static void launch_gemm_v2_cfg(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
-                               cudaStream_t st) {
+static void launch_gemm_v2_cfg(int64_t nblk, const int* r0, const int* cnt, const T* B, int bc,
+                               const T* C, int cc, T* D1, cudaStream_t st) {
   using G = GemmCfg<T, BM, BN, BK, TM, TN, 3>;
   auto kern = k_gemm_stream<T, BM, BN, BK, TM, TN, 3>;
   static bool attr = false;
@@ -2363,9 +2419,9 @@ static void launch_gemm_v2_cfg(tfg_plan& pl, const T* B, int bc, const T* C, int
   }
   int per_sm = 1;
   TFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, G::SMEM));
-  const int64_t gx = std::min<int64_t>(pl.n_fo_blocks, (int64_t)sm_count() * std::max(per_sm, 1));
-  kern<<<dim3((unsigned)gx, cc / BN), G::THREADS, G::SMEM, st>>>(pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p,
-                                                          B, bc, C, cc, D1, cc);
+  const int64_t gx = std::min<int64_t>(nblk, (int64_t)sm_count() * std::max(per_sm, 1));
+  kern<<<dim3((unsigned)gx, cc / BN), G::THREADS, G::SMEM, st>>>(nblk, r0, cnt, B, bc, C, cc, D1,
+                                                                 cc);
   TFG_LAUNCH_CHECK();
 }
 
@@ -2402,18 +2458,44 @@ static void launch_fused_v2(tfg_plan& pl, T* D1, T* D, cudaStream_t st) {
 }
 
 template <class T>
-static void launch_gemm_v2(tfg_plan& pl, const T* B, int bc, const T* C, int cc, T* D1,
-                           cudaStream_t st) {
+static void launch_gemm_v2(tfg_plan& pl, int64_t nblk, const int* r0, const int* cnt, const T* B,
+                           int bc, const T* C, int cc, T* D1, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     if (pl.gemm_kind == 2)
-      launch_gemm_v2_cfg<T, 128, 128, 32, 8, 8>(pl, B, bc, C, cc, D1, st);
+      launch_gemm_v2_cfg<T, 128, 128, 32, 8, 8>(nblk, r0, cnt, B, bc, C, cc, D1, st);
     else
-      launch_gemm_v2_cfg<T, 128, 64, 32, 8, 4>(pl, B, bc, C, cc, D1, st);
+      launch_gemm_v2_cfg<T, 128, 64, 32, 8, 4>(nblk, r0, cnt, B, bc, C, cc, D1, st);
   } else {
     if (pl.gemm_kind == 2)
-      launch_gemm_v2_cfg<T, 64, 128, 16, 4, 8>(pl, B, bc, C, cc, D1, st);
+      launch_gemm_v2_cfg<T, 64, 128, 16, 4, 8>(nblk, r0, cnt, B, bc, C, cc, D1, st);
     else
-      launch_gemm_v2_cfg<T, 64, 64, 16, 8, 4>(pl, B, bc, C, cc, D1, st);
+      launch_gemm_v2_cfg<T, 64, 64, 16, 8, 4>(nblk, r0, cnt, B, bc, C, cc, D1, st);
+  }
+}
+
+// Dense first op D1[rows] = B[rows] C over row blocks (r0, cnt; ihi = r0 +
+// cnt for the tensor-core kernel): the plan's first-op kernel on any block
+// list (the plan's own, or a multi-GPU halo recomputed locally).
+template <class T>
+static void first_op_blocks(tfg_plan& pl, int64_t nblk, const int* r0, const int* cnt,
+                            const int* ihi, T* D1, cudaStream_t st) {
+  const tfg_problem& pr = pl.p;
+  const int cc = pr.c_cols, bc = pr.b_cols;
+  const T* C = static_cast<const T*>(pr.d_c);
+  if (!nblk) return;
+  if (pl.tc.on) {
+    if constexpr (sizeof(T) == 4)
+      tc_run(pl.tc, pr.n, bc, cc, nblk, r0, ihi, nullptr, nullptr, nullptr, nullptr, nullptr,
+             nullptr, nullptr, nullptr, nullptr, reinterpret_cast<float*>(D1), nullptr, st);
+  } else if (pl.gemm_kind) {
+    launch_gemm_v2<T>(pl, nblk, r0, cnt, static_cast<const T*>(pr.d_b_dense), bc, C, cc, D1, st);
+  } else {
+    const int gy = (cc + kGemmBN - 1) / kGemmBN;
+    const int64_t gx = std::min<int64_t>(nblk, (int64_t)sm_count() * 16);
+    k_gemm_blocks<T, kGemmBM, kGemmBN, kGemmBK, kGemmTM, kGemmTN>
+        <<<dim3((unsigned)gx, gy), (kGemmBM / kGemmTM) * (kGemmBN / kGemmTN), 0, st>>>(
+            nblk, r0, cnt, static_cast<const T*>(pr.d_b_dense), bc, C, cc, D1, cc);
+    TFG_LAUNCH_CHECK();
   }
 }
 
@@ -2433,22 +2515,7 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
       tc_prep_c(pl.tc, reinterpret_cast<const float*>(C), bc, cc, st);
   }
   if (pr.b_is_dense) {
-    if (pl.n_fo_blocks && pl.tc.on) {
-      if constexpr (sizeof(T) == 4)
-        tc_run(pl.tc, pr.n, bc, cc, pl.n_fo_blocks, pl.fo_r0.p, pl.fo_ihi.p, nullptr, nullptr,
-               nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-               reinterpret_cast<float*>(D1), nullptr, st);
-    } else if (pl.n_fo_blocks && pl.gemm_kind) {
-      launch_gemm_v2<T>(pl, static_cast<const T*>(pr.d_b_dense), bc, C, cc, D1, st);
-    } else if (pl.n_fo_blocks) {
-      const int gy = (cc + kGemmBN - 1) / kGemmBN;
-      const int64_t gx = std::min<int64_t>(pl.n_fo_blocks, (int64_t)sm_count() * 16);
-      k_gemm_blocks<T, kGemmBM, kGemmBN, kGemmBK, kGemmTM, kGemmTN>
-          <<<dim3((unsigned)gx, gy), (kGemmBM / kGemmTM) * (kGemmBN / kGemmTN), 0, st>>>(
-              pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p, static_cast<const T*>(pr.d_b_dense),
-              bc, C, cc, D1, cc);
-      TFG_LAUNCH_CHECK();
-    }
+    first_op_blocks<T>(pl, pl.n_fo_blocks, pl.fo_r0.p, pl.fo_cnt.p, pl.fo_ihi.p, D1, st);
   } else {
     spmm_run<T>(pl.fo_sparse, pr.d_b_row_ptr, pr.d_b_col_idx,
                 static_cast<const T*>(pr.d_b_val), C, cc, D1, st);
@@ -2533,6 +2600,215 @@ size_t plan_scratch_bytes(const tfg_plan& pl) {
          pl.ft_jrows.bytes() + pl.second.bytes();
 }
 
+
+// ---------------------------------------------------------------------------
+// Multi-GPU row-block partition: cuts, halo, one step.
+// ---------------------------------------------------------------------------
+
+// Row-block cuts at wavefront-0 tile starts, balanced by estimated bytes per
+// row: the first op (B row + D1 row) plus the second op (A row + one gathered
+// D1 row per nonzero + D row) -- the wavefront-1 gathers dominate skewed
+// matrices, so equal row counts would not balance them.
+void partition_bounds(const tfg_schedule& s, const int* rp, int bc, int cc, size_t elem,
+                      bool b_dense, int world, int* bounds) {
+  const int n = s.n;
+  std::vector<int> ilo(s.n_tiles[0]);
+  d2h(ilo.data(), s.i_lo[0].p, ilo.size(), nullptr);
+  TFG_CUDA(cudaStreamSynchronize(nullptr));
+  std::sort(ilo.begin(), ilo.end());
+  if (ilo.empty() || ilo[0] != 0) ilo.insert(ilo.begin(), 0);
+  std::vector<double> P(n + 1, 0.0);
+  const double e = (double)elem;
+  for (int i = 0; i < n; ++i) {
+    const double nnz = rp[i + 1] - rp[i];
+    const double first = b_dense ? (double)bc * e + cc * e : nnz * (4 + e) + cc * e;
+    const double second = nnz * (4 + e + cc * e) + cc * e;
+    P[i + 1] = P[i] + first + second;
+  }
+  bounds[0] = 0;
+  for (int k = 1; k < world; ++k) {
+    const double target = P[n] * k / world;
+    const int row = (int)(std::lower_bound(P.begin(), P.end(), target) - P.begin());
+    auto it = std::lower_bound(ilo.begin(), ilo.end(), row);
+    int c = it == ilo.end() ? ilo.back() : *it;
+    if (it != ilo.begin()) {
+      const int prev = *(it - 1);
+      if (it == ilo.end() || std::fabs(P[prev] - target) < std::fabs(P[c] - target)) c = prev;
+    }
+    bounds[k] = std::max(c, bounds[k - 1]);
+  }
+  bounds[world] = n;
+}
+
+void halo_create(tfg_plan& pl, const tfg_schedule& s, const int* bounds, int world, int rank,
+                 int mode, tfg_halo& h, cudaStream_t st) {
+  const tfg_problem& pr = pl.p;
+  const int n = pr.n, cc = pr.c_cols;
+  if (world < 1 || world > 32 || rank < 0 || rank >= world)
+    throw invalid_argument("halo: world must be in [1, 32] and rank in [0, world)");
+  if (bounds[0] != 0 || bounds[world] != n) throw invalid_argument("halo: bounds must span [0, n]");
+  for (int q = 0; q < world; ++q)
+    if (bounds[q] > bounds[q + 1]) throw invalid_argument("halo: bounds must be ascending");
+  if (bounds[rank] != pl.row_lo || bounds[rank + 1] != pl.row_hi)
+    throw invalid_argument("halo: the plan is not this rank's partition plan");
+  if (mode == TFG_HALO_RECOMPUTE && !pr.b_is_dense)
+    throw invalid_argument("halo: recompute needs a dense B (GeMM-SpMM)");
+  h.world = world;
+  h.rank = rank;
+  const int lo = pl.row_lo, hi = pl.row_hi;
+  // readers of every D1 row, from every rank's wavefront-1 rows
+  dbuf<int> bd(world + 1);
+  h2d(bd.p, bounds, world + 1, st);
+  dbuf<unsigned> mask(n);
+  TFG_CUDA(cudaMemsetAsync(mask.p, 0, (size_t)n * 4, st));
+  const int64_t nj1 = s.n_jrows[1];
+  if (nj1) {
+    k_mark_readers<<<blocks_for(nj1 * 32), 256, 0, st>>>(nj1, s.j_rows[1].p, pr.d_a_row_ptr,
+                                                          pr.d_a_col_idx, bd.p, world, mask.p);
+    TFG_LAUNCH_CHECK();
+  }
+  std::vector<unsigned> m(n);
+  d2h(m.data(), mask.p, n, st);
+  TFG_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> recv, send;
+  h.recv_off.assign(1, 0);
+  h.send_off.assign(1, 0);
+  for (int q = 0; q < world; ++q) {
+    if (q != rank)
+      for (int i = bounds[q]; i < bounds[q + 1]; ++i)
+        if (m[i] >> rank & 1u) recv.push_back(i);
+    h.recv_off.push_back((int64_t)recv.size());
+    if (q != rank)
+      for (int i = lo; i < hi; ++i)
+        if (m[i] >> q & 1u) send.push_back(i);
+    h.send_off.push_back((int64_t)send.size());
+  }
+  h.n_recv = (int64_t)recv.size();
+  h.n_send = (int64_t)send.size();
+  const size_t rb = (size_t)cc * pl.elem;
+  // cost model: NVLink transfer of the halo rows vs recomputing them from
+  // the locally resident B rows (B row read + D1 row write at HBM speed)
+  const double nvlink = 700e9, hbm = 6500e9;
+  h.t_exchange_us = (double)h.n_recv * rb / nvlink * 1e6;
+  h.t_recompute_us = pr.b_is_dense ? (double)h.n_recv * ((double)pr.b_cols * pl.elem + rb) / hbm * 1e6 : 1e300;
+  h.mode = mode == TFG_HALO_AUTO ? (pr.b_is_dense && h.t_recompute_us < h.t_exchange_us
+                                        ? TFG_HALO_RECOMPUTE : TFG_HALO_EXCHANGE)
+                                 : mode;
+  h.recv_rows.alloc(std::max<int64_t>(h.n_recv, 1));
+  h2d(h.recv_rows.p, recv.data(), recv.size(), st);
+  h.send_rows.alloc(std::max<int64_t>(h.n_send, 1));
+  h2d(h.send_rows.p, send.data(), send.size(), st);
+  if (h.mode == TFG_HALO_RECOMPUTE) {
+    std::vector<int> r0, cnt, ihi;
+    for (size_t q = 0; q < recv.size();) {
+      size_t e = q + 1;
+      while (e < recv.size() && recv[e] == recv[e - 1] + 1 && (int)(e - q) < pl.gemm_bm) ++e;
+      r0.push_back(recv[q]);
+      cnt.push_back((int)(e - q));
+      ihi.push_back(recv[q] + (int)(e - q));
+      q = e;
+    }
+    h.n_rblk = (int64_t)r0.size();
+    h.r_r0.alloc(std::max<size_t>(r0.size(), 1));
+    h.r_cnt.alloc(std::max<size_t>(r0.size(), 1));
+    h.r_ihi.alloc(std::max<size_t>(r0.size(), 1));
+    h2d(h.r_r0.p, r0.data(), r0.size(), st);
+    h2d(h.r_cnt.p, cnt.data(), cnt.size(), st);
+    h2d(h.r_ihi.p, ihi.data(), ihi.size(), st);
+  } else {
+    h.recv_buf.alloc(std::max<size_t>((size_t)h.n_recv * rb, 16));
+    h.send_buf.alloc(std::max<size_t>((size_t)h.n_send * rb, 16));
+    TFG_CUDA(cudaStreamCreateWithFlags(&h.comm, cudaStreamNonBlocking));
+    TFG_CUDA(cudaEventCreateWithFlags(&h.ev_packed, cudaEventDisableTiming));
+    TFG_CUDA(cudaEventCreateWithFlags(&h.ev_recv, cudaEventDisableTiming));
+    // wavefront-1 rows that read only local D1 overlap the exchange (row-list
+    // kernels; a grid-stencil slab keeps its one plane-streaming pass)
+    if (!pl.second.stencil && !pl.w1_rows.empty() && h.n_recv > 0) {
+      const int64_t nr = (int64_t)pl.w1_rows.size();
+      dbuf<int> rows(nr);
+      h2d(rows.p, pl.w1_rows.data(), nr, st);
+      dbuf<uint8_t> flag(nr);
+      k_reads_remote<<<blocks_for(nr * 32), 256, 0, st>>>(nr, rows.p, pr.d_a_row_ptr,
+                                                           pr.d_a_col_idx, lo, hi, flag.p);
+      TFG_LAUNCH_CHECK();
+      std::vector<uint8_t> f(nr);
+      d2h(f.data(), flag.p, nr, st);
+      std::vector<int> arp(n + 1);
+      d2h(arp.data(), pr.d_a_row_ptr, n + 1, st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+      std::vector<int> in_rows, bd_rows;
+      for (int64_t q = 0; q < nr; ++q) (f[q] ? bd_rows : in_rows).push_back(pl.w1_rows[q]);
+      h.interior.exact = h.boundary.exact = pl.second.exact;
+      h.interior.build(in_rows, arp, cc, pl.elem, st);
+      h.boundary.build(bd_rows, arp, cc, pl.elem, st);
+      h.split = true;
+    }
+  }
+  TFG_CUDA(cudaStreamSynchronize(st));
+}
+
+template <class T>
+static void execute_dist_t(tfg_plan& pl, tfg_halo& h, void* comm, T* D, cudaStream_t st) {
+  const tfg_problem& pr = pl.p;
+  const int cc = pr.c_cols;
+  T* D1 = reinterpret_cast<T*>(pl.d1.p);
+  const T* av = static_cast<const T*>(pr.d_a_val);
+  plan_execute_t<T>(pl, D, st, nullptr, 0);  // wavefront 0 (no communication)
+  if (h.mode == TFG_HALO_RECOMPUTE) {
+    // the halo's D1 rows from the resident B rows, no transfer
+    first_op_blocks<T>(pl, h.n_rblk, h.r_r0.p, h.r_cnt.p, h.r_ihi.p, D1, st);
+    plan_execute_t<T>(pl, D, st, nullptr, 1);
+    return;
+  }
+  if (h.world > 1 && (h.n_recv || h.n_send)) {
+    if (!comm) throw invalid_argument("plan_execute_dist: exchange needs an NCCL communicator");
+    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    if (h.n_send) {
+      k_gather_rows<T><<<blocks_for(h.n_send * cc), 256, 0, st>>>(
+          D1, cc, h.send_rows.p, h.n_send, reinterpret_cast<T*>(h.send_buf.p));
+      TFG_LAUNCH_CHECK();
+    }
+    TFG_CUDA(cudaEventRecord(h.ev_packed, st));
+    TFG_CUDA(cudaStreamWaitEvent(h.comm, h.ev_packed, 0));
+    const NcclApi& nc = nccl();
+    auto* c = static_cast<ncclComm_t>(comm);
+    nccl_check(nc.GroupStart(), "ncclGroupStart");
+    for (int q = 0; q < h.world; ++q) {
+      const int64_t ns = h.send_off[q + 1] - h.send_off[q], nr = h.recv_off[q + 1] - h.recv_off[q];
+      if (ns)
+        nccl_check(nc.Send(reinterpret_cast<T*>(h.send_buf.p) + h.send_off[q] * cc, (size_t)ns * cc,
+                           dt, q, c, h.comm), "ncclSend");
+      if (nr)
+        nccl_check(nc.Recv(reinterpret_cast<T*>(h.recv_buf.p) + h.recv_off[q] * cc, (size_t)nr * cc,
+                           dt, q, c, h.comm), "ncclRecv");
+    }
+    nccl_check(nc.GroupEnd(), "ncclGroupEnd");
+    TFG_CUDA(cudaEventRecord(h.ev_recv, h.comm));
+  }
+  if (h.split) {
+    spmm_run<T>(h.interior, pr.d_a_row_ptr, pr.d_a_col_idx, av, D1, cc, D, st);  // overlaps NCCL
+    if (h.ev_recv) TFG_CUDA(cudaStreamWaitEvent(st, h.ev_recv, 0));
+  } else if (h.ev_recv) {
+    TFG_CUDA(cudaStreamWaitEvent(st, h.ev_recv, 0));
+  }
+  if (h.n_recv) {
+    k_scatter_rows<T><<<blocks_for(h.n_recv * cc), 256, 0, st>>>(
+        reinterpret_cast<const T*>(h.recv_buf.p), cc, h.recv_rows.p, h.n_recv, D1);
+    TFG_LAUNCH_CHECK();
+  }
+  if (h.split)
+    spmm_run<T>(h.boundary, pr.d_a_row_ptr, pr.d_a_col_idx, av, D1, cc, D, st);
+  else
+    plan_execute_t<T>(pl, D, st, nullptr, 1);
+}
+
+void execute_dist(tfg_plan& pl, tfg_halo& h, void* comm, void* d, cudaStream_t st) {
+  if (pl.p.dtype == TFG_F64)
+    execute_dist_t<double>(pl, h, comm, static_cast<double*>(d), st);
+  else
+    execute_dist_t<float>(pl, h, comm, static_cast<float*>(d), st);
+}
+
 }  // namespace tfg
 
 // ===========================================================================
@@ -2589,6 +2865,57 @@ tfg_status tfg_plan_create_partition(const tfg_problem* p, const tfg_schedule* s
       throw;
     }
     *out = pl;
+  });
+}
+
+tfg_status tfg_partition_bounds(const tfg_schedule* s, const int32_t* h_row_ptr, int32_t b_cols,
+                                int32_t c_cols, int32_t dtype, int32_t b_is_dense, int32_t world,
+                                int32_t* h_bounds) {
+  return guard([&] {
+    if (!s || !h_row_ptr || !h_bounds || world < 1)
+      throw invalid_argument("partition_bounds: bad arguments");
+    partition_bounds(*s, h_row_ptr, b_cols, c_cols, dtype == TFG_F64 ? 8 : 4, b_is_dense != 0,
+                     world, h_bounds);
+  });
+}
+
+tfg_status tfg_halo_create(tfg_plan* pl, const tfg_schedule* s, const int32_t* h_bounds,
+                           int32_t world, int32_t rank, int32_t mode, void* stream,
+                           tfg_halo** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!pl || !s || !h_bounds) throw invalid_argument("halo_create: null argument");
+    if (mode < TFG_HALO_AUTO || mode > TFG_HALO_RECOMPUTE) throw invalid_argument("halo_create: bad mode");
+    auto* h = new tfg_halo;
+    try {
+      halo_create(*pl, *s, h_bounds, world, rank, mode, *h, as_stream(stream));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+tfg_status tfg_halo_info(const tfg_halo* h, int32_t* mode, int64_t* recv_rows, int64_t* send_rows,
+                         double* t_exchange_us, double* t_recompute_us) {
+  return guard([&] {
+    if (!h) throw invalid_argument("halo_info: null halo");
+    if (mode) *mode = h->mode;
+    if (recv_rows) *recv_rows = h->n_recv;
+    if (send_rows) *send_rows = h->n_send;
+    if (t_exchange_us) *t_exchange_us = h->t_exchange_us;
+    if (t_recompute_us) *t_recompute_us = h->t_recompute_us;
+  });
+}
+
+void tfg_halo_destroy(tfg_halo* h) { delete h; }
+
+tfg_status tfg_plan_execute_dist(tfg_plan* pl, tfg_halo* h, void* nccl_comm, void* d, void* stream) {
+  return guard([&] {
+    if (!pl || !h || !d) throw invalid_argument("plan_execute_dist: null argument");
+    if ((uintptr_t)d % 16 != 0) throw invalid_argument("plan_execute: D must be 16-byte aligned");
+    execute_dist(*pl, *h, nccl_comm, d, as_stream(stream));
   });
 }
 

@@ -31,6 +31,9 @@
 // the single product by index_to_scalar_ratio, so the bits match.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <vector>
+
 #include <chrono>
 #include <vector>
 
@@ -122,7 +125,7 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
 }
 
 __global__ void __launch_bounds__(kSplitThreads)
-    k_split(int n, int t, const int* __restrict__ rp,
+    k_split(int n, int t, int base, const int* __restrict__ rp,
             const int* __restrict__ ci, const int* __restrict__ seg_off,
             int* buf, int* tmp, int* demoted, int* n_demoted,
             uint32_t* gbitmap, int bm_words, int smem_bitmap, CostParams cp,
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kSplitThreads)
 
   const int tid = threadIdx.x;
   const int v = blockIdx.x;
-  const int tlo = (int)((long long)v * t);
+  const int tlo = base + (int)((long long)v * t);
   const int thi = (int)min((long long)tlo + t, (long long)n);
   uint32_t* bm = smem_bitmap ? sbm : gbitmap + (size_t)v * bm_words;
 
@@ -239,6 +242,29 @@ __global__ void __launch_bounds__(kSplitThreads)
     __syncthreads();
   }
   if (tid == 0) piece_cnt[v] = s_npieces;
+}
+
+// tile_cost (scheduler.cpp:29-64, :196-200) of one arbitrary tile: distinct
+// columns of its j rows (anywhere in the matrix) by a global bitmap, then
+// the Eq. 3 formula in the reference's operation order.
+__global__ void __launch_bounds__(kSplitThreads)
+    k_tile_cost(int i_lo, int i_hi, const int* __restrict__ rp, const int* __restrict__ ci,
+                const int* __restrict__ jrows, int nj, uint32_t* bm, int bm_words, CostParams cp,
+                double* cost) {
+  __shared__ long long red[kSplitThreads / 32];
+  long long my_nnz = 0;
+  for (int q = threadIdx.x; q < nj; q += blockDim.x) {
+    const int j = jrows[q];
+    for (int k = rp[j]; k < rp[j + 1]; ++k) atomicOr(&bm[ci[k] >> 5], 1u << (ci[k] & 31));
+    my_nnz += rp[j + 1] - rp[j];
+  }
+  __syncthreads();
+  long long my_uc = 0;
+  for (int w = threadIdx.x; w < bm_words; w += blockDim.x) my_uc += __popc(bm[w]);
+  const long long nnzj = block_sum(my_nnz, red);
+  const long long uc = block_sum(my_uc, red);
+  if (threadIdx.x == 0)
+    *cost = eq3_cost(cp, uc, nnzj, nj, i_hi - i_lo, (long long)rp[i_hi] - rp[i_lo]);
 }
 
 // ---- 3. wavefront-0 compaction ----------------------------------------
@@ -513,7 +539,7 @@ void build_schedule_device(int32_t n_rows, int32_t n_cols, int64_t nnz,
   dbuf<double> pc_cost(n);
   TFG_CUDA(cudaMemsetAsync(n_demoted.p, 0, sizeof(int), st));
   k_split<<<nt, kSplitThreads, smem_bm ? bm_bytes : 0, st>>>(
-      n, t, rp, ci, seg_off.p, buf.p, tmp.p, demoted.p, n_demoted.p, gbm.p,
+      n, t, 0, rp, ci, seg_off.p, buf.p, tmp.p, demoted.p, n_demoted.p, gbm.p,
       bm_words, smem_bm ? 1 : 0, cp, pc_lo.p, pc_hi.p, pc_start.p, pc_len.p,
       pc_cost.p, piece_cnt.p);
   TFG_LAUNCH_CHECK();
@@ -629,6 +655,104 @@ void build_schedule_device(int32_t n_rows, int32_t n_cols, int64_t nnz,
   TFG_CUDA(cudaStreamSynchronize(st));
   out.inspect_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+
+// ---- single-step entry points (scheduler.hpp:80-97): the same kernels the
+// pipeline runs, on one tile / one list -------------------------------------
+static CostParams cost_params(const tfg_config& cfg, int n) {
+  CostParams cp;
+  cp.c_cols = (double)cfg.c_cols;
+  cp.b_cols = (double)cfg.b_cols;
+  cp.ratio = cfg.index_to_scalar_ratio;
+  cp.budget = (double)cfg.cache_size_words;
+  cp.n_rows = (double)n;
+  cp.b_is_dense = cfg.b_is_dense != 0;
+  cp.whole_b = cfg.whole_b_cost != 0;
+  return cp;
+}
+
+double tile_cost_device(int n, const int* rp, const int* ci, int i_lo, int i_hi,
+                        const int* jrows, int nj, const tfg_config& cfg, cudaStream_t st) {
+  if (i_lo < 0 || i_hi > n || i_lo > i_hi) throw invalid_argument("tile_cost: i_range out of bounds");
+  const int bm_words = (n + 31) / 32;
+  dbuf<uint32_t> bm(bm_words);
+  TFG_CUDA(cudaMemsetAsync(bm.p, 0, (size_t)bm_words * 4, st));
+  dbuf<double> cost(1);
+  k_tile_cost<<<1, kSplitThreads, 0, st>>>(i_lo, i_hi, rp, ci, jrows, nj, bm.p, bm_words,
+                                          cost_params(cfg, n), cost.p);
+  TFG_LAUNCH_CHECK();
+  double h = 0;
+  TFG_CUDA(cudaMemcpyAsync(&h, cost.p, sizeof h, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+// split_tile through k_split on one coarse tile (base = i_lo, width t =
+// i_hi - i_lo): pieces in DFS pre-order, demoted rows ascending.  j rows must
+// lie inside the tile (the tiles step 1 produces).
+void split_tile_device(int n, const int* rp, const int* ci, int i_lo, int i_hi, const int* jrows,
+                       int nj, const tfg_config& cfg, cudaStream_t st, std::vector<int>& lo,
+                       std::vector<int>& hi, std::vector<double>& cost,
+                       std::vector<int64_t>& joff, std::vector<int>& jout,
+                       std::vector<int>& demoted) {
+  if (i_lo < 0 || i_hi > n || i_lo >= i_hi) throw invalid_argument("split_tile: i_range out of bounds");
+  const int t = i_hi - i_lo;
+  dbuf<int> seg(3), buf(std::max(nj, 1)), tmp(std::max(nj, 1)), dem(std::max(nj, 1)), ndem(1);
+  const int so[3] = {0, nj, nj};
+  TFG_CUDA(cudaMemcpyAsync(seg.p, so, sizeof so, cudaMemcpyHostToDevice, st));
+  if (nj) TFG_CUDA(cudaMemcpyAsync(buf.p, jrows, (size_t)nj * 4, cudaMemcpyDeviceToDevice, st));
+  TFG_CUDA(cudaMemsetAsync(ndem.p, 0, 4, st));
+  const int bm_words = (t + 31) / 32 + 2;
+  dbuf<uint32_t> gbm(bm_words);
+  dbuf<int> pc_lo(n), pc_hi(n), pc_start(n), pc_len(n), pcnt(1);
+  dbuf<double> pc_cost(n);
+  k_split<<<1, kSplitThreads, 0, st>>>(n, t, i_lo, rp, ci, seg.p, buf.p, tmp.p, dem.p, ndem.p,
+                                       gbm.p, bm_words, 0, cost_params(cfg, n), pc_lo.p, pc_hi.p,
+                                       pc_start.p, pc_len.p, pc_cost.p, pcnt.p);
+  TFG_LAUNCH_CHECK();
+  int np = 0, nd = 0;
+  TFG_CUDA(cudaMemcpyAsync(&np, pcnt.p, 4, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaMemcpyAsync(&nd, ndem.p, 4, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> start(np), len(np), rows(std::max(nj, 1));
+  lo.resize(np);
+  hi.resize(np);
+  cost.resize(np);
+  demoted.resize(nd);
+  TFG_CUDA(cudaMemcpyAsync(lo.data(), pc_lo.p + i_lo, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaMemcpyAsync(hi.data(), pc_hi.p + i_lo, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaMemcpyAsync(cost.data(), pc_cost.p + i_lo, (size_t)np * 8, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaMemcpyAsync(start.data(), pc_start.p + i_lo, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaMemcpyAsync(len.data(), pc_len.p + i_lo, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
+  if (nj) TFG_CUDA(cudaMemcpyAsync(rows.data(), buf.p, (size_t)nj * 4, cudaMemcpyDeviceToHost, st));
+  if (nd) TFG_CUDA(cudaMemcpyAsync(demoted.data(), dem.p, (size_t)nd * 4, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaStreamSynchronize(st));
+  std::sort(demoted.begin(), demoted.end());
+  joff.assign(1, 0);
+  jout.clear();
+  for (int q = 0; q < np; ++q) {
+    jout.insert(jout.end(), rows.begin() + start[q], rows.begin() + start[q] + len[q]);
+    joff.push_back((int64_t)jout.size());
+  }
+}
+
+// balance through k_balance: chunk starts over a weight list
+void balance_device(int64_t U, const int64_t* h_w, int64_t num_chunks, int64_t* h_starts,
+                    cudaStream_t st) {
+  if (num_chunks < 1) throw invalid_argument("balance: num_chunks must be >= 1");
+  std::vector<int64_t> P(U + 1, 0);
+  for (int64_t q = 0; q < U; ++q) P[q + 1] = P[q] + h_w[q];
+  dbuf<int64_t> Pd(U + 1), cs(num_chunks + 1), nc(1);
+  TFG_CUDA(cudaMemcpyAsync(Pd.p, P.data(), (size_t)(U + 1) * 8, cudaMemcpyHostToDevice, st));
+  k_balance<<<1, 32, 0, st>>>(U, num_chunks, Pd.p, cs.p, nc.p);
+  TFG_LAUNCH_CHECK();
+  int64_t c = 0;
+  TFG_CUDA(cudaMemcpyAsync(&c, nc.p, 8, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaStreamSynchronize(st));
+  TFG_CUDA(cudaMemcpyAsync(h_starts, cs.p, (size_t)(c + 1) * 8, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaStreamSynchronize(st));
+  for (int64_t k = c + 1; k <= num_chunks; ++k) h_starts[k] = U;  // trailing empty chunks
 }
 
 }  // namespace tfg

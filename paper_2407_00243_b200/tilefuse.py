@@ -133,29 +133,18 @@ class Csr:
         return f"Csr({self.n_rows}x{self.n_cols}, nnz={self.nnz})"
 
 
-def _take_csr(n, rp, ci, v) -> Csr:
-    row_ptr = np.ctypeslib.as_array(rp, shape=(n + 1,)).copy()
-    nnz = int(row_ptr[-1])
-    col = np.ctypeslib.as_array(ci, shape=(nnz + 1,))[:nnz].copy()
-    val = np.ctypeslib.as_array(v, shape=(nnz + 1,))[:nnz].copy()
-    for p in (rp, ci, v):
-        lib().tfg_free(C.cast(p, C.c_void_p))
-    return Csr(n, n, row_ptr, col, val, validate=False)
-
-
 def gen_random_sparse(n: int, density: float, seed: int = 42) -> Csr:
-    """generate.hpp:15-63 (bindings.cpp:111-112)."""
-    rp, ci, v = i32p(), i32p(), f64p()
-    check(lib().tfg_gen_random_sparse(int(n), float(density), int(seed), C.byref(rp), C.byref(ci),
-                                      C.byref(v)))
-    return _take_csr(int(n), rp, ci, v)
+    """generate.hpp:15-63 (bindings.cpp:111-112); host-side, see generate.py."""
+    from .generate import gen_random_sparse as g
+
+    return g(n, density, seed)
 
 
 def gen_banded(n: int, half_bandwidth: int) -> Csr:
-    """generate.hpp:66-94 (bindings.cpp:113-114)."""
-    rp, ci, v = i32p(), i32p(), f64p()
-    check(lib().tfg_gen_banded(int(n), int(half_bandwidth), C.byref(rp), C.byref(ci), C.byref(v)))
-    return _take_csr(int(n), rp, ci, v)
+    """generate.hpp:66-94 (bindings.cpp:113-114); host-side, see generate.py."""
+    from .generate import gen_banded as g
+
+    return g(n, half_bandwidth)
 
 
 def choose_tile_size(n: int, num_workers: int, ct_size: int) -> int:

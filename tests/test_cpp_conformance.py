@@ -31,3 +31,29 @@ def test_conformance_program_passes(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASSED" in r.stdout
+
+
+UNIT = os.path.join(ROOT, "oracle", "_ref", "ref_unit_tests")
+
+
+def test_reference_unit_tests_build():
+    """The reference's tests/test_scheduler.cpp and tests/test_kernels.cpp
+    compile UNCHANGED against include/tilefuse/*.hpp (+ the repo's
+    doctest-compatible shim) and link libtfg (oracle/Makefile `unit`)."""
+    if not os.path.isdir("/root/reference/proj/tests"):
+        pytest.skip("reference sources not in this container (the GPU box uses the prebuilt binary)")
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "unit"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert os.path.exists(UNIT)
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_pass(cuda):
+    """The reference's own scheduler and kernel unit tests pass through the
+    drop-in headers on the B200 (GPU inspector, GPU executors)."""
+    if not os.path.exists(UNIT):
+        pytest.skip("oracle/_ref/ref_unit_tests not built (needs /root/reference at build time)")
+    r = subprocess.run([UNIT], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "Status: SUCCESS!" in r.stdout
