@@ -478,20 +478,22 @@ def run_ours(args, rank, world, dist):
         plan = P.Plan(prob, sched)
         torch.cuda.synchronize()
         plan_s = time.perf_counter() - t0
-    dplan, bounds, halo = None, None, None
+    dplan, bounds, comm = None, None, None
     if world > 1:
-        # row-block partition of the same global problem (strong scaling)
+        # row-block partition of the same global problem (strong scaling),
+        # entirely behind the C-ABI: cost-balanced cuts at tile starts, a
+        # device-built halo that NCCL moves (overlapped with the local-only
+        # wavefront-1 rows) or that is recomputed from B (GeMM-SpMM)
         from paper_2407_00243_b200 import distributed as PD
 
-        flat = sched.export()
-        bounds = PD.tile_boundaries(flat, w.n, world)
-        halo = PD.halo_plan(w.a.row_ptr, w.a.col_idx, flat, bounds, rank)
-        eng = PD.GpuEngine(prob, sched, *bounds[rank])
-        dplan = PD.DistributedPlan(eng, halo, dist, w.c_cols)
-        launches = eng.launches + 3  # + gather, scatter, NCCL all-to-all
+        comm = PD.nccl_comm(dist, world, rank)
+        bounds = PD.partition_bounds(sched, w.a, w.b_cols, w.c_cols, w.dtype, w.op == "gemm-spmm",
+                                     world)
+        dplan = PD.NativeDistributedPlan(prob, sched, bounds, rank, PD.HALO_AUTO, comm=comm)
+        launches = dplan.launches
 
         def step():
-            dplan.execute(out)
+            dplan.execute(out, stream)
     else:
         launches = plan.launches
 
@@ -513,7 +515,8 @@ def run_ours(args, rank, world, dist):
     # execute, D -> pinned host, every step, two buffer sets and three streams
     e2e_pipe = None
     if not args.no_e2e:
-        e2e_pipe = _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan)
+        e2e_pipe = _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan,
+                                  comm)
 
     if rank != 0:
         sampler.stop()
@@ -589,8 +592,9 @@ def run_ours(args, rank, world, dist):
 
     parallelism = "single GPU"
     if world > 1:
-        parallelism = (f"row-block partition x{world} at tile boundaries; D1 halo via one NCCL "
-                       f"all_to_all per step (rank-0 halo rows {dplan.halo_rows})")
+        parallelism = (f"row-block partition x{world} at tile starts (cost-balanced); rank-0 halo "
+                       f"{dplan.halo_rows} D1 rows by {dplan.mode_name} (model: NVLink "
+                       f"{dplan.t_exchange_us:.0f} us vs recompute {dplan.t_recompute_us:.0f} us)")
     config = config_dict(args, w, cfg, sched.num_tiles_per_wave, sched.fused_ratio(), spill_rows)
     config["schedule"].update({"tile_size": sched.tile_size,
                                "inspector_seconds_gpu": sched.inspect_seconds,
@@ -621,7 +625,7 @@ def run_ours(args, rank, world, dist):
                      "peak_source": peak_src,
                      "compute": cr},
         "cpu_baseline": cpu,
-        "e2e": e2e,
+        "e2e": e2e if world == 1 else e2e_pipe,
         "e2e_pipelined": e2e_pipe,
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
@@ -629,22 +633,28 @@ def run_ours(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
-def _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan):
+def _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, plan, dplan,
+                   comm=None):
     import torch
 
     import paper_2407_00243_b200 as P
 
     sets = [prob, prob.clone()]
     host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in prob.device_inputs()]
+    gather_bufs = None
     if world > 1:
         from paper_2407_00243_b200 import distributed as PD
 
         own = torch.as_tensor(PD.owned_output_rows(sched.export(), bounds, rank), device=dev)
-        flat = sched.export()
-        engines = [dplan.engine, PD.GpuEngine(sets[1], sched, *bounds[rank])]
-        dplans = [dplan, PD.DistributedPlan(engines[1], dplan.halo, dist, w.c_cols)]
-        execs = [lambda o, i=i: dplans[i].execute(o) for i in range(2)]
-        del flat
+        dplans = [dplan, PD.NativeDistributedPlan(sets[1], sched, bounds, rank, PD.HALO_AUTO, comm=comm)]
+        execs = [lambda o, i=i: dplans[i].execute(o, torch.cuda.current_stream()) for i in range(2)]
+        # each rank uploads 1/world of every input over its own PCIe link and
+        # NVLink all-gathers the rest (inputs stay replicated on the devices)
+        gather_bufs = []
+        for t in prob.device_inputs():
+            flat = t.reshape(-1)
+            chunk = (flat.numel() + world - 1) // world
+            gather_bufs.append(torch.empty(chunk * world, dtype=t.dtype, device=dev))
     else:
         own = None
         plans = [plan, P.Plan(sets[1], sched)]
@@ -653,6 +663,8 @@ def _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, pl
     nout = w.n if own is None else int(own.numel())
     host_out = [torch.empty((nout, w.c_cols), dtype=out.dtype, pin_memory=True) for _ in range(2)]
     h2d = int(sum(h.numel() * h.element_size() for h in host_in))
+    if world > 1:
+        h2d = int(sum(((h.numel() + world - 1) // world) * h.element_size() for h in host_in))
     d2h = int(host_out[0].numel() * host_out[0].element_size())
     s_h, s_c, s_d = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     ev_h = [torch.cuda.Event() for _ in range(2)]
@@ -665,8 +677,19 @@ def _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, pl
             with torch.cuda.stream(s_h):
                 if k >= 2:
                     s_h.wait_event(ev_c[b])  # inputs of step k-2 consumed
-                for hsrc, ddst in zip(host_in, sets[b].device_inputs()):
-                    ddst.copy_(hsrc, non_blocking=True)
+                if gather_bufs is None:
+                    for hsrc, ddst in zip(host_in, sets[b].device_inputs()):
+                        ddst.copy_(hsrc, non_blocking=True)
+                else:
+                    for hsrc, ddst, gb in zip(host_in, sets[b].device_inputs(), gather_bufs):
+                        hf, df = hsrc.reshape(-1), ddst.reshape(-1)
+                        chunk = gb.numel() // world
+                        lo, hi = rank * chunk, min((rank + 1) * chunk, hf.numel())
+                        mine = gb[lo:lo + chunk]
+                        if hi > lo:
+                            mine[:hi - lo].copy_(hf[lo:hi], non_blocking=True)
+                        dist.all_gather_into_tensor(gb, mine)
+                        df.copy_(gb[:df.numel()], non_blocking=True)
                 ev_h[b].record(s_h)
             with torch.cuda.stream(s_c):
                 s_c.wait_event(ev_h[b])
@@ -699,7 +722,9 @@ def _e2e_pipelined(args, w, prob, sched, bounds, rank, world, dist, dev, out, pl
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / args.steps,
             "path": ("pinned host A, B (aliased when B is A), C -> HBM, plan execute, D -> pinned host, "
                      "every step; steps pipelined over two buffer sets and H2D/compute/D2H streams; "
-                     "max over ranks")}
+                     + ("N > 1: each rank uploads 1/N of every input, NCCL all-gathers the rest over "
+                        "NVLink, D2H of its own D rows; " if world > 1 else "")
+                     + "max over ranks")}
 
 
 def main():

@@ -336,6 +336,12 @@ void tfg_halo_destroy(tfg_halo *h);
 tfg_status tfg_plan_execute_dist(tfg_plan *plan, tfg_halo *halo, void *nccl_comm, void *d_d,
                                  void *stream);
 
+/* Test / debug: the step of ALL `world` ranks on one GPU, sequentially, the
+ * NCCL transfer replaced by device copies between the ranks' halo buffers
+ * (plans[r], halos[r], d[r] of rank r). */
+tfg_status tfg_plan_execute_dist_emulated(tfg_plan **plans, tfg_halo **halos, int32_t world,
+                                          void **d, void *stream);
+
 /* Halo pack / unpack of D1 rows around a caller-driven exchange.  rows:
  * device int32 list. */
 tfg_status tfg_gather_rows(int32_t dtype, const void *d_src, int32_t cols,

@@ -89,6 +89,19 @@ SIGNATURES = [
                                  C.POINTER(TfgConfig), i64p, i32p, i32p, C.POINTER(C.c_double),
                                  i64p, i32p, i64p, i32p]),
     ("tfg_balance", C.c_int, [C.c_int64, i64p, C.c_int64, i64p]),
+    ("tfg_nccl_unique_id", C.c_int, [C.c_void_p, C.c_size_t]),
+    ("tfg_nccl_comm_init", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("tfg_nccl_comm_destroy", C.c_int, [C.c_void_p]),
+    ("tfg_partition_bounds", C.c_int, [C.c_void_p, i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_int32, i32p]),
+    ("tfg_halo_create", C.c_int, [C.c_void_p, C.c_void_p, i32p, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("tfg_halo_info", C.c_int, [C.c_void_p, i32p, i64p, i64p, C.POINTER(C.c_double),
+                                C.POINTER(C.c_double)]),
+    ("tfg_halo_destroy", None, [C.c_void_p]),
+    ("tfg_plan_execute_dist", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tfg_plan_execute_dist_emulated", C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                                 C.c_int32, C.POINTER(C.c_void_p), C.c_void_p]),
     ("tfg_plan_create", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
     ("tfg_plan_create_ex", C.c_int, [C.POINTER(TfgProblem), C.c_void_p, C.c_uint32, C.c_int32,

@@ -2747,27 +2747,58 @@ void halo_create(tfg_plan& pl, const tfg_schedule& s, const int* bounds, int wor
   TFG_CUDA(cudaStreamSynchronize(st));
 }
 
+// The step in phases (execute_dist runs them in order with NCCL between
+// 0 and 2; the single-GPU emulation moves the buffers itself).
+// phase 0: wavefront 0, then pack the rows peers need (or recompute the halo)
 template <class T>
-static void execute_dist_t(tfg_plan& pl, tfg_halo& h, void* comm, T* D, cudaStream_t st) {
+static void dist_phase0(tfg_plan& pl, tfg_halo& h, T* D, cudaStream_t st) {
+  const int cc = pl.p.c_cols;
+  T* D1 = reinterpret_cast<T*>(pl.d1.p);
+  plan_execute_t<T>(pl, D, st, nullptr, 0);  // no communication
+  if (h.mode == TFG_HALO_RECOMPUTE) {  // the halo's D1 rows from the resident B rows
+    first_op_blocks<T>(pl, h.n_rblk, h.r_r0.p, h.r_cnt.p, h.r_ihi.p, D1, st);
+    return;
+  }
+  if (h.n_send) {
+    k_gather_rows<T><<<blocks_for(h.n_send * cc), 256, 0, st>>>(
+        D1, cc, h.send_rows.p, h.n_send, reinterpret_cast<T*>(h.send_buf.p));
+    TFG_LAUNCH_CHECK();
+  }
+}
+// phase 2: the wavefront-1 rows that read only local D1 (while the halo moves)
+template <class T>
+static void dist_phase2(tfg_plan& pl, tfg_halo& h, T* D, cudaStream_t st) {
+  const tfg_problem& pr = pl.p;
+  if (h.mode == TFG_HALO_EXCHANGE && h.split)
+    spmm_run<T>(h.interior, pr.d_a_row_ptr, pr.d_a_col_idx, static_cast<const T*>(pr.d_a_val),
+                reinterpret_cast<const T*>(pl.d1.p), pr.c_cols, D, st);
+}
+// phase 3: unpack the received rows, then the rest of wavefront 1
+template <class T>
+static void dist_phase3(tfg_plan& pl, tfg_halo& h, T* D, cudaStream_t st) {
   const tfg_problem& pr = pl.p;
   const int cc = pr.c_cols;
   T* D1 = reinterpret_cast<T*>(pl.d1.p);
-  const T* av = static_cast<const T*>(pr.d_a_val);
-  plan_execute_t<T>(pl, D, st, nullptr, 0);  // wavefront 0 (no communication)
-  if (h.mode == TFG_HALO_RECOMPUTE) {
-    // the halo's D1 rows from the resident B rows, no transfer
-    first_op_blocks<T>(pl, h.n_rblk, h.r_r0.p, h.r_cnt.p, h.r_ihi.p, D1, st);
-    plan_execute_t<T>(pl, D, st, nullptr, 1);
-    return;
+  if (h.mode == TFG_HALO_EXCHANGE && h.n_recv) {
+    k_scatter_rows<T><<<blocks_for(h.n_recv * cc), 256, 0, st>>>(
+        reinterpret_cast<const T*>(h.recv_buf.p), cc, h.recv_rows.p, h.n_recv, D1);
+    TFG_LAUNCH_CHECK();
   }
-  if (h.world > 1 && (h.n_recv || h.n_send)) {
+  if (h.mode == TFG_HALO_EXCHANGE && h.split)
+    spmm_run<T>(h.boundary, pr.d_a_row_ptr, pr.d_a_col_idx, static_cast<const T*>(pr.d_a_val),
+                D1, cc, D, st);
+  else
+    plan_execute_t<T>(pl, D, st, nullptr, 1);
+}
+
+template <class T>
+static void execute_dist_t(tfg_plan& pl, tfg_halo& h, void* comm, T* D, cudaStream_t st) {
+  const int cc = pl.p.c_cols;
+  dist_phase0<T>(pl, h, D, st);
+  const bool xfer = h.mode == TFG_HALO_EXCHANGE && h.world > 1 && (h.n_recv || h.n_send);
+  if (xfer) {
     if (!comm) throw invalid_argument("plan_execute_dist: exchange needs an NCCL communicator");
     const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-    if (h.n_send) {
-      k_gather_rows<T><<<blocks_for(h.n_send * cc), 256, 0, st>>>(
-          D1, cc, h.send_rows.p, h.n_send, reinterpret_cast<T*>(h.send_buf.p));
-      TFG_LAUNCH_CHECK();
-    }
     TFG_CUDA(cudaEventRecord(h.ev_packed, st));
     TFG_CUDA(cudaStreamWaitEvent(h.comm, h.ev_packed, 0));
     const NcclApi& nc = nccl();
@@ -2785,21 +2816,37 @@ static void execute_dist_t(tfg_plan& pl, tfg_halo& h, void* comm, T* D, cudaStre
     nccl_check(nc.GroupEnd(), "ncclGroupEnd");
     TFG_CUDA(cudaEventRecord(h.ev_recv, h.comm));
   }
-  if (h.split) {
-    spmm_run<T>(h.interior, pr.d_a_row_ptr, pr.d_a_col_idx, av, D1, cc, D, st);  // overlaps NCCL
-    if (h.ev_recv) TFG_CUDA(cudaStreamWaitEvent(st, h.ev_recv, 0));
-  } else if (h.ev_recv) {
-    TFG_CUDA(cudaStreamWaitEvent(st, h.ev_recv, 0));
+  dist_phase2<T>(pl, h, D, st);  // overlaps the NCCL transfer
+  if (xfer) TFG_CUDA(cudaStreamWaitEvent(st, h.ev_recv, 0));
+  dist_phase3<T>(pl, h, D, st);
+}
+
+// All ranks of a partitioned step on ONE GPU, one after another, the NCCL
+// transfer replaced by device copies between the ranks' halo buffers (every
+// rank's memory is local): checks cuts, halo lists and the split without a
+// second GPU.  No kernel waits on another.
+template <class T>
+static void execute_dist_emulated_t(tfg_plan** pls, tfg_halo** hs, int world, void** ds,
+                                    cudaStream_t st) {
+  for (int r = 0; r < world; ++r) dist_phase0<T>(*pls[r], *hs[r], static_cast<T*>(ds[r]), st);
+  for (int r = 0; r < world; ++r) {
+    tfg_halo& h = *hs[r];
+    if (h.mode != TFG_HALO_EXCHANGE) continue;
+    const size_t rb = (size_t)pls[r]->p.c_cols * sizeof(T);
+    for (int q = 0; q < world; ++q) {  // rows r receives from q = rows q sends to r
+      const tfg_halo& g = *hs[q];
+      const int64_t nr = h.recv_off[q + 1] - h.recv_off[q];
+      if (nr != g.send_off[r + 1] - g.send_off[r])
+        throw runtime_error("halo emulation: send / recv lists of a rank pair disagree");
+      if (nr)
+        TFG_CUDA(cudaMemcpyAsync(h.recv_buf.p + h.recv_off[q] * rb, g.send_buf.p + g.send_off[r] * rb,
+                                 (size_t)nr * rb, cudaMemcpyDeviceToDevice, st));
+    }
   }
-  if (h.n_recv) {
-    k_scatter_rows<T><<<blocks_for(h.n_recv * cc), 256, 0, st>>>(
-        reinterpret_cast<const T*>(h.recv_buf.p), cc, h.recv_rows.p, h.n_recv, D1);
-    TFG_LAUNCH_CHECK();
+  for (int r = 0; r < world; ++r) {
+    dist_phase2<T>(*pls[r], *hs[r], static_cast<T*>(ds[r]), st);
+    dist_phase3<T>(*pls[r], *hs[r], static_cast<T*>(ds[r]), st);
   }
-  if (h.split)
-    spmm_run<T>(h.boundary, pr.d_a_row_ptr, pr.d_a_col_idx, av, D1, cc, D, st);
-  else
-    plan_execute_t<T>(pl, D, st, nullptr, 1);
 }
 
 void execute_dist(tfg_plan& pl, tfg_halo& h, void* comm, void* d, cudaStream_t st) {
@@ -2807,6 +2854,13 @@ void execute_dist(tfg_plan& pl, tfg_halo& h, void* comm, void* d, cudaStream_t s
     execute_dist_t<double>(pl, h, comm, static_cast<double*>(d), st);
   else
     execute_dist_t<float>(pl, h, comm, static_cast<float*>(d), st);
+}
+
+void execute_dist_emulated(tfg_plan** pls, tfg_halo** hs, int world, void** ds, cudaStream_t st) {
+  if (pls[0]->p.dtype == TFG_F64)
+    execute_dist_emulated_t<double>(pls, hs, world, ds, st);
+  else
+    execute_dist_emulated_t<float>(pls, hs, world, ds, st);
 }
 
 }  // namespace tfg
@@ -2910,6 +2964,19 @@ tfg_status tfg_halo_info(const tfg_halo* h, int32_t* mode, int64_t* recv_rows, i
 }
 
 void tfg_halo_destroy(tfg_halo* h) { delete h; }
+
+tfg_status tfg_plan_execute_dist_emulated(tfg_plan** plans, tfg_halo** halos, int32_t world,
+                                          void** d, void* stream) {
+  return guard([&] {
+    if (!plans || !halos || !d || world < 1) throw invalid_argument("execute_dist_emulated: bad arguments");
+    for (int r = 0; r < world; ++r) {
+      if (!plans[r] || !halos[r] || !d[r]) throw invalid_argument("execute_dist_emulated: null entry");
+      if (halos[r]->world != world || halos[r]->rank != r)
+        throw invalid_argument("execute_dist_emulated: halos must be ranks 0..world-1 of one partition");
+    }
+    execute_dist_emulated(plans, halos, world, d, as_stream(stream));
+  });
+}
 
 tfg_status tfg_plan_execute_dist(tfg_plan* pl, tfg_halo* h, void* nccl_comm, void* d, void* stream) {
   return guard([&] {

@@ -11,10 +11,20 @@ NCCL all-to-all (NVLink/NVSwitch), scattered into r's D1 by global row index.
 
 Inputs (A, B, C) are resident on every rank (each B200 holds 180 GB), so the
 halo lists are computed deterministically on every rank from the replicated
-pattern and schedule -- no list exchange is needed.  The compute calls go
-through an engine: `GpuEngine` (libtfg partition plans) in the product;
-the CPU test suite substitutes a NumPy engine to exercise the partition and
-exchange logic over gloo without a GPU.
+pattern and schedule -- no list exchange is needed.
+
+Two drivers share the partition:
+* `NativeDistributedPlan` -- the product path, entirely behind the C-ABI
+  (include/tfg.h multi-GPU section): cost-balanced cuts
+  (tfg_partition_bounds), a device-built halo (tfg_halo_create) that either
+  moves the D1 halo with grouped NCCL send/recv while the local-only
+  wavefront-1 rows run, or -- GeMM-SpMM, when the cost model says so --
+  recomputes the halo rows from the resident B rows; one call per step
+  (tfg_plan_execute_dist).  torch.distributed only exchanges the NCCL
+  unique id at setup.
+* `DistributedPlan` -- the same exchange orchestrated from Python over
+  torch.distributed (all_to_all_single); with the NumPy engine of the CPU
+  test suite it checks the partition and exchange logic over gloo.
 """
 from __future__ import annotations
 
@@ -226,3 +236,134 @@ def owned_output_rows(flat_sched, bounds, rank) -> np.ndarray:
     w1 = wave1_rows(flat_sched)
     rows.append(w1[(w1 >= lo) & (w1 < hi)])
     return np.sort(np.concatenate(rows).astype(np.int64)) if rows else np.zeros(0, np.int64)
+
+
+# ---------------------------------------------------------------------------
+# Native path (C-ABI)
+# ---------------------------------------------------------------------------
+HALO_AUTO, HALO_EXCHANGE, HALO_RECOMPUTE = 0, 1, 2
+
+
+def partition_bounds(sched, a, b_cols: int, c_cols: int, dtype, b_is_dense: bool, world: int):
+    """tfg_partition_bounds: cuts at wavefront-0 tile starts, balanced by
+    estimated bytes per row; returns [(lo, hi)] per rank."""
+    import ctypes as C
+
+    from ._lib import check, lib
+
+    rp = np.ascontiguousarray(a.row_ptr, np.int32)
+    out = np.zeros(world + 1, np.int32)
+    code = 1 if np.dtype(dtype) == np.float64 else 0
+    check(lib().tfg_partition_bounds(sched.handle, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     int(b_cols), int(c_cols), code, int(b_is_dense), int(world),
+                                     out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return [(int(out[k]), int(out[k + 1])) for k in range(world)]
+
+
+def nccl_comm(dist, world: int, rank: int):
+    """An NCCL communicator (ncclComm_t as int) from the NCCL the library binds;
+    the unique id travels over the torch.distributed group."""
+    import ctypes as C
+
+    from ._lib import check, lib
+
+    uid = (C.c_char * 128)()
+    if rank == 0:
+        check(lib().tfg_nccl_unique_id(uid, 128))
+    box = [bytes(uid)]
+    if dist is not None and world > 1:
+        dist.broadcast_object_list(box, src=0)
+    uid = (C.c_char * 128).from_buffer_copy(box[0])
+    comm = C.c_void_p()
+    check(lib().tfg_nccl_comm_init(int(world), uid, int(rank), C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm):
+    from ._lib import check, lib
+
+    import ctypes as C
+
+    check(lib().tfg_nccl_comm_destroy(C.c_void_p(comm)))
+
+
+class NativeDistributedPlan:
+    """One rank of the partitioned product behind the C-ABI."""
+
+    def __init__(self, problem, sched, bounds, rank: int, mode: int = HALO_AUTO, comm=None,
+                 stream=None, reference_bits: bool = False):
+        import ctypes as C
+
+        from ._lib import PLAN_REFERENCE_BITS, check, lib
+        from .tilefuse import _stream_ptr
+
+        self.problem, self.bounds, self.rank, self.comm = problem, bounds, rank, comm
+        self.world = len(bounds)
+        self._p = problem.c_struct()
+        lo, hi = bounds[rank]
+        h = C.c_void_p()
+        check(lib().tfg_plan_create_ex(C.byref(self._p), sched.handle,
+                                       PLAN_REFERENCE_BITS if reference_bits else 0, int(lo),
+                                       int(hi), _stream_ptr(stream), C.byref(h)))
+        self._plan = h
+        b = np.array([lo_ for lo_, _ in bounds] + [bounds[-1][1]], np.int32)
+        hh = C.c_void_p()
+        check(lib().tfg_halo_create(h, sched.handle, b.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    self.world, int(rank), int(mode), _stream_ptr(stream),
+                                    C.byref(hh)))
+        self._halo = hh
+        md, nr, ns = C.c_int32(), C.c_int64(), C.c_int64()
+        tx, tr = C.c_double(), C.c_double()
+        check(lib().tfg_halo_info(hh, C.byref(md), C.byref(nr), C.byref(ns), C.byref(tx), C.byref(tr)))
+        self.mode, self.halo_rows, self.send_rows = md.value, nr.value, ns.value
+        self.t_exchange_us, self.t_recompute_us = tx.value, tr.value
+        la = C.c_int32()
+        check(lib().tfg_plan_info(h, None, None, C.byref(la), None))
+        self.launches = la.value + (2 if self.mode == HALO_EXCHANGE else 1)
+        self._lib, self._check, self._sp = lib, check, _stream_ptr
+
+    @property
+    def mode_name(self):
+        return {HALO_EXCHANGE: "exchange", HALO_RECOMPUTE: "recompute"}.get(self.mode, "?")
+
+    def execute(self, out, stream=None):
+        import ctypes as C
+
+        import torch
+
+        st = self._sp(stream if stream is not None else torch.cuda.current_stream())
+        self._check(self._lib().tfg_plan_execute_dist(self._plan, self._halo,
+                                                      C.c_void_p(self.comm) if self.comm else None,
+                                                      C.c_void_p(out.data_ptr()), st))
+        return out
+
+    def close(self):
+        if getattr(self, "_halo", None):
+            self._lib().tfg_halo_destroy(self._halo)
+            self._halo = None
+        if getattr(self, "_plan", None):
+            self._lib().tfg_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def execute_emulated(dplans, outs, stream=None):
+    """All ranks' steps on one GPU (tfg_plan_execute_dist_emulated)."""
+    import ctypes as C
+
+    import torch
+
+    from ._lib import check, lib
+    from .tilefuse import _stream_ptr
+
+    w = len(dplans)
+    plans = (C.c_void_p * w)(*[d._plan.value for d in dplans])
+    halos = (C.c_void_p * w)(*[d._halo.value for d in dplans])
+    ds = (C.c_void_p * w)(*[o.data_ptr() for o in outs])
+    check(lib().tfg_plan_execute_dist_emulated(plans, halos, w, ds,
+                                               _stream_ptr(stream or torch.cuda.current_stream())))
