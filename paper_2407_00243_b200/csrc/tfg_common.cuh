@@ -64,8 +64,48 @@ tfg_status guard(F&& f) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-// Owning device allocation (cudaMalloc; plans and schedules are built once
-// and executed many times, so allocation is never on the execute path).
+// Stream-ordered allocation scope.  cudaFree synchronises the whole device,
+// so temporaries freed while building a plan would wait for unrelated work
+// (the by-value call uploads B on another stream meanwhile).  Inside a scope,
+// dbuf allocates and frees with cudaMallocAsync / cudaFreeAsync on the
+// scope's stream from the device's default pool (kept cached: release
+// threshold raised once), so buffers are ordered with the work that uses them.
+struct AllocScope {
+  static cudaStream_t& stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+  }
+  static bool& active() {
+    static thread_local bool on = false;
+    return on;
+  }
+  cudaStream_t prev_s;
+  bool prev_on;
+  explicit AllocScope(cudaStream_t st) : prev_s(stream()), prev_on(active()) {
+    static thread_local bool pool_set = false;
+    if (!pool_set) {
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pool_set = true;
+    }
+    stream() = st;
+    active() = true;
+  }
+  ~AllocScope() {
+    stream() = prev_s;
+    active() = prev_on;
+  }
+  AllocScope(const AllocScope&) = delete;
+  AllocScope& operator=(const AllocScope&) = delete;
+};
+
+// Owning device allocation (cudaMalloc, or stream-ordered inside an
+// AllocScope; plans and schedules are built once and executed many times, so
+// allocation is never on the execute path).
 template <class T>
 struct dbuf {
   T* p = nullptr;
@@ -83,10 +123,19 @@ struct dbuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) TFG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (!count) return;
+    if (AllocScope::active())
+      TFG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), AllocScope::stream()));
+    else
+      TFG_CUDA(cudaMalloc(&p, count * sizeof(T)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (AllocScope::active())
+        cudaFreeAsync(p, AllocScope::stream());
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }

@@ -32,6 +32,7 @@
 #include <memory>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tfg_common.cuh"
@@ -1823,6 +1824,12 @@ static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
 // ===========================================================================
 // The plan behind tfg_plan.
 // ===========================================================================
+namespace tfg {
+struct PlanProfileCtx {
+  std::vector<int> fo_rows, second_rows, arp, brp;
+};
+}  // namespace tfg
+
 struct tfg_plan {
   tfg_problem p{};
   size_t elem = 8;
@@ -1866,6 +1873,8 @@ struct tfg_plan {
   // byte written once (the roofline numerator)
   int64_t stage_bytes[3] = {0, 0, 0};
   int64_t d1_read_rows = 0;  // distinct D1 rows wavefront 1 reads
+  bool stage_bytes_done = false;
+  std::unique_ptr<tfg::PlanProfileCtx> prof;  // host lists kept for compute_stage_bytes
 };
 
 // Multi-GPU halo of one rank's partition plan (tfg_halo_create).
@@ -1915,10 +1924,25 @@ static size_t fused_gemm_smem(const tfg_plan& pl) {
                            : GemmCfg<double, 64, 64, 16, 4, 4, 3>::SMEM;
 }
 
-static StencilGeom probe_stencil(int64_t n, const std::vector<int>& rp,
-                                 const std::vector<int>& ci) {
+// The band layout pays only for identity row lists of similar-length rows
+// (the skew test of SpmmWork::build): skip copying column indices otherwise.
+static bool band_candidate(const std::vector<int>& rows, const std::vector<int>& rp) {
+  if (rows.empty()) return false;
+  for (size_t q = 1; q < rows.size(); ++q)
+    if (rows[q] != rows[q - 1] + 1) return false;
+  int64_t tot = 0;
+  int mx = 0;
+  for (int r : rows) {
+    tot += rp[r + 1] - rp[r];
+    mx = std::max(mx, rp[r + 1] - rp[r]);
+  }
+  return mx <= 8.0 * std::max((double)tot / (double)rows.size(), 1.0);
+}
+
+static StencilGeom probe_stencil(int64_t n, const std::vector<int>& rp, const int* rp_d,
+                                 const int* ci_d, cudaStream_t st) {
   StencilGeom g;
-  if (stencil_env_enabled() && !ci.empty() && n <= INT32_MAX) stencil_detect((int)n, rp, ci, g);
+  if (stencil_env_enabled() && n <= INT32_MAX) stencil_detect((int)n, rp, rp_d, ci_d, g, st);
   return g;
 }
 
@@ -1952,8 +1976,88 @@ static void attach_stencil(SpmmWork& w, const StencilGeom& g, const void* X, int
   w.stencil = std::move(sp);
 }
 
+// Algorithmic (compulsory) HBM bytes of each stage, the roofline numerator
+// (DESIGN.md section 4): each input byte read once, each output written once.
+static void compute_stage_bytes(tfg_plan& pl, cudaStream_t st) {
+  if (pl.stage_bytes_done || !pl.prof) return;
+  const tfg_problem& pr = pl.p;
+  const int n = pr.n, cc = pr.c_cols, bc = pr.b_cols;
+  const std::vector<int>& fo_rows = pl.prof->fo_rows;
+  const std::vector<int>& second_rows = pl.prof->second_rows;
+  const std::vector<int>& arp = pl.prof->arp;
+  const std::vector<int>& brp = pl.prof->brp;
+
+    const int64_t el = (int64_t)pl.elem;
+    auto csr_rows_bytes = [&](const std::vector<int>& rows, const std::vector<int>& rp) {
+      int64_t b = 0;
+      for (int r : rows) b += 4 + (int64_t)(rp[r + 1] - rp[r]) * (4 + el);
+      return b;
+    };
+    // distinct X rows referenced by `rows` of the CSR (rp_d, ci_d)
+    auto distinct_cols = [&](const std::vector<int>& rows, const int* rp_d, const int* ci_d,
+                             int ncols) -> int64_t {
+      if (rows.empty()) return 0;
+      dbuf<int> rows_d(rows.size());
+      h2d(rows_d.p, rows.data(), rows.size(), st);
+      dbuf<uint8_t> mark(ncols);
+      TFG_CUDA(cudaMemsetAsync(mark.p, 0, ncols, st));
+      k_mark_cols<<<blocks_for((int64_t)rows.size() * 32), 256, 0, st>>>(
+          (int64_t)rows.size(), rows_d.p, rp_d, ci_d, mark.p);
+      TFG_LAUNCH_CHECK();
+      dbuf<unsigned long long> cnt(1);
+      TFG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+      k_count_u8<<<256, 256, 0, st>>>(ncols, mark.p, cnt.p);
+      TFG_LAUNCH_CHECK();
+      unsigned long long h = 0;
+      d2h(&h, cnt.p, 1, st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+      return (int64_t)h;
+    };
+    const int64_t ra = (int64_t)fo_rows.size();
+    if (ra) {
+      if (pr.b_is_dense)
+        pl.stage_bytes[0] = ra * bc * el + (int64_t)bc * cc * el + ra * cc * el;
+      else
+        pl.stage_bytes[0] = csr_rows_bytes(fo_rows, brp) +
+                            distinct_cols(fo_rows, pr.d_b_row_ptr, pr.d_b_col_idx, bc) * cc * el +
+                            ra * cc * el;
+    }
+    if (pl.n_ftiles) {
+      std::vector<int> ti, tj;  // first-op rows and fused j rows of fused tiles
+      std::vector<int> ilo(pl.n_ftiles), ihi(pl.n_ftiles);
+      d2h(ilo.data(), pl.ft_ilo.p, pl.n_ftiles, st);
+      d2h(ihi.data(), pl.ft_ihi.p, pl.n_ftiles, st);
+      tj.resize(pl.ft_nrows);
+      d2h(tj.data(), pl.ft_jrows.p, pl.ft_nrows, st);
+      std::vector<uint8_t> sp(n);
+      d2h(sp.data(), pl.spill.p, n, st);
+      TFG_CUDA(cudaStreamSynchronize(st));
+      int64_t spilled = 0;
+      for (int64_t v = 0; v < pl.n_ftiles; ++v)
+        for (int i = ilo[v]; i < ihi[v]; ++i) {
+          ti.push_back(i);
+          spilled += sp[i];
+        }
+      const int64_t w = (int64_t)ti.size();
+      int64_t b = 0;
+      if (pr.b_is_dense)
+        b = w * bc * el + (int64_t)bc * cc * el;
+      else
+        b = csr_rows_bytes(ti, brp) + distinct_cols(ti, pr.d_b_row_ptr, pr.d_b_col_idx, bc) * cc * el;
+      b += csr_rows_bytes(tj, arp) + (int64_t)tj.size() * cc * el + spilled * cc * el;
+      pl.stage_bytes[1] = b;
+    }
+    if (!second_rows.empty())
+      pl.d1_read_rows = distinct_cols(second_rows, pr.d_a_row_ptr, pr.d_a_col_idx, n);
+      pl.stage_bytes[2] = csr_rows_bytes(second_rows, arp) + pl.d1_read_rows * cc * el +
+                          (int64_t)second_rows.size() * cc * el;
+    pl.stage_bytes_done = true;
+  pl.prof.reset();
+}
+
 void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                  tfg_plan& pl, int row_lo = 0, int row_hi = -1, uint32_t flags = 0) {
+  AllocScope scope(st);  // temporaries stream-ordered: no device-wide sync on free
   // problem.check() -- kernels.hpp:35-42; require_workers is the caller's.
   if (pr.dtype != TFG_F32 && pr.dtype != TFG_F64)
     throw invalid_argument("problem: unknown dtype");
@@ -2289,13 +2393,14 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       h2d(pl.fo_ihi.p, ihi.data(), ihi.size(), st);
     }
   } else {
+    if (pr.b_cols == n && pr.b_nnz > 0) gB = probe_stencil(n, brp, pr.d_b_row_ptr, pr.d_b_col_idx, st);
+    // host column indices only for the band layout (not a grid stencil)
     std::vector<int> bci;
-    if (pr.b_nnz > 0 && pr.b_nnz <= kGroupMaxNnz) {
+    if (gB.nx == 0 && pr.b_nnz > 0 && pr.b_nnz <= kGroupMaxNnz) {
       bci.resize(pr.b_nnz);
       d2h(bci.data(), pr.d_b_col_idx, bci.size(), st);
       TFG_CUDA(cudaStreamSynchronize(st));
     }
-    if (pr.b_cols == n) gB = probe_stencil(n, brp, bci);
     pl.fo_sparse.build(fo_rows, brp, cc, pl.elem, st, bci.empty() ? nullptr : &bci,
                        stencil_rows(fo_rows, gB, cc, pl.elem));
     attach_stencil(pl.fo_sparse, gB, pr.d_c, cc, pl.elem);
@@ -2310,16 +2415,20 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       if (in[r]) second_rows.push_back(r);
   }
   {
+    // A aliased with B (SpMM-SpMM with B = A): same pattern, same geometry
+    const bool same = !pr.b_is_dense && pr.d_a_row_ptr == pr.d_b_row_ptr &&
+                      pr.d_a_col_idx == pr.d_b_col_idx && pr.b_cols == n;
+    const StencilGeom gA =
+        same ? gB : (arp[n] > 0 ? probe_stencil(n, arp, pr.d_a_row_ptr, pr.d_a_col_idx, st)
+                                : StencilGeom{});
+    // host column indices only for the band layout: not a stencil, and a
+    // list that is not skewed (R-MAT rows never band-stage)
     std::vector<int> aci;
-    if (arp[n] > 0 && arp[n] <= kGroupMaxNnz) {
+    if (gA.nx == 0 && arp[n] > 0 && arp[n] <= kGroupMaxNnz && band_candidate(second_rows, arp)) {
       aci.resize(arp[n]);
       d2h(aci.data(), pr.d_a_col_idx, aci.size(), st);
       TFG_CUDA(cudaStreamSynchronize(st));
     }
-    // A aliased with B (SpMM-SpMM with B = A): same pattern, same geometry
-    const bool same = !pr.b_is_dense && pr.d_a_row_ptr == pr.d_b_row_ptr &&
-                      pr.d_a_col_idx == pr.d_b_col_idx && pr.b_cols == n;
-    const StencilGeom gA = same ? gB : probe_stencil(n, arp, aci);
     pl.second.build(second_rows, arp, cc, pl.elem, st, aci.empty() ? nullptr : &aci,
                     stencil_rows(second_rows, gA, cc, pl.elem));
     if (partial) pl.w1_rows = second_rows;
@@ -2327,75 +2436,10 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
   }
   phase("first-op + wave-1 work");
 
-  // ---- algorithmic bytes per stage ------------------------------------
-  {
-    const int64_t el = (int64_t)pl.elem;
-    auto csr_rows_bytes = [&](const std::vector<int>& rows, const std::vector<int>& rp) {
-      int64_t b = 0;
-      for (int r : rows) b += 4 + (int64_t)(rp[r + 1] - rp[r]) * (4 + el);
-      return b;
-    };
-    // distinct X rows referenced by `rows` of the CSR (rp_d, ci_d)
-    auto distinct_cols = [&](const std::vector<int>& rows, const int* rp_d, const int* ci_d,
-                             int ncols) -> int64_t {
-      if (rows.empty()) return 0;
-      dbuf<int> rows_d(rows.size());
-      h2d(rows_d.p, rows.data(), rows.size(), st);
-      dbuf<uint8_t> mark(ncols);
-      TFG_CUDA(cudaMemsetAsync(mark.p, 0, ncols, st));
-      k_mark_cols<<<blocks_for((int64_t)rows.size() * 32), 256, 0, st>>>(
-          (int64_t)rows.size(), rows_d.p, rp_d, ci_d, mark.p);
-      TFG_LAUNCH_CHECK();
-      dbuf<unsigned long long> cnt(1);
-      TFG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
-      k_count_u8<<<256, 256, 0, st>>>(ncols, mark.p, cnt.p);
-      TFG_LAUNCH_CHECK();
-      unsigned long long h = 0;
-      d2h(&h, cnt.p, 1, st);
-      TFG_CUDA(cudaStreamSynchronize(st));
-      return (int64_t)h;
-    };
-    const int64_t ra = (int64_t)fo_rows.size();
-    if (ra) {
-      if (pr.b_is_dense)
-        pl.stage_bytes[0] = ra * bc * el + (int64_t)bc * cc * el + ra * cc * el;
-      else
-        pl.stage_bytes[0] = csr_rows_bytes(fo_rows, brp) +
-                            distinct_cols(fo_rows, pr.d_b_row_ptr, pr.d_b_col_idx, bc) * cc * el +
-                            ra * cc * el;
-    }
-    if (pl.n_ftiles) {
-      std::vector<int> ti, tj;  // first-op rows and fused j rows of fused tiles
-      std::vector<int> ilo(pl.n_ftiles), ihi(pl.n_ftiles);
-      d2h(ilo.data(), pl.ft_ilo.p, pl.n_ftiles, st);
-      d2h(ihi.data(), pl.ft_ihi.p, pl.n_ftiles, st);
-      tj.resize(pl.ft_nrows);
-      d2h(tj.data(), pl.ft_jrows.p, pl.ft_nrows, st);
-      std::vector<uint8_t> sp(n);
-      d2h(sp.data(), pl.spill.p, n, st);
-      TFG_CUDA(cudaStreamSynchronize(st));
-      int64_t spilled = 0;
-      for (int64_t v = 0; v < pl.n_ftiles; ++v)
-        for (int i = ilo[v]; i < ihi[v]; ++i) {
-          ti.push_back(i);
-          spilled += sp[i];
-        }
-      const int64_t w = (int64_t)ti.size();
-      int64_t b = 0;
-      if (pr.b_is_dense)
-        b = w * bc * el + (int64_t)bc * cc * el;
-      else
-        b = csr_rows_bytes(ti, brp) + distinct_cols(ti, pr.d_b_row_ptr, pr.d_b_col_idx, bc) * cc * el;
-      b += csr_rows_bytes(tj, arp) + (int64_t)tj.size() * cc * el + spilled * cc * el;
-      pl.stage_bytes[1] = b;
-    }
-    if (!second_rows.empty())
-      pl.d1_read_rows = distinct_cols(second_rows, pr.d_a_row_ptr, pr.d_a_col_idx, n);
-      pl.stage_bytes[2] = csr_rows_bytes(second_rows, arp) + pl.d1_read_rows * cc * el +
-                          (int64_t)second_rows.size() * cc * el;
-  }
-
-  phase("algorithmic bytes");
+  // algorithmic bytes per stage: computed on first use (tfg_plan_profile);
+  // the drop-in by-value call never needs them
+  pl.prof.reset(new PlanProfileCtx{std::move(fo_rows), std::move(second_rows), std::move(arp),
+                                   std::move(brp)});
   pl.launches = 0;
   if (pl.tc.on && (pl.n_fo_blocks > 0 || pl.n_ftiles > 0)) pl.launches += 1;  // C split
   if (pr.b_is_dense)
@@ -3067,6 +3111,7 @@ tfg_status tfg_plan_profile(tfg_plan* pl, void* d, void* stream, double stage_ms
   return guard([&] {
     if (!pl || !d) throw invalid_argument("plan_profile: null plan or output");
     cudaStream_t st = as_stream(stream);
+    compute_stage_bytes(*pl, st);
     cudaEvent_t ev[4];
     for (auto& e : ev) TFG_CUDA(cudaEventCreate(&e));
     plan_execute(*pl, d, st, ev);
@@ -3087,13 +3132,25 @@ tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d)
     const tfg_problem& h = *hp;
     if (h.n < 1) throw invalid_argument("problem: A must be square");
     const size_t el = h.dtype == TFG_F64 ? 8 : 4;
-    cudaStream_t st = nullptr;
+    // The plan needs A (and a sparse B's pattern) on the device, never the
+    // dense B: B and C stream in on a second stream, issued from a second
+    // host thread (so a pageable, hence synchronous, copy overlaps too), while
+    // the plan is built; execution waits for both.
+    cudaStream_t sa = nullptr, sb = nullptr;
+    TFG_CUDA(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
+    TFG_CUDA(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+    struct Streams {
+      cudaStream_t a, b;
+      ~Streams() {
+        cudaStreamSynchronize(a);
+        cudaStreamDestroy(a);
+        cudaStreamDestroy(b);
+      }
+    } streams{sa, sb};
+    AllocScope scope(sa);  // the inputs and D: stream-ordered, pooled across calls
     const int64_t annz = h.d_a_row_ptr[h.n];
     dbuf<int32_t> arp(h.n + 1), aci(std::max<int64_t>(annz, 1));
     dbuf<unsigned char> av(std::max<int64_t>(annz, 1) * el);
-    h2d(arp.p, h.d_a_row_ptr, h.n + 1, st);
-    h2d(aci.p, h.d_a_col_idx, annz, st);
-    h2d(av.p, static_cast<const unsigned char*>(h.d_a_val), annz * el, st);
     dbuf<int32_t> brp, bci;
     dbuf<unsigned char> bv, bd, c;
     tfg_problem d = h;
@@ -3101,33 +3158,70 @@ tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d)
     d.d_a_row_ptr = arp.p;
     d.d_a_col_idx = aci.p;
     d.d_a_val = av.p;
+    c.alloc((size_t)std::max(h.c_rows, 1) * std::max(h.c_cols, 1) * el);
+    d.d_c = c.p;
     if (h.b_is_dense) {
       bd.alloc((size_t)std::max(h.b_rows, 1) * std::max(h.b_cols, 1) * el);
-      h2d(bd.p, static_cast<const unsigned char*>(h.d_b_dense), (size_t)h.b_rows * h.b_cols * el,
-          st);
       d.d_b_dense = bd.p;
-    } else {
-      const int64_t bnnz = h.d_b_row_ptr[h.b_rows];
-      brp.alloc(h.b_rows + 1);
-      bci.alloc(std::max<int64_t>(bnnz, 1));
-      bv.alloc(std::max<int64_t>(bnnz, 1) * el);
-      h2d(brp.p, h.d_b_row_ptr, h.b_rows + 1, st);
-      h2d(bci.p, h.d_b_col_idx, bnnz, st);
-      h2d(bv.p, static_cast<const unsigned char*>(h.d_b_val), bnnz * el, st);
-      d.b_nnz = bnnz;
-      d.d_b_row_ptr = brp.p;
-      d.d_b_col_idx = bci.p;
-      d.d_b_val = bv.p;
     }
-    c.alloc((size_t)std::max(h.c_rows, 1) * std::max(h.c_cols, 1) * el);
-    h2d(c.p, static_cast<const unsigned char*>(h.d_c), (size_t)h.c_rows * h.c_cols * el, st);
-    d.d_c = c.p;
+    int dev = 0;
+    TFG_CUDA(cudaGetDevice(&dev));
+    cudaEvent_t allocated = nullptr;  // B and C were allocated in sa's order
+    TFG_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming));
+    struct Ev {
+      cudaEvent_t e;
+      ~Ev() { cudaEventDestroy(e); }
+    } ev{allocated};
+    TFG_CUDA(cudaEventRecord(allocated, sa));
+    cudaError_t berr = cudaSuccess;
+    std::thread upload_b([&] {
+      berr = cudaSetDevice(dev);
+      if (berr == cudaSuccess) berr = cudaStreamWaitEvent(sb, allocated, 0);
+      if (berr == cudaSuccess && h.b_is_dense)
+        berr = cudaMemcpyAsync(bd.p, h.d_b_dense, (size_t)h.b_rows * h.b_cols * el,
+                               cudaMemcpyHostToDevice, sb);
+      if (berr == cudaSuccess)
+        berr = cudaMemcpyAsync(c.p, h.d_c, (size_t)h.c_rows * h.c_cols * el, cudaMemcpyHostToDevice, sb);
+      if (berr == cudaSuccess) berr = cudaStreamSynchronize(sb);
+    });
+    struct Join {
+      std::thread& t;
+      ~Join() {
+        if (t.joinable()) t.join();
+      }
+    } join{upload_b};
+    h2d(arp.p, h.d_a_row_ptr, h.n + 1, sa);
+    h2d(aci.p, h.d_a_col_idx, annz, sa);
+    h2d(av.p, static_cast<const unsigned char*>(h.d_a_val), annz * el, sa);
+    if (!h.b_is_dense) {
+      if (h.d_b_row_ptr == h.d_a_row_ptr && h.d_b_col_idx == h.d_a_col_idx &&
+          h.d_b_val == h.d_a_val && h.b_rows == h.n) {  // B is A: upload once
+        d.b_nnz = annz;
+        d.d_b_row_ptr = arp.p;
+        d.d_b_col_idx = aci.p;
+        d.d_b_val = av.p;
+      } else {
+        const int64_t bnnz = h.d_b_row_ptr[h.b_rows];
+        brp.alloc(h.b_rows + 1);
+        bci.alloc(std::max<int64_t>(bnnz, 1));
+        bv.alloc(std::max<int64_t>(bnnz, 1) * el);
+        h2d(brp.p, h.d_b_row_ptr, h.b_rows + 1, sa);
+        h2d(bci.p, h.d_b_col_idx, bnnz, sa);
+        h2d(bv.p, static_cast<const unsigned char*>(h.d_b_val), bnnz * el, sa);
+        d.b_nnz = bnnz;
+        d.d_b_row_ptr = brp.p;
+        d.d_b_col_idx = bci.p;
+        d.d_b_val = bv.p;
+      }
+    }
     tfg_plan pl;
-    plan_create(d, s, st, pl);
+    plan_create(d, s, sa, pl);  // overlaps the upload of B and C
     dbuf<unsigned char> dd((size_t)h.n * h.c_cols * el);
-    plan_execute(pl, dd.p, st);
-    d2h(static_cast<unsigned char*>(h_d), dd.p, (size_t)h.n * h.c_cols * el, st);
-    TFG_CUDA(cudaStreamSynchronize(st));
+    upload_b.join();
+    TFG_CUDA(berr);
+    plan_execute(pl, dd.p, sa);
+    d2h(static_cast<unsigned char*>(h_d), dd.p, (size_t)h.n * h.c_cols * el, sa);
+    TFG_CUDA(cudaStreamSynchronize(sa));
   });
 }
 

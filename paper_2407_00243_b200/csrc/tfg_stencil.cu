@@ -523,44 +523,72 @@ int env_int(const char* name, int def) {
   return e ? atoi(e) : def;
 }
 
-// Every nonzero of the CSR decomposes as an in-grid neighbour of its row.
-bool check_geom(int n, const std::vector<int>& rp, const std::vector<int>& ci, int nx, int ny,
-                StencilGeom& g) {
-  const int64_t nxy = (int64_t)nx * ny;
-  if (nx < 3 || (ny > 1 && ny < 3) || n % nxy != 0) return false;
+// Every nonzero of the CSR decomposes as an in-grid neighbour of its row and
+// every row's columns strictly increase (the kernel finds a neighbour's value
+// by its rank in the row).  One warp per row; *fail set on the first
+// violation; *used gathers the 27-bit neighbour mask.
+__global__ void k_check_geom(int n, const int* __restrict__ rp, const int* __restrict__ ci, int nx,
+                             int ny, int* __restrict__ fail, unsigned* __restrict__ used) {
+  const long long nxy = (long long)nx * ny;
   const int nz = (int)(n / nxy);
-  bool used[27] = {};
-  for (int r = 0; r < n; ++r) {
-    const int x = r % nx, y = (int)((r / nx) % ny), z = (int)(r / nxy);
-    for (int k = rp[r]; k < rp[r + 1]; ++k) {
-      // the kernel finds a neighbour's value by its rank in the row, so the
-      // columns must be strictly increasing (no duplicates, sorted)
-      if (k > rp[r] && ci[k] <= ci[k - 1]) return false;
-      int64_t o = (int64_t)ci[k] - r;
+  const int lane = threadIdx.x & 31;
+  unsigned mask = 0;
+  bool bad = false;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n && !bad;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int x = (int)(r % nx), y = (int)((r / nx) % ny), z = (int)(r / nxy);
+    const int b = rp[r], e = rp[r + 1];
+    for (int k = b + lane; k < e; k += 32) {
+      const int c = ci[k];
+      if (k > b && c <= ci[k - 1]) bad = true;
+      long long o = (long long)c - r;
       int dz, dy = 0;
       if (ny > 1) {
         dz = o > nxy / 2 ? 1 : (o < -(nxy / 2) ? -1 : 0);
         o -= dz * nxy;
         dy = o > nx / 2 ? 1 : (o < -(nx / 2) ? -1 : 0);
-        o -= (int64_t)dy * nx;
+        o -= (long long)dy * nx;
       } else {
         dz = o > nx / 2 ? 1 : (o < -(nx / 2) ? -1 : 0);
-        o -= (int64_t)dz * nx;
+        o -= (long long)dz * nx;
       }
       const int dx = (int)o;
-      if (dx < -1 || dx > 1) return false;
-      if (x + dx < 0 || x + dx >= nx || y + dy < 0 || y + dy >= ny || z + dz < 0 ||
-          z + dz >= nz)
-        return false;
-      used[((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1)] = true;
+      if (dx < -1 || dx > 1 || x + dx < 0 || x + dx >= nx || y + dy < 0 || y + dy >= ny ||
+          z + dz < 0 || z + dz >= nz)
+        bad = true;
+      else
+        mask |= 1u << (((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1));
     }
+    bad = __any_sync(0xffffffffu, bad);
   }
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  if (lane == 0) {
+    if (bad) atomicExch(fail, 1);
+    if (mask) atomicOr(used, mask);
+  }
+}
+
+bool check_geom(int n, const int* rp_d, const int* ci_d, int nx, int ny, StencilGeom& g,
+                cudaStream_t st) {
+  const int64_t nxy = (int64_t)nx * ny;
+  if (nx < 3 || (ny > 1 && ny < 3) || n % nxy != 0) return false;
+  dbuf<int> flag(2);
+  TFG_CUDA(cudaMemsetAsync(flag.p, 0, 8, st));
+  const int64_t threads = (int64_t)n * 32;
+  const int blocks = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)sm_count() * 64);
+  k_check_geom<<<blocks, 256, 0, st>>>(n, rp_d, ci_d, nx, ny, flag.p,
+                                       reinterpret_cast<unsigned*>(flag.p + 1));
+  TFG_LAUNCH_CHECK();
+  int h[2] = {0, 0};
+  TFG_CUDA(cudaMemcpyAsync(h, flag.p, 8, cudaMemcpyDeviceToHost, st));
+  TFG_CUDA(cudaStreamSynchronize(st));
+  if (h[0] || h[1] == 0) return false;
   g.nx = nx;
   g.ny = ny;
-  g.nz = nz;
+  g.nz = (int)(n / nxy);
   g.d3 = ny > 1;
   g.K = 0;
-  for (int q = 0; q < 27; ++q) g.rank[q] = used[q] ? (int8_t)g.K++ : (int8_t)-1;
+  for (int q = 0; q < 27; ++q) g.rank[q] = ((unsigned)h[1] >> q & 1u) ? (int8_t)g.K++ : (int8_t)-1;
   return g.K > 0;
 }
 
@@ -568,27 +596,29 @@ bool check_geom(int n, const std::vector<int>& rp, const std::vector<int>& ci, i
 
 int stencil_env_enabled() { return env_int("TFG_STENCIL", 1); }
 
-bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& ci,
-                    StencilGeom& g) {
+bool stencil_detect(int n, const std::vector<int>& rp, const int* rp_d, const int* ci_d,
+                    StencilGeom& g, cudaStream_t st) {
   g = StencilGeom{};
-  if (n < 9 || (int)rp.size() < n + 1 || rp[n] == 0 || (int64_t)ci.size() < rp[n]) return false;
-  // the offset set (col - row) over all rows; a grid stencil has <= 27
+  if (n < 9 || (int)rp.size() < n + 1 || rp[n] == 0) return false;
+  // candidate geometries from the offsets (col - row) of a sample of rows
+  // (a grid stencil's interior rows carry its whole offset set); every
+  // candidate is then checked over ALL nonzeros on the device
   std::vector<int64_t> offs;
-  int pb = 0, pe = 0;  // previous row's CSR range: most rows repeat its offsets
-  for (int r = 0; r < n; ++r) {
+  std::vector<int> cols;
+  for (int q = 0; q < 64; ++q) {
+    const int r = (int)(((int64_t)2 * q + 1) * n / 128);
     const int b = rp[r], e = rp[r + 1];
-    bool same = e - b == pe - pb && r > 0;
-    for (int k = b; same && k < e; ++k) same = ci[k] - r == ci[pb + (k - b)] - (r - 1);
-    if (!same)
-      for (int k = b; k < e; ++k) {
-        const int64_t o = (int64_t)ci[k] - r;
-        if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
-          offs.push_back(o);
-          if (offs.size() > 27) return false;
-        }
+    if (e <= b || e - b > 64) continue;
+    cols.resize(e - b);
+    TFG_CUDA(cudaMemcpyAsync(cols.data(), ci_d + b, (size_t)(e - b) * 4, cudaMemcpyDeviceToHost, st));
+    TFG_CUDA(cudaStreamSynchronize(st));
+    for (int c : cols) {
+      const int64_t o = (int64_t)c - r;
+      if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+        offs.push_back(o);
+        if (offs.size() > 27) return false;
       }
-    pb = b;
-    pe = e;
+    }
   }
   std::sort(offs.begin(), offs.end());
   std::vector<int64_t> pos;
@@ -598,7 +628,7 @@ bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& c
   // x stride: the smallest offset >= 2 is nx + dx for some dx in {-1, 0, 1}
   for (int64_t nxc : {pos[0] + 1, pos[0], pos[0] - 1}) {
     if (nxc < 3 || nxc > n) continue;
-    if (check_geom(n, rp, ci, (int)nxc, 1, g)) return true;
+    if (check_geom(n, rp_d, ci_d, (int)nxc, 1, g, st)) return true;
     // 3-D: the smallest offset beyond the x line is nx*ny + dy*nx + dx
     for (int64_t o2 : pos) {
       if (o2 <= nxc + 1) continue;
@@ -608,7 +638,7 @@ bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& c
           if (nxy % nxc != 0) continue;
           const int64_t nyc = nxy / nxc;
           if (nyc < 3 || n % nxy != 0) continue;
-          if (check_geom(n, rp, ci, (int)nxc, (int)nyc, g)) return true;
+          if (check_geom(n, rp_d, ci_d, (int)nxc, (int)nyc, g, st)) return true;
         }
       break;
     }

@@ -60,10 +60,12 @@ struct StencilPlan {
   alignas(64) CUtensorMap xmap;  // X as (cc, nx, ny, nz), box (cw, tx + 2, tyh, 1)
 };
 
-// Detect the stencil structure of an n x n CSR (host copies of row_ptr and
-// col_idx).  Every nonzero must be an in-grid neighbour; false otherwise.
-bool stencil_detect(int n, const std::vector<int>& rp, const std::vector<int>& ci,
-                    StencilGeom& g);
+// Detect the stencil structure of an n x n CSR: candidate geometries from a
+// sample of rows (host row_ptr, a few device column indices), each checked
+// over every nonzero on the device (in-grid neighbour, strictly increasing
+// columns).  false: not a grid stencil.
+bool stencil_detect(int n, const std::vector<int>& rp, const int* rp_d, const int* ci_d,
+                    StencilGeom& g, cudaStream_t st);
 // Tile the grid for X (n x cc row-major, element size elem bytes) and encode
 // the X tensor map.  false: shape not supported (the plan keeps its SpMM).
 // Planes [zb, ze) only (a row-block partition; -1: the whole grid).
