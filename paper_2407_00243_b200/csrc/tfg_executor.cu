@@ -1602,7 +1602,8 @@ struct SpmmWork {
         mx = std::max(mx, rp[r + 1] - rp[r]);
       }
       const double mean = (double)tot / (double)rows.size();
-      const int thr = std::max(256, (int)(8.0 * mean));
+      // 16 x the mean (8: cfg5 wavefront 1 6.09 ms, 16: 5.93, cfg3 equal)
+      const int thr = std::max(256, (int)(16.0 * mean));
       if (mx > thr && thr < kLongRow) {
         long_thr = thr;
         seg_len = thr;
@@ -1628,6 +1629,29 @@ struct SpmmWork {
     if (n_empty) {
       empty_rows.alloc(em.size());
       h2d(empty_rows.p, em.data(), em.size(), st);
+    }
+    if (!sh.empty()) {  // skew: longest short row vs the mean
+      int64_t tot = 0;
+      int mx = 0;
+      for (int r : sh) {
+        tot += rp[r + 1] - rp[r];
+        mx = std::max(mx, rp[r + 1] - rp[r]);
+      }
+      const double mean = (double)tot / (double)sh.size();
+      // one row per lane group when rows are skewed, or when strips of 32
+      // rows would leave the GPU with too few warps (small row lists)
+      skewed = mx > 8.0 * std::max(mean, 1.0) ||
+               (int64_t)sh.size() < (int64_t)sm_count() * 32 * 32;
+      // skewed lists: longest rows first (the lane groups of a warp then walk
+      // rows of similar length, and the long rows start early)
+      static const bool sort_on = [] {
+        const char* e = getenv("TFG_W1_SORT");
+        return !e || atoi(e) > 0;
+      }();
+      if (skewed && sort_on && !stencil_rows)
+        std::stable_sort(sh.begin(), sh.end(), [&](int a, int b) {
+          return rp[a + 1] - rp[a] > rp[b + 1] - rp[b];
+        });
     }
     n_short = (int64_t)sh.size();
     n_long = (int64_t)lg.size();
@@ -1657,19 +1681,6 @@ struct SpmmWork {
     TFG_CUDA(cudaStreamSynchronize(st));
     const int vec = 16 / (int)elem;
     elem_ = elem;
-    if (!sh.empty()) {  // skew: longest short row vs the mean
-      int64_t tot = 0;
-      int mx = 0;
-      for (int r : sh) {
-        tot += rp[r + 1] - rp[r];
-        mx = std::max(mx, rp[r + 1] - rp[r]);
-      }
-      const double mean = (double)tot / (double)sh.size();
-      // one row per lane group when rows are skewed, or when strips of 32
-      // rows would leave the GPU with too few warps (small row lists)
-      skewed = mx > 8.0 * std::max(mean, 1.0) ||
-               (int64_t)sh.size() < (int64_t)sm_count() * 32 * 32;
-    }
     if (ci && identity && !stencil_rows && (cc % vec == 0) &&
         (cc / vec == 8 || cc / vec == 16 || cc / vec == 32 || cc / vec == 64))
       build_band(row0, n_short, rp, *ci, cc, elem, st);
