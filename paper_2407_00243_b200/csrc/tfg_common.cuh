@@ -4,8 +4,11 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -159,9 +162,85 @@ inline int sm_count() {
   return cached;
 }
 
+// Small host->device uploads without the copy engine.  Inside the drop-in
+// by-value call (tfg_run_host) the H2D copy engine is busy with gigabytes of
+// operands for ~0.2 s; a plan's own work-list uploads queued behind them
+// would stall plan creation for that long (measured: 130 ms).  With an
+// UploadScope active, h2d() stages the bytes in a pinned arena and a copy
+// kernel reads them over the bus (zero-copy), sharing only bandwidth.
+struct UploadArena {
+  unsigned char* base = nullptr;
+  size_t cap = 0, off = 0;
+  std::mutex mu;
+  static UploadArena& get() {
+    static UploadArena a;
+    return a;
+  }
+};
+struct UploadScope {
+  static UploadArena*& active() {
+    static thread_local UploadArena* a = nullptr;
+    return a;
+  }
+  cudaStream_t st;
+  bool owns = false;
+  explicit UploadScope(cudaStream_t s, size_t bytes = (size_t)256 << 20) : st(s) {
+    UploadArena& a = UploadArena::get();
+    if (active() || !a.mu.try_lock()) return;  // nested or in use elsewhere: plain copies
+    if (!a.base && cudaHostAlloc(reinterpret_cast<void**>(&a.base), bytes, cudaHostAllocDefault) ==
+                       cudaSuccess)
+      a.cap = bytes;
+    if (!a.base) {
+      cudaGetLastError();
+      a.mu.unlock();
+      return;
+    }
+    a.off = 0;
+    owns = true;
+    active() = &a;
+  }
+  ~UploadScope() {
+    if (!owns) return;
+    cudaStreamSynchronize(st);  // the copy kernels have read the arena
+    active() = nullptr;
+    UploadArena::get().mu.unlock();
+  }
+  UploadScope(const UploadScope&) = delete;
+  UploadScope& operator=(const UploadScope&) = delete;
+};
+#ifdef __CUDACC__
+static __global__ void k_upload_copy(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                     size_t n16, size_t bytes) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && threadIdx.x < (bytes & 15)) {
+    const size_t o = (n16 << 4) + threadIdx.x;
+    reinterpret_cast<unsigned char*>(dst)[o] = reinterpret_cast<const unsigned char*>(src)[o];
+  }
+}
+#endif
+
 template <class T>
 inline void h2d(T* d, const T* h, size_t count, cudaStream_t s) {
-  if (count) TFG_CUDA(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  if (!count) return;
+#ifdef __CUDACC__
+  if (UploadArena* a = UploadScope::active()) {
+    const size_t bytes = count * sizeof(T), need = (bytes + 255) & ~(size_t)255;
+    if (a->off + need <= a->cap && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+      unsigned char* stage = a->base + a->off;
+      a->off += need;
+      std::memcpy(stage, h, bytes);
+      const size_t n16 = bytes >> 4;
+      const unsigned blocks = (unsigned)std::min<size_t>(std::max<size_t>((n16 + 255) / 256, 1), 64);
+      k_upload_copy<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(stage),
+                                           reinterpret_cast<uint4*>(d), n16, bytes);
+      TFG_LAUNCH_CHECK();
+      return;
+    }
+  }
+#endif
+  TFG_CUDA(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
 }
 template <class T>
 inline void d2h(T* h, const T* d, size_t count, cudaStream_t s) {

@@ -1610,6 +1610,7 @@ struct SpmmWork {
       }
     }
     std::vector<int> em;
+    em.reserve(rows.size());
     for (int r : rows) {
       const int b = rp[r], e = rp[r + 1];
       if (e == b && !stencil_rows && ((size_t)cc * elem) % 16 == 0) {
@@ -1648,10 +1649,16 @@ struct SpmmWork {
         const char* e = getenv("TFG_W1_SORT");
         return !e || atoi(e) > 0;
       }();
-      if (skewed && sort_on && !stencil_rows)
-        std::stable_sort(sh.begin(), sh.end(), [&](int a, int b) {
-          return rp[a + 1] - rp[a] > rp[b + 1] - rp[b];
-        });
+      if (skewed && sort_on && !stencil_rows) {
+        // stable counting sort by descending length (lengths <= long_thr); a
+        // comparison sort of millions of rows costs ~0.2 s of plan creation
+        std::vector<int64_t> start((size_t)mx + 2, 0);
+        for (int r : sh) ++start[(size_t)(mx - (rp[r + 1] - rp[r])) + 1];
+        for (size_t l = 1; l < start.size(); ++l) start[l] += start[l - 1];
+        std::vector<int> sorted(sh.size());
+        for (int r : sh) sorted[(size_t)start[(size_t)(mx - (rp[r + 1] - rp[r]))]++] = r;
+        sh.swap(sorted);
+      }
     }
     n_short = (int64_t)sh.size();
     n_long = (int64_t)lg.size();
@@ -2172,6 +2179,11 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     TFG_CUDA(cudaStreamSynchronize(st));
     std::vector<int> f_ilo, f_ihi, f_rows;
     std::vector<int64_t> f_joff{0};
+    f_rows.reserve(jr0.size());
+    zero_rows.reserve(jr0.size());
+    f_ilo.reserve(nt0);
+    f_ihi.reserve(nt0);
+    f_joff.reserve(nt0 + 1);
     int w_max = 0;
     int64_t fused_here = 0;
     for (int64_t v = 0; v < nt0; ++v) {
@@ -2211,6 +2223,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
       pl.ft_jrows.alloc(f_rows.size());
       h2d(pl.ft_jrows.p, f_rows.data(), f_rows.size(), st);
       pl.ft_nrows = (int64_t)f_rows.size();
+        phase("  ft lists uploaded");
       if (pr.b_is_dense && pl.gemm_kind) {
         // v2: stage only the D1 rows the tile's fused rows read
         const int BN = pl.gemm_kind == 2 ? 128 : 64;
@@ -2231,6 +2244,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         std::vector<int> tc(pl.n_ftiles);
         d2h(tc.data(), tcount.p, tc.size(), st);
         TFG_CUDA(cudaStreamSynchronize(st));
+        phase("  marks + slots");
         const size_t gsm = fused_gemm_smem(pl);
         // stage capacity: two CTAs per SM when the GEMM ring leaves room
         const size_t per_cta = 2 * gsm + 16 * 1024 <= kFusedSmemMax ? kFusedSmemMax / 2 - 1024
@@ -2293,6 +2307,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         }
         pl.ft_wide.alloc(pl.n_ftiles);
         h2d(pl.ft_wide.p, wide.data(), wide.size(), st);
+        phase("  slice choice");
         pl.stage_cap = cap;
         pl.fused_smem = gsm + (size_t)cap * BN * pl.elem;
         if (pl.tc.on) {
@@ -2416,12 +2431,15 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
                        stencil_rows(fo_rows, gB, cc, pl.elem));
     attach_stencil(pl.fo_sparse, gB, pr.d_c, cc, pl.elem);
   }
+  phase("first-op work");
   // (c) second-op work (wavefront-1 rows, then the empty fused rows)
   if (!zero_rows.empty()) {  // ascending union, O(n) (a sort of millions of rows costs 0.5 s)
     std::vector<uint8_t> in(n, 0);
     for (int r : second_rows) in[r] = 1;
     for (int r : zero_rows) in[r] = 1;
+    const size_t total = second_rows.size() + zero_rows.size();
     second_rows.clear();
+    second_rows.reserve(total);
     for (int r = 0; r < n; ++r)
       if (in[r]) second_rows.push_back(r);
   }
@@ -2432,6 +2450,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     const StencilGeom gA =
         same ? gB : (arp[n] > 0 ? probe_stencil(n, arp, pr.d_a_row_ptr, pr.d_a_col_idx, st)
                                 : StencilGeom{});
+    phase("wave-1 row union + stencil probe");
     // host column indices only for the band layout: not a stencil, and a
     // list that is not skewed (R-MAT rows never band-stage)
     std::vector<int> aci;
@@ -2445,7 +2464,7 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
     if (partial) pl.w1_rows = second_rows;
     attach_stencil(pl.second, gA, pl.d1.p, cc, pl.elem);
   }
-  phase("first-op + wave-1 work");
+  phase("wave-1 work");
 
   // algorithmic bytes per stage: computed on first use (tfg_plan_profile);
   // the drop-in by-value call never needs them
@@ -3143,10 +3162,11 @@ tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d)
     const tfg_problem& h = *hp;
     if (h.n < 1) throw invalid_argument("problem: A must be square");
     const size_t el = h.dtype == TFG_F64 ? 8 : 4;
-    // The plan needs A (and a sparse B's pattern) on the device, never the
-    // dense B: B and C stream in on a second stream, issued from a second
-    // host thread (so a pageable, hence synchronous, copy overlaps too), while
-    // the plan is built; execution waits for both.
+    // The plan needs only the patterns (A's, and a sparse B's) on the device:
+    // row pointers and column indices go first, alone on the link; then the
+    // values, B and C stream in on a second stream, issued from a second host
+    // thread (so a pageable, hence synchronous, copy overlaps too), while the
+    // plan is built; execution waits for both.
     cudaStream_t sa = nullptr, sb = nullptr;
     TFG_CUDA(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
     TFG_CUDA(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
@@ -3175,24 +3195,77 @@ tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d)
       bd.alloc((size_t)std::max(h.b_rows, 1) * std::max(h.b_cols, 1) * el);
       d.d_b_dense = bd.p;
     }
+    const bool b_is_a = !h.b_is_dense && h.d_b_row_ptr == h.d_a_row_ptr &&
+                        h.d_b_col_idx == h.d_a_col_idx && h.d_b_val == h.d_a_val &&
+                        h.b_rows == h.n;  // B is A: upload once
+    int64_t bnnz = 0;
+    if (!h.b_is_dense) {
+      if (b_is_a) {
+        d.b_nnz = annz;
+        d.d_b_row_ptr = arp.p;
+        d.d_b_col_idx = aci.p;
+        d.d_b_val = av.p;
+      } else {
+        bnnz = h.d_b_row_ptr[h.b_rows];
+        brp.alloc(h.b_rows + 1);
+        bci.alloc(std::max<int64_t>(bnnz, 1));
+        bv.alloc(std::max<int64_t>(bnnz, 1) * el);
+        d.b_nnz = bnnz;
+        d.d_b_row_ptr = brp.p;
+        d.d_b_col_idx = bci.p;
+        d.d_b_val = bv.p;
+      }
+    }
     int dev = 0;
     TFG_CUDA(cudaGetDevice(&dev));
-    cudaEvent_t allocated = nullptr;  // B and C were allocated in sa's order
-    TFG_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming));
+    // patterns first (sa), then everything else (sb) once they are through
+    h2d(arp.p, h.d_a_row_ptr, h.n + 1, sa);
+    h2d(aci.p, h.d_a_col_idx, annz, sa);
+    if (!h.b_is_dense && !b_is_a) {
+      h2d(brp.p, h.d_b_row_ptr, h.b_rows + 1, sa);
+      h2d(bci.p, h.d_b_col_idx, bnnz, sa);
+    }
+    cudaEvent_t patterns = nullptr;  // allocations made and patterns uploaded, in sa's order
+    TFG_CUDA(cudaEventCreateWithFlags(&patterns, cudaEventDisableTiming));
     struct Ev {
       cudaEvent_t e;
       ~Ev() { cudaEventDestroy(e); }
-    } ev{allocated};
-    TFG_CUDA(cudaEventRecord(allocated, sa));
+    } ev{patterns};
+    TFG_CUDA(cudaEventRecord(patterns, sa));
     cudaError_t berr = cudaSuccess;
+    // in pieces, at most two queued at a time: the copy engine serves copies
+    // in submission order, so the plan's own small uploads (work lists, on
+    // sa) wait for two pieces instead of for the whole of B
+    cudaEvent_t piece_ev[2] = {nullptr, nullptr};
+    for (auto& e : piece_ev) TFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct PieceEv {
+      cudaEvent_t* e;
+      ~PieceEv() {
+        cudaEventDestroy(e[0]);
+        cudaEventDestroy(e[1]);
+      }
+    } piece_guard{piece_ev};
+    size_t piece_no = 0;
+    auto upload = [&](void* dst, const void* src, size_t bytes) {
+      constexpr size_t kPiece = (size_t)16 << 20;
+      for (size_t o = 0; o < bytes && berr == cudaSuccess; o += kPiece, ++piece_no) {
+        if (piece_no >= 2) berr = cudaEventSynchronize(piece_ev[piece_no & 1]);
+        if (berr == cudaSuccess)
+          berr = cudaMemcpyAsync(static_cast<unsigned char*>(dst) + o,
+                                 static_cast<const unsigned char*>(src) + o,
+                                 std::min(kPiece, bytes - o), cudaMemcpyHostToDevice, sb);
+        if (berr == cudaSuccess) berr = cudaEventRecord(piece_ev[piece_no & 1], sb);
+      }
+    };
     std::thread upload_b([&] {
       berr = cudaSetDevice(dev);
-      if (berr == cudaSuccess) berr = cudaStreamWaitEvent(sb, allocated, 0);
+      if (berr == cudaSuccess) berr = cudaStreamWaitEvent(sb, patterns, 0);
       if (berr == cudaSuccess && h.b_is_dense)
-        berr = cudaMemcpyAsync(bd.p, h.d_b_dense, (size_t)h.b_rows * h.b_cols * el,
-                               cudaMemcpyHostToDevice, sb);
-      if (berr == cudaSuccess)
-        berr = cudaMemcpyAsync(c.p, h.d_c, (size_t)h.c_rows * h.c_cols * el, cudaMemcpyHostToDevice, sb);
+        upload(bd.p, h.d_b_dense, (size_t)h.b_rows * h.b_cols * el);
+      if (berr == cudaSuccess) upload(c.p, h.d_c, (size_t)h.c_rows * h.c_cols * el);
+      if (berr == cudaSuccess && annz > 0) upload(av.p, h.d_a_val, (size_t)annz * el);
+      if (berr == cudaSuccess && !h.b_is_dense && !b_is_a && bnnz > 0)
+        upload(bv.p, h.d_b_val, (size_t)bnnz * el);
       if (berr == cudaSuccess) berr = cudaStreamSynchronize(sb);
     });
     struct Join {
@@ -3201,38 +3274,29 @@ tfg_status tfg_run_host(const tfg_problem* hp, const tfg_schedule* s, void* h_d)
         if (t.joinable()) t.join();
       }
     } join{upload_b};
-    h2d(arp.p, h.d_a_row_ptr, h.n + 1, sa);
-    h2d(aci.p, h.d_a_col_idx, annz, sa);
-    h2d(av.p, static_cast<const unsigned char*>(h.d_a_val), annz * el, sa);
-    if (!h.b_is_dense) {
-      if (h.d_b_row_ptr == h.d_a_row_ptr && h.d_b_col_idx == h.d_a_col_idx &&
-          h.d_b_val == h.d_a_val && h.b_rows == h.n) {  // B is A: upload once
-        d.b_nnz = annz;
-        d.d_b_row_ptr = arp.p;
-        d.d_b_col_idx = aci.p;
-        d.d_b_val = av.p;
-      } else {
-        const int64_t bnnz = h.d_b_row_ptr[h.b_rows];
-        brp.alloc(h.b_rows + 1);
-        bci.alloc(std::max<int64_t>(bnnz, 1));
-        bv.alloc(std::max<int64_t>(bnnz, 1) * el);
-        h2d(brp.p, h.d_b_row_ptr, h.b_rows + 1, sa);
-        h2d(bci.p, h.d_b_col_idx, bnnz, sa);
-        h2d(bv.p, static_cast<const unsigned char*>(h.d_b_val), bnnz * el, sa);
-        d.b_nnz = bnnz;
-        d.d_b_row_ptr = brp.p;
-        d.d_b_col_idx = bci.p;
-        d.d_b_val = bv.p;
-      }
-    }
+    const bool dbg_t = getenv("TFG_DEBUG") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, bool sync) {
+      if (!dbg_t) return;
+      if (sync) cudaStreamSynchronize(sa);
+      fprintf(stderr, "[tfg] run_host %-22s at %8.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
+    };
+    mark("patterns queued", false);
+    UploadScope staged(sa);  // the plan's work lists bypass the busy H2D copy engine
     tfg_plan pl;
-    plan_create(d, s, sa, pl);  // overlaps the upload of B and C
+    plan_create(d, s, sa, pl);  // overlaps the upload of values, B and C
+    mark("plan created", false);
     dbuf<unsigned char> dd((size_t)h.n * h.c_cols * el);
     upload_b.join();
     TFG_CUDA(berr);
+    mark("operands uploaded", false);
     plan_execute(pl, dd.p, sa);
+    mark("executed", true);
     d2h(static_cast<unsigned char*>(h_d), dd.p, (size_t)h.n * h.c_cols * el, sa);
     TFG_CUDA(cudaStreamSynchronize(sa));
+    mark("D downloaded", false);
   });
 }
 
