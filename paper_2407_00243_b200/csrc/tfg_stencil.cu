@@ -20,6 +20,10 @@ using dev::stv;
 constexpr int kMaxNS = 8;      // plane ring depth cap
 constexpr size_t kSliceBytes = 512;  // column slice of X / out per CTA
 constexpr size_t kSmemBudget = 224 * 1024;
+// value slots per warp: 3-D output planes keep their values for three steps
+// (z-sliding accumulators) and load them four planes ahead; 2-D: two ahead
+template <bool D3>
+constexpr int kValueSlots = D3 ? 5 : 3;
 
 // One sparse operand (a stencil CSR) of a kernel.
 struct OpArgs {
@@ -359,6 +363,91 @@ __device__ __forceinline__ void stencil_points(const StencilArgs& a, const OpArg
     if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * ostride, acc[m]);
 }
 
+// z-sliding accumulation (3-D full-box interior groups).  Instead of reading
+// the three X planes z-1, z, z+1 again for every output plane (each X row 9
+// times), one pass over the NEWEST plane p adds its rows to three output
+// planes at once: as dz = +1 of output p-1 (accA, that plane's values of
+// lines 6..8), dz = 0 of output p (accB, lines 3..5) and dz = -1 of output
+// p+1 (accC, lines 0..2) -- each X row is read from shared memory 3 times
+// instead of 9.  An output plane still receives its terms in ascending
+// (dz, dy, dx) order (dz = -1 from plane z-1 first, then plane z, then z+1,
+// each in dy, dx order), so the bits equal stencil_compute's.  MASK selects
+// the live targets (bit 0 accA, 1 accB, 2 accC): planes that are not full-box
+// groups, or lie outside the item, are skipped.
+template <class T, int M, int ROW, bool EXACT, int MASK>
+__device__ __forceinline__ void slide_plane(const T* __restrict__ P, int wy, int col0, int lane,
+                                            const T* __restrict__ svA, const T* __restrict__ svB,
+                                            const T* __restrict__ svC,
+                                            T (&accA)[M][16 / sizeof(T)],
+                                            T (&accB)[M][16 / sizeof(T)],
+                                            T (&accC)[M][16 / sizeof(T)]) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int CW = (int)(kSliceBytes / sizeof(T));
+  constexpr int NL = 9;
+  auto load_line = [&](const T* sv, int l, T(&vl)[M][4]) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const T* q = sv + m * 4 * NL + 4 * l;
+      if constexpr (sizeof(T) == 8) {
+        T v01[2];
+        ldv<T, 2>(v01, q);
+        vl[m][0] = v01[0];
+        vl[m][1] = v01[1];
+        vl[m][2] = q[2];
+      } else {
+        ldv<T, 4>(vl[m], q);
+      }
+    }
+  };
+#pragma unroll
+  for (int dyi = 0; dyi < 3; ++dyi) {
+    const T* base = P + ((wy + dyi) * ROW + col0) * CW + lane * VEC;
+    T vA[M][4], vB[M][4], vC[M][4];
+    if constexpr ((MASK & 1) != 0) load_line(svA, 6 + dyi, vA);
+    if constexpr ((MASK & 2) != 0) load_line(svB, 3 + dyi, vB);
+    if constexpr ((MASK & 4) != 0) load_line(svC, dyi, vC);
+#pragma unroll
+    for (int k = 0; k < M + 2; ++k) {
+      T xr[VEC];
+      ldv<T, VEC>(xr, base + k * CW);
+      if constexpr ((MASK & 4) != 0) {  // dz = -1 terms come first in their output's order
+        if (k < M) axpy<T, VEC, EXACT>(accC[k], vC[k][0], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC, EXACT>(accC[k - 1], vC[k - 1][1], xr);
+        if (k >= 2) axpy<T, VEC, EXACT>(accC[k - 2], vC[k - 2][2], xr);
+      }
+      if constexpr ((MASK & 2) != 0) {
+        if (k < M) axpy<T, VEC, EXACT>(accB[k], vB[k][0], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC, EXACT>(accB[k - 1], vB[k - 1][1], xr);
+        if (k >= 2) axpy<T, VEC, EXACT>(accB[k - 2], vB[k - 2][2], xr);
+      }
+      if constexpr ((MASK & 1) != 0) {
+        if (k < M) axpy<T, VEC, EXACT>(accA[k], vA[k][0], xr);
+        if (k >= 1 && k - 1 < M) axpy<T, VEC, EXACT>(accA[k - 1], vA[k - 1][1], xr);
+        if (k >= 2) axpy<T, VEC, EXACT>(accA[k - 2], vA[k - 2][2], xr);
+      }
+    }
+  }
+}
+
+template <class T, int M, int ROW, bool EXACT>
+__device__ __forceinline__ void slide_plane_masked(unsigned mask, const T* __restrict__ P, int wy,
+                                                   int col0, int lane, const T* __restrict__ svA,
+                                                   const T* __restrict__ svB,
+                                                   const T* __restrict__ svC,
+                                                   T (&accA)[M][16 / sizeof(T)],
+                                                   T (&accB)[M][16 / sizeof(T)],
+                                                   T (&accC)[M][16 / sizeof(T)]) {
+  switch (mask) {  // warp-uniform
+#define TFG_SLIDE(MK)                                                                          \
+  case MK:                                                                                     \
+    slide_plane<T, M, ROW, EXACT, MK>(P, wy, col0, lane, svA, svB, svC, accA, accB, accC);     \
+    break;
+    TFG_SLIDE(1) TFG_SLIDE(2) TFG_SLIDE(3) TFG_SLIDE(4) TFG_SLIDE(5) TFG_SLIDE(6) TFG_SLIDE(7)
+#undef TFG_SLIDE
+    default: break;
+  }
+}
+
 template <class T, bool D3, int NW, int M, int MINB, bool EXACT>
 __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     k_spmm_stencil(const __grid_constant__ CUtensorMap xmap, const StencilArgs a) {
@@ -408,10 +497,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   constexpr int VR = (M * (D3 ? 27 : 9) + 31) / 32;  // value elements per lane and plane
   constexpr int VS0 = VR * 32;
   constexpr int VS = VS0 > M * 4 * (D3 ? 9 : 3) ? VS0 : M * 4 * (D3 ? 9 : 3);  // value slot
-  T* svb = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * 3 * VS;
+  // 3-D: z-sliding accumulators (slide_plane); an output plane's values are
+  // then in use over three steps, so its ring is deeper and loaded further ahead
+  constexpr bool SLIDE = D3;
+  constexpr int VSL = kValueSlots<D3>;  // value slots per warp
+  constexpr int VAHEAD = SLIDE ? 4 : 2;  // values are issued this many planes ahead
+  T* svb = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * VSL * VS;
   int* srp = reinterpret_cast<int*>(reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) +
-                                    (size_t)NW * 3 * VS) + warp * 8 * 16;
+                                    (size_t)NW * VSL * VS) + warp * 8 * 16;
   const int wy = D3 ? warp : 0, wx = D3 ? 0 : warp;
+  int pidx[VR];  // padded slot position of this lane's value elements (loop invariant)
+#pragma unroll
+  for (int i = 0; i < VR; ++i) pidx[i] = pad_index<D3>(lane + 32 * i);
   int s0 = 0;        // ring slot of the current item's plane z-1
   uint32_t p0 = 0;   // its full-barrier phase parity
   const OpArgs& opa = a.op;
@@ -438,31 +535,63 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     auto issue_vals = [&](int jj) {  // row pointers of plane jj must be visible
       if (!wlive || jj >= nzl) return;
       const int v0 = srp[(jj & 7) * 16], v1 = srp[(jj & 7) * 16 + M];
-      T* dst = svb + (jj % 3) * VS;
+      T* dst = svb + (jj % VSL) * VS;
       // the compute side takes the padded full-box path exactly when this holds
       const bool pad = opa.full && valid != 0 && v1 - v0 == M * (D3 ? 27 : 9);
 #pragma unroll
       for (int i = 0; i < VR; ++i) {
         const int t = lane + 32 * i;
-        if (v0 + t < v1) cp_async_ca<sizeof(T)>(dst + (pad ? pad_index<D3>(t) : t), av + v0 + t);
+        if (v0 + t < v1) cp_async_ca<sizeof(T)>(dst + (pad ? pidx[i] : t), av + v0 + t);
       }
     };
-    issue_rp(0);
-    issue_rp(1);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    issue_vals(0);
-    issue_rp(2);
-    cp_async_commit();
-    issue_vals(1);
-    issue_rp(3);
-    cp_async_commit();
-    for (int j = 0; j < nzl; ++j) {
-      cp_async_wait<1>();  // values of plane j, row pointers of plane j + 2
+    // full-box interior group at output plane jj of this item (warp-uniform)
+    auto fast_at = [&](int jj) {
+      if (jj >= nzl || !opa.full || valid == 0) return false;
+      return srp[(jj & 7) * 16 + M] - srp[(jj & 7) * 16] == M * (D3 ? 27 : 9);
+    };
+    constexpr int VEC = 16 / sizeof(T);
+    [[maybe_unused]] T acc3[3][M][VEC];  // SLIDE: output planes j, j + 1, j + 2
+    [[maybe_unused]] bool f0 = false, f1 = false, f2 = false;
+    if constexpr (SLIDE) {
+      issue_rp(0);
+      issue_rp(1);
+      issue_rp(2);
+      issue_rp(3);
+      cp_async_commit();
+      cp_async_wait<0>();
       __syncwarp();
-      issue_vals(j + 2);
-      issue_rp(j + 4);
+      issue_vals(0);
+      issue_vals(1);
+      issue_vals(2);
+      issue_rp(4);
+      cp_async_commit();
+      issue_vals(3);
+      issue_rp(5);
+      cp_async_commit();
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc3[q][m][v] = T(0);
+    } else {
+      issue_rp(0);
+      issue_rp(1);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+      issue_vals(0);
+      issue_rp(2);
+      cp_async_commit();
+      issue_vals(1);
+      issue_rp(3);
+      cp_async_commit();
+    }
+    for (int j = 0; j < nzl; ++j) {
+      cp_async_wait<1>();  // values up to plane j + VAHEAD - 2, row pointers two further
+      __syncwarp();
+      issue_vals(j + VAHEAD);
+      issue_rp(j + VAHEAD + 2);
       cp_async_commit();
       const int rp_j = live ? srp[(j & 7) * 16 + lane] : 0;
       // ring positions of planes z-1 (s0), z (s1), z+1 (s2)
@@ -478,11 +607,50 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       }
       s_bar_wait(&full[s2], p2);
       const int rb = r0 + j * a.nxy;
-      stencil_points<T, D3, M, TL::ROW, true, EXACT>(
-          a, opa, planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
-          planes + (size_t)s2 * a.plane_elems, svb + (j % 3) * VS, rp_j, valid, wy, wx * M, rb,
-          x, y, z0 + j, outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * (16 / sizeof(T)),
-          a.cc, lane);
+      const T* P0 = planes + (size_t)s0 * a.plane_elems;
+      const T* P1 = planes + (size_t)s1 * a.plane_elems;
+      const T* P2 = planes + (size_t)s2 * a.plane_elems;
+      T* const outp = outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * VEC;
+      bool slid = false;
+      if constexpr (SLIDE) {
+        const T* sv0 = svb + (j % VSL) * VS;
+        const T* sv1 = svb + ((j + 1) % VSL) * VS;
+        const T* sv2 = svb + ((j + 2) % VSL) * VS;
+        if (j == 0) {
+          f0 = fast_at(0);
+          f1 = fast_at(1);
+          // planes z0-1 and z0 of the item: dz = -1 and 0 of output 0, dz = -1 of output 1
+          slide_plane_masked<T, M, TL::ROW, EXACT>(f0 ? 4u : 0u, P0, wy, wx * M, lane, sv0, sv0, sv0,
+                                                   acc3[0], acc3[0], acc3[0]);
+          slide_plane_masked<T, M, TL::ROW, EXACT>((f0 ? 2u : 0u) | (f1 ? 4u : 0u), P1, wy, wx * M,
+                                                   lane, sv0, sv0, sv1, acc3[0], acc3[0], acc3[1]);
+        }
+        f2 = fast_at(j + 2);
+        // the newest plane (z+1): dz = +1 of output j, 0 of j + 1, -1 of j + 2
+        slide_plane_masked<T, M, TL::ROW, EXACT>((f0 ? 1u : 0u) | (f1 ? 2u : 0u) | (f2 ? 4u : 0u), P2,
+                                                 wy, wx * M, lane, sv0, sv1, sv2, acc3[0], acc3[1],
+                                                 acc3[2]);
+        if (f0) {
+#pragma unroll
+          for (int m = 0; m < M; ++m)
+            if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * a.cc, acc3[0][m]);
+          slid = true;
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            acc3[0][m][v] = acc3[1][m][v];
+            acc3[1][m][v] = acc3[2][m][v];
+            acc3[2][m][v] = T(0);
+          }
+        f0 = f1;
+        f1 = f2;
+      }
+      if (!slid)
+        stencil_points<T, D3, M, TL::ROW, true, EXACT>(a, opa, P0, P1, P2, svb + (j % VSL) * VS, rp_j,
+                                                       valid, wy, wx * M, rb, x, y, z0 + j, outp,
+                                                       a.cc, lane);
       __syncwarp();
       if (lane == 0) {
         s_bar_arrive(&empty[s0]);
@@ -684,7 +852,8 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   // per warp: 3 value slots + 8 row-pointer slots (consumer cp.async ring)
   const size_t vslot = std::max<size_t>((sp.M * (g.d3 ? 27 : 9) + 31) / 32 * 32,
                                         (size_t)sp.M * 4 * (g.d3 ? 9 : 3));
-  const size_t vbytes = (size_t)sp.nw * (3 * vslot * elem + 8 * 16 * 4);
+  const size_t vbytes = (size_t)sp.nw * ((g.d3 ? kValueSlots<true> : kValueSlots<false>) * vslot * elem +
+                                         8 * 16 * 4);
   // CTAs per SM, then the deepest ring that fits (>= 3 planes in use)
   const int per_env = env_int("TFG_STENCIL_CTAS", 0);
   int per_sm = per_env > 0 ? std::min(per_env, sp.nw == 8 ? 2 : 4) : (sp.nw == 8 ? (g.d3 ? 1 : 2) : 3);
