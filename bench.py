@@ -308,6 +308,19 @@ def _stage_profile(plan, out, stream, flush, reps=5):
     return {k: (float(np.mean([m for m, _ in v])), int(v[0][1])) for k, v in stages.items()}
 
 
+# why a stage's DRAM traffic exceeds its algorithmic bytes (profiles/)
+TRAFFIC_NOTES = {
+    ("cfg5", "wave1_spmm"): (
+        "gathers of 256-byte D1 rows: 258.7 M nonzeros, 24 % of them in columns outside the 262 144 "
+        "most-gathered (64 MB of D1) -- 15.8 GB of compulsory misses for a cache that size "
+        "(profiles/r02_col_popularity.json); measured L2 hit rate 51-58 %; R-MAT rows have no "
+        "column locality to reorder for"),
+    ("cfg3", "wave1_spmm"): (
+        "gathers of 512-byte D1 rows of an R-MAT graph: misses are compulsory for the L2 size "
+        "(profiles/r02_col_popularity.json)"),
+}
+
+
 def _traffic(config, stage):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(tp):
@@ -622,6 +635,11 @@ def run_ours(args, rank, world, dist):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
                      "traffic_over_algorithmic": traffic / dom_bytes if traffic and dom_bytes else None,
+                     # the same kernel(s) by the DRAM bytes ncu counted instead of
+                     # the algorithmic ones: how busy HBM really is while they run
+                     "dram_frac_of_peak": (traffic / (dom_ms * 1e-3) / 1e9 / peak
+                                           if traffic and dom_ms > 0 else None),
+                     "traffic_note": TRAFFIC_NOTES.get((args.config, dom)),
                      "peak_source": peak_src,
                      "compute": cr},
         "cpu_baseline": cpu,
