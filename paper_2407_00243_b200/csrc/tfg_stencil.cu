@@ -532,22 +532,74 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       if (live && jj < nzl) cp_async_ca<4>(srp + (jj & 7) * 16 + lane, opa.rp + min(r0 + jj * a.nxy + lane, a.n));
     };
     const bool wlive = yvalid && x < a.nx;  // warp-uniform: the warp has points
+    // Staging of an output plane's values, and with it the plane's path
+    // (3-D; recorded in the row-pointer slot's spare word for fast_at):
+    //  2  interior full-box group: value t of the group at padded slot pidx
+    //  1  every point of the group is a grid-face point holding exactly its
+    //     in-grid neighbours: the same padded slots by neighbour POSITION, a
+    //     zero stored where a neighbour lies outside the grid -- the X plane
+    //     is zero-filled there too, so the full-box code adds an exact +0 and
+    //     face, edge and corner groups cost what interior groups do
+    //  0  anything else (rows missing in-grid neighbours): values as stored,
+    //     per-point paths
     auto issue_vals = [&](int jj) {  // row pointers of plane jj must be visible
       if (!wlive || jj >= nzl) return;
-      const int v0 = srp[(jj & 7) * 16], v1 = srp[(jj & 7) * 16 + M];
+      const int* rpl = srp + (jj & 7) * 16;
+      const int v0 = rpl[0], v1 = rpl[M];
       T* dst = svb + (jj % VSL) * VS;
       // the compute side takes the padded full-box path exactly when this holds
       const bool pad = opa.full && valid != 0 && v1 - v0 == M * (D3 ? 27 : 9);
+      if constexpr (SLIDE) {
+        int mode = pad ? 2 : 0;
+        unsigned face = 0;
+        if (!pad && opa.full && valid != 0) {
+          const int pz = z0 + jj;
+          face = (1u << 27) - 1u;
+          if (y == 0) face &= ~nb_bits(1, -1);
+          if (y == a.ny - 1) face &= ~nb_bits(1, 1);
+          if (pz == 0) face &= ~nb_bits(2, -1);
+          if (pz == a.nz - 1) face &= ~nb_bits(2, 1);
+          // lanes 0..M-1 check their point: outside the grid, or exactly its in-grid neighbours
+          bool ok = true;
+          if (lane < M && ((valid >> lane) & 1u)) {
+            unsigned pmm = face;
+            if (x + lane == 0) pmm &= ~nb_bits(0, -1);
+            if (x + lane == a.nx - 1) pmm &= ~nb_bits(0, 1);
+            ok = rpl[lane + 1] - rpl[lane] == __popc(pmm);
+          }
+          mode = __all_sync(0xffffffffu, ok) ? 1 : 0;
+        }
+        if (lane == 0) srp[(jj & 7) * 16 + 15] = mode;
+        if (mode == 1) {
+#pragma unroll
+          for (int i = 0; i < VR; ++i) {
+            const int t = lane + 32 * i;  // neighbour position t = m * 27 + q
+            if (t >= M * 27) continue;
+            const int m = t / 27, q = t - m * 27;
+            unsigned pmm = ((valid >> m) & 1u) ? face : 0u;
+            if (x + m == 0) pmm &= ~nb_bits(0, -1);
+            if (x + m == a.nx - 1) pmm &= ~nb_bits(0, 1);
+            if ((pmm >> q) & 1u)
+              cp_async_ca<sizeof(T)>(dst + pidx[i], av + rpl[m] + __popc(pmm & ((1u << q) - 1u)));
+            else
+              dst[pidx[i]] = T(0);
+          }
+          return;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < VR; ++i) {
         const int t = lane + 32 * i;
         if (v0 + t < v1) cp_async_ca<sizeof(T)>(dst + (pad ? pidx[i] : t), av + v0 + t);
       }
     };
-    // full-box interior group at output plane jj of this item (warp-uniform)
+    // the group at output plane jj of this item takes the full-box code (warp-uniform)
     auto fast_at = [&](int jj) {
       if (jj >= nzl || !opa.full || valid == 0) return false;
-      return srp[(jj & 7) * 16 + M] - srp[(jj & 7) * 16] == M * (D3 ? 27 : 9);
+      if constexpr (SLIDE)
+        return srp[(jj & 7) * 16 + 15] != 0;
+      else
+        return srp[(jj & 7) * 16 + M] - srp[(jj & 7) * 16] == M * (D3 ? 27 : 9);
     };
     constexpr int VEC = 16 / sizeof(T);
     [[maybe_unused]] T acc3[3][M][VEC];  // SLIDE: output planes j, j + 1, j + 2
@@ -876,8 +928,12 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
   const int zc_env = env_int("TFG_STENCIL_ZC", 0);
   int best = nzr;
   double best_cost = 1e300;
-  // short chunks measured best on cfg2 (16 planes: 0.239 ms vs 0.26 at 24-28)
-  for (int zc = std::min(8, nzr); zc <= std::min(16, std::max(1, nzr)); ++zc) {
+  // 2-D: short chunks measured best on cfg2 (16 planes: 0.239 ms vs 0.26 at
+  // 24-28).  3-D: an item pays its two extra planes and a prologue, and face
+  // groups cost what interior groups do, so long chunks win (cfg4 per pass:
+  // 16 planes 1.355 ms, 32 1.313, 64 1.304, 128 1.297)
+  for (int zc = std::min(8, nzr); zc <= (g.d3 ? std::max(1, nzr) : std::min(16, std::max(1, nzr)));
+       ++zc) {
     const int64_t nzc = (nzr + zc - 1) / zc;
     const int64_t items = tiles * nzc;
     const double waves = (double)((items + sp.grid - 1) / sp.grid);
