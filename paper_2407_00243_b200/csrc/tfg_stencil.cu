@@ -169,6 +169,128 @@ __device__ __forceinline__ int pad_index(int t) {  // t = m * K + 3 l + j
   return m * (4 * (D3 ? 9 : 3)) + 4 * l + (r - 3 * l);
 }
 
+// The per-point paths of one output plane's M points (grid faces and rows
+// missing in-grid neighbours), restricted to the neighbours with dz + 1 in
+// [dz_lo, dz_hi): all three planes at once (0, 3), or one input plane at a
+// time in ascending dz (the z-sliding loop; P0 = P1 = P2 = that plane).  acc
+// is accumulated into, not cleared.
+template <class T, bool D3, int M, int ROW, bool EXACT>
+__device__ __forceinline__ void stencil_slow(const StencilArgs& a, const OpArgs& op,
+                                             const T* __restrict__ P0, const T* __restrict__ P1,
+                                             const T* __restrict__ P2, const T* __restrict__ sv,
+                                             int rpl, unsigned valid, int wy, int col0, int rbase,
+                                             int px, int py, int pz, int lane, int dz_lo, int dz_hi,
+                                             T (&acc)[M][16 / sizeof(T)]) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int CW = (int)(kSliceBytes / sizeof(T));
+  constexpr int NL = D3 ? 9 : 3;
+  const int v0 = __shfl_sync(0xffffffffu, rpl, 0);
+  // Grid-face points: a row whose nonzero count equals the number of its
+  // in-grid stencil neighbours holds exactly those (every nonzero was checked
+  // to be an in-grid neighbour at plan time), so its value for neighbour bit
+  // q sits at popc(mask & (2^q - 1)) -- the same compile-time loop as the
+  // fast path, predicated per point.  Other rows (missing in-grid
+  // neighbours) walk their own CSR entries.
+  int vb[M + 1];
+#pragma unroll
+  for (int m = 0; m <= M; ++m) vb[m] = __shfl_sync(0xffffffffu, rpl, m);
+  unsigned pm[M];
+  unsigned geo = 0;
+  {
+    unsigned face = op.used;
+    if (D3) {
+      if (py == 0) face &= ~nb_bits(1, -1);
+      if (py == a.ny - 1) face &= ~nb_bits(1, 1);
+    }
+    if (pz == 0) face &= ~nb_bits(D3 ? 2 : 2, -1);
+    if (pz == a.nz - 1) face &= ~nb_bits(2, 1);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      unsigned pmm = face;
+      if (px + m == 0) pmm &= ~nb_bits(0, -1);
+      if (px + m == a.nx - 1) pmm &= ~nb_bits(0, 1);
+      pm[m] = pmm;
+      if (((valid >> m) & 1u) && vb[m + 1] - vb[m] == __popc(pmm)) geo |= 1u << m;
+    }
+  }
+  if (geo) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int dz = D3 ? l / 3 - 1 : l - 1;
+      const int dy = D3 ? l % 3 - 1 : 0;
+      const int li = (dz + 1) * 3 + (dy + 1);
+      if (!(op.used & (7u << (3 * li)))) continue;
+      if (dz + 1 < dz_lo || dz + 1 >= dz_hi) continue;
+      const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+      const T* base = P + ((D3 ? (wy + 1 + dy) * ROW : 0) + col0) * CW + lane * VEC;
+      // the line's values of all M points first (independent shared loads,
+      // absent neighbours read a dummy slot), then the predicated updates:
+      // a face group costs about what an interior group does, so the CTA's
+      // other warps are not held at the plane ring by it
+      T vl[M][3];
+      unsigned pr = 0;  // bit 3 m + j: point m has neighbour dx = j - 1 on this line
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const unsigned bits = ((geo >> m) & 1u) ? (pm[m] >> (3 * li)) & 7u : 0u;
+        pr |= bits << (3 * m);
+        // value index of the line's first present neighbour, then +1 per bit
+        int idx = vb[m] - v0 + __popc(pm[m] & ((1u << (3 * li)) - 1u));
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const bool has = (bits >> j) & 1u;
+          vl[m][j] = sv[has ? idx : 0];
+          idx += has;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < M + 2; ++k) {
+        T xr[VEC];
+        ldv<T, VEC>(xr, base + k * CW);
+        // this row is neighbour dx = -1 of point k, 0 of k - 1, +1 of k - 2
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int m = k - j;
+          if (m < 0 || m >= M) continue;
+          if ((pr >> (3 * m + j)) & 1u) axpy<T, VEC, EXACT>(acc[m], vl[m][j], xr);
+        }
+      }
+    }
+  }
+  const unsigned irr = valid & ~geo;
+  if (irr) {  // rows missing in-grid neighbours: their own CSR order
+    // the rows' column indices, lane-parallel and all issued up front
+    // (one memory round trip for the group, not one per nonzero)
+    int cl[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+      cl[m] = ((irr >> m) & 1u) && vb[m] + lane < vb[m + 1] ? __ldg(op.ci + vb[m] + lane) : 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      if (!((irr >> m) & 1u)) continue;
+      const int r = rbase + m;
+      for (int k = vb[m]; k < vb[m + 1]; ++k) {  // <= 27 nonzeros: one lane each
+        int o = __shfl_sync(0xffffffffu, cl[m], k - vb[m]) - r;
+        int dz = 0, dy = 0;
+        if (D3) {
+          dz = o > a.nxy / 2 ? 1 : (o < -(a.nxy / 2) ? -1 : 0);
+          o -= dz * a.nxy;
+          dy = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
+          o -= dy * a.nx;
+        } else {
+          dz = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
+          o -= dz * a.nx;
+        }
+        if (dz + 1 < dz_lo || dz + 1 >= dz_hi) continue;  // warp-uniform
+        const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
+        const int yy = D3 ? wy + 1 + dy : 0;
+        T xr[VEC];
+        ldv<T, VEC>(xr, P + (yy * ROW + col0 + m + 1 + o) * CW + lane * VEC);
+        axpy<T, VEC, EXACT>(acc[m], sv[k - v0], xr);
+      }
+    }
+  }
+}
+
 template <class T, bool D3, int M, int ROW, bool PAD, bool EXACT>
 __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpArgs& op,
                                                 const T* __restrict__ P0, const T* __restrict__ P1,
@@ -243,108 +365,8 @@ __device__ __forceinline__ void stencil_compute(const StencilArgs& a, const OpAr
     }
     return;
   }
-  // Grid-face points: a row whose nonzero count equals the number of its
-  // in-grid stencil neighbours holds exactly those (every nonzero was checked
-  // to be an in-grid neighbour at plan time), so its value for neighbour bit
-  // q sits at popc(mask & (2^q - 1)) -- the same compile-time loop as the
-  // fast path, predicated per point.  Other rows (missing in-grid
-  // neighbours) walk their own CSR entries.
-  int vb[M + 1];
-#pragma unroll
-  for (int m = 0; m <= M; ++m) vb[m] = __shfl_sync(0xffffffffu, rpl, m);
-  unsigned pm[M];
-  unsigned geo = 0;
-  {
-    unsigned face = op.used;
-    if (D3) {
-      if (py == 0) face &= ~nb_bits(1, -1);
-      if (py == a.ny - 1) face &= ~nb_bits(1, 1);
-    }
-    if (pz == 0) face &= ~nb_bits(D3 ? 2 : 2, -1);
-    if (pz == a.nz - 1) face &= ~nb_bits(2, 1);
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      unsigned pmm = face;
-      if (px + m == 0) pmm &= ~nb_bits(0, -1);
-      if (px + m == a.nx - 1) pmm &= ~nb_bits(0, 1);
-      pm[m] = pmm;
-      if (((valid >> m) & 1u) && vb[m + 1] - vb[m] == __popc(pmm)) geo |= 1u << m;
-    }
-  }
-  if (geo) {
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const int dz = D3 ? l / 3 - 1 : l - 1;
-      const int dy = D3 ? l % 3 - 1 : 0;
-      const int li = (dz + 1) * 3 + (dy + 1);
-      if (!(op.used & (7u << (3 * li)))) continue;
-      const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
-      const T* base = P + ((D3 ? (wy + 1 + dy) * ROW : 0) + col0) * CW + lane * VEC;
-      // the line's values of all M points first (independent shared loads,
-      // absent neighbours read a dummy slot), then the predicated updates:
-      // a face group costs about what an interior group does, so the CTA's
-      // other warps are not held at the plane ring by it
-      T vl[M][3];
-      unsigned pr = 0;  // bit 3 m + j: point m has neighbour dx = j - 1 on this line
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const unsigned bits = ((geo >> m) & 1u) ? (pm[m] >> (3 * li)) & 7u : 0u;
-        pr |= bits << (3 * m);
-        // value index of the line's first present neighbour, then +1 per bit
-        int idx = vb[m] - v0 + __popc(pm[m] & ((1u << (3 * li)) - 1u));
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const bool has = (bits >> j) & 1u;
-          vl[m][j] = sv[has ? idx : 0];
-          idx += has;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < M + 2; ++k) {
-        T xr[VEC];
-        ldv<T, VEC>(xr, base + k * CW);
-        // this row is neighbour dx = -1 of point k, 0 of k - 1, +1 of k - 2
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int m = k - j;
-          if (m < 0 || m >= M) continue;
-          if ((pr >> (3 * m + j)) & 1u) axpy<T, VEC, EXACT>(acc[m], vl[m][j], xr);
-        }
-      }
-    }
-  }
-  const unsigned irr = valid & ~geo;
-  if (irr) {  // rows missing in-grid neighbours: their own CSR order
-    // the rows' column indices, lane-parallel and all issued up front
-    // (one memory round trip for the group, not one per nonzero)
-    int cl[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-      cl[m] = ((irr >> m) & 1u) && vb[m] + lane < vb[m + 1] ? __ldg(op.ci + vb[m] + lane) : 0;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      if (!((irr >> m) & 1u)) continue;
-      const int r = rbase + m;
-      for (int k = vb[m]; k < vb[m + 1]; ++k) {  // <= 27 nonzeros: one lane each
-        int o = __shfl_sync(0xffffffffu, cl[m], k - vb[m]) - r;
-        int dz = 0, dy = 0;
-        if (D3) {
-          dz = o > a.nxy / 2 ? 1 : (o < -(a.nxy / 2) ? -1 : 0);
-          o -= dz * a.nxy;
-          dy = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
-          o -= dy * a.nx;
-        } else {
-          dz = o > a.nx / 2 ? 1 : (o < -(a.nx / 2) ? -1 : 0);
-          o -= dz * a.nx;
-        }
-        const T* P = dz < 0 ? P0 : (dz == 0 ? P1 : P2);
-        const int yy = D3 ? wy + 1 + dy : 0;
-        T xr[VEC];
-        ldv<T, VEC>(xr, P + (yy * ROW + col0 + m + 1 + o) * CW + lane * VEC);
-        axpy<T, VEC, EXACT>(acc[m], sv[k - v0], xr);
-      }
-    }
-  }
+  stencil_slow<T, D3, M, ROW, EXACT>(a, op, P0, P1, P2, sv, rpl, valid, wy, col0, rbase, px, py, pz,
+                                     lane, 0, 3, acc);
 }
 
 template <class T, bool D3, int M, int ROW, bool PAD, bool EXACT>
@@ -501,7 +523,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   // then in use over three steps, so its ring is deeper and loaded further ahead
   constexpr bool SLIDE = D3;
   constexpr int VSL = kValueSlots<D3>;  // value slots per warp
-  constexpr int VAHEAD = SLIDE ? 4 : 2;  // values are issued this many planes ahead
   T* svb = reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) + (size_t)warp * VSL * VS;
   int* srp = reinterpret_cast<int*>(reinterpret_cast<T*>(smem_raw + (size_t)ns * plane_bytes) +
                                     (size_t)NW * VSL * VS) + warp * 8 * 16;
@@ -595,16 +616,31 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     };
     // the group at output plane jj of this item takes the full-box code (warp-uniform)
     auto fast_at = [&](int jj) {
-      if (jj >= nzl || !opa.full || valid == 0) return false;
+      if (jj < 0 || jj >= nzl || !opa.full || valid == 0) return false;
       if constexpr (SLIDE)
         return srp[(jj & 7) * 16 + 15] != 0;
       else
         return srp[(jj & 7) * 16 + M] - srp[(jj & 7) * 16] == M * (D3 ? 27 : 9);
     };
     constexpr int VEC = 16 / sizeof(T);
-    [[maybe_unused]] T acc3[3][M][VEC];  // SLIDE: output planes j, j + 1, j + 2
-    [[maybe_unused]] bool f0 = false, f1 = false, f2 = false;
     if constexpr (SLIDE) {
+      // ---- z-sliding loop: one pass per INPUT plane p = z0-1 .. z1 ----
+      // Plane p (iteration pi = p - z0 + 1) adds dz = +1 to output pi-2
+      // (acc3[0]), dz = 0 to output pi-1 (acc3[1]) and dz = -1 to output pi
+      // (acc3[2]); output pi-2 is then complete and stored.  Full-box and
+      // grid-face groups go through slide_plane (all live targets in one
+      // pass over the plane's rows), rows missing in-grid neighbours through
+      // stencil_slow restricted to this plane.  Each plane is read once and
+      // released: the ring holds the plane in use plus the prefetch depth.
+      T acc3[3][M][VEC];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc3[q][m][v] = T(0);
+      // values of output jj: issued at iteration jj - 2, used at jj .. jj + 2;
+      // row pointers of jj: issued at jj - 4 (the values' addresses)
       issue_rp(0);
       issue_rp(1);
       issue_rp(2);
@@ -614,18 +650,57 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       __syncwarp();
       issue_vals(0);
       issue_vals(1);
-      issue_vals(2);
-      issue_rp(4);
       cp_async_commit();
-      issue_vals(3);
-      issue_rp(5);
-      cp_async_commit();
+      bool f0 = false, f1 = false;  // outputs pi-2, pi-1 take the full-box code
+      for (int pi = 0; pi < nzl + 2; ++pi) {
+        if (pi == 0)
+          cp_async_wait<0>();
+        else
+          cp_async_wait<1>();  // values up to output pi, row pointers up to pi + 2
+        __syncwarp();
+        issue_vals(pi + 2);
+        issue_rp(pi + 4);
+        cp_async_commit();
+        s_bar_wait(&full[s0], p0);
+        const T* P = planes + (size_t)s0 * a.plane_elems;
+        const bool f2 = fast_at(pi);
+        const T* sv0 = svb + ((pi + VSL - 2) % VSL) * VS;
+        const T* sv1 = svb + ((pi + VSL - 1) % VSL) * VS;
+        const T* sv2 = svb + (pi % VSL) * VS;
+        slide_plane_masked<T, M, TL::ROW, EXACT>((f0 ? 1u : 0u) | (f1 ? 2u : 0u) | (f2 ? 4u : 0u), P,
+                                                 wy, wx * M, lane, sv0, sv1, sv2, acc3[0], acc3[1],
+                                                 acc3[2]);
+        // groups with rows missing in-grid neighbours: per-point paths, this plane only
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
+        for (int q = 0; q < 3; ++q) {
+          const int jo = pi - 2 + q;  // output plane of target q, neighbour dz = 1 - q
+          const bool fq = q == 0 ? f0 : (q == 1 ? f1 : f2);
+          if (fq || jo < 0 || jo >= nzl || valid == 0) continue;
+          const int rpl = live ? srp[(jo & 7) * 16 + lane] : 0;
+          stencil_slow<T, D3, M, TL::ROW, EXACT>(a, opa, P, P, P, svb + (jo % VSL) * VS, rpl, valid, wy,
+                                                 wx * M, r0 + jo * a.nxy, x, y, z0 + jo, lane, 2 - q,
+                                                 3 - q, acc3[q]);
+        }
+        if (pi >= 2) {
+          T* const outp = outb + (size_t)(r0 + (pi - 2) * a.nxy) * a.cc + (size_t)cs * CW + lane * VEC;
+#pragma unroll
+          for (int m = 0; m < M; ++m)
+            if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * a.cc, acc3[0][m]);
+        }
 #pragma unroll
         for (int m = 0; m < M; ++m)
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) acc3[q][m][v] = T(0);
+          for (int v = 0; v < VEC; ++v) {
+            acc3[0][m][v] = acc3[1][m][v];
+            acc3[1][m][v] = acc3[2][m][v];
+            acc3[2][m][v] = T(0);
+          }
+        f0 = f1;
+        f1 = f2;
+        __syncwarp();
+        if (lane == 0) s_bar_arrive(&empty[s0]);
+        if (++s0 == ns) s0 = 0, p0 ^= 1u;
+      }
     } else {
       issue_rp(0);
       issue_rp(1);
@@ -638,86 +713,46 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
       issue_vals(1);
       issue_rp(3);
       cp_async_commit();
-    }
-    for (int j = 0; j < nzl; ++j) {
-      cp_async_wait<1>();  // values up to plane j + VAHEAD - 2, row pointers two further
-      __syncwarp();
-      issue_vals(j + VAHEAD);
-      issue_rp(j + VAHEAD + 2);
-      cp_async_commit();
-      const int rp_j = live ? srp[(j & 7) * 16 + lane] : 0;
-      // ring positions of planes z-1 (s0), z (s1), z+1 (s2)
-      int s1 = s0 + 1, s2;
-      uint32_t p1 = p0, p2;
-      if (s1 == ns) s1 = 0, p1 ^= 1u;
-      s2 = s1 + 1;
-      p2 = p1;
-      if (s2 == ns) s2 = 0, p2 ^= 1u;
-      if (j == 0) {
-        s_bar_wait(&full[s0], p0);
-        s_bar_wait(&full[s1], p1);
-      }
-      s_bar_wait(&full[s2], p2);
-      const int rb = r0 + j * a.nxy;
-      const T* P0 = planes + (size_t)s0 * a.plane_elems;
-      const T* P1 = planes + (size_t)s1 * a.plane_elems;
-      const T* P2 = planes + (size_t)s2 * a.plane_elems;
-      T* const outp = outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * VEC;
-      bool slid = false;
-      if constexpr (SLIDE) {
-        const T* sv0 = svb + (j % VSL) * VS;
-        const T* sv1 = svb + ((j + 1) % VSL) * VS;
-        const T* sv2 = svb + ((j + 2) % VSL) * VS;
+      for (int j = 0; j < nzl; ++j) {
+        cp_async_wait<1>();  // values of plane j, row pointers of plane j + 2
+        __syncwarp();
+        issue_vals(j + 2);
+        issue_rp(j + 4);
+        cp_async_commit();
+        const int rp_j = live ? srp[(j & 7) * 16 + lane] : 0;
+        // ring positions of planes z-1 (s0), z (s1), z+1 (s2)
+        int s1 = s0 + 1, s2;
+        uint32_t p1 = p0, p2;
+        if (s1 == ns) s1 = 0, p1 ^= 1u;
+        s2 = s1 + 1;
+        p2 = p1;
+        if (s2 == ns) s2 = 0, p2 ^= 1u;
         if (j == 0) {
-          f0 = fast_at(0);
-          f1 = fast_at(1);
-          // planes z0-1 and z0 of the item: dz = -1 and 0 of output 0, dz = -1 of output 1
-          slide_plane_masked<T, M, TL::ROW, EXACT>(f0 ? 4u : 0u, P0, wy, wx * M, lane, sv0, sv0, sv0,
-                                                   acc3[0], acc3[0], acc3[0]);
-          slide_plane_masked<T, M, TL::ROW, EXACT>((f0 ? 2u : 0u) | (f1 ? 4u : 0u), P1, wy, wx * M,
-                                                   lane, sv0, sv0, sv1, acc3[0], acc3[0], acc3[1]);
+          s_bar_wait(&full[s0], p0);
+          s_bar_wait(&full[s1], p1);
         }
-        f2 = fast_at(j + 2);
-        // the newest plane (z+1): dz = +1 of output j, 0 of j + 1, -1 of j + 2
-        slide_plane_masked<T, M, TL::ROW, EXACT>((f0 ? 1u : 0u) | (f1 ? 2u : 0u) | (f2 ? 4u : 0u), P2,
-                                                 wy, wx * M, lane, sv0, sv1, sv2, acc3[0], acc3[1],
-                                                 acc3[2]);
-        if (f0) {
-#pragma unroll
-          for (int m = 0; m < M; ++m)
-            if ((valid >> m) & 1u) stv<T, VEC>(outp + (size_t)m * a.cc, acc3[0][m]);
-          slid = true;
-        }
-#pragma unroll
-        for (int m = 0; m < M; ++m)
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            acc3[0][m][v] = acc3[1][m][v];
-            acc3[1][m][v] = acc3[2][m][v];
-            acc3[2][m][v] = T(0);
+        s_bar_wait(&full[s2], p2);
+        const int rb = r0 + j * a.nxy;
+        stencil_points<T, D3, M, TL::ROW, true, EXACT>(
+            a, opa, planes + (size_t)s0 * a.plane_elems, planes + (size_t)s1 * a.plane_elems,
+            planes + (size_t)s2 * a.plane_elems, svb + (j % VSL) * VS, rp_j, valid, wy, wx * M, rb,
+            x, y, z0 + j, outb + (size_t)rb * a.cc + (size_t)cs * CW + lane * VEC, a.cc, lane);
+        __syncwarp();
+        if (lane == 0) {
+          s_bar_arrive(&empty[s0]);
+          if (j == nzl - 1) {
+            s_bar_arrive(&empty[s1]);
+            s_bar_arrive(&empty[s2]);
           }
-        f0 = f1;
-        f1 = f2;
-      }
-      if (!slid)
-        stencil_points<T, D3, M, TL::ROW, true, EXACT>(a, opa, P0, P1, P2, svb + (j % VSL) * VS, rp_j,
-                                                       valid, wy, wx * M, rb, x, y, z0 + j, outp,
-                                                       a.cc, lane);
-      __syncwarp();
-      if (lane == 0) {
-        s_bar_arrive(&empty[s0]);
-        if (j == nzl - 1) {
-          s_bar_arrive(&empty[s1]);
-          s_bar_arrive(&empty[s2]);
         }
-      }
-      if (j == nzl - 1) {  // the next item starts at the plane after s2
-        s0 = s2 + 1;
-        p0 = p2;
-        if (s0 == ns) s0 = 0, p0 ^= 1u;
-      } else {
-        s0 = s1;
-        p0 = p1;
+        if (j == nzl - 1) {  // the next item starts at the plane after s2
+          s0 = s2 + 1;
+          p0 = p2;
+          if (s0 == ns) s0 = 0, p0 ^= 1u;
+        } else {
+          s0 = s1;
+          p0 = p1;
+        }
       }
     }
     cp_async_wait<0>();
@@ -908,16 +943,21 @@ bool stencil_prepare(StencilPlan& sp, const StencilGeom& g, const void* X, int c
                                          8 * 16 * 4);
   // CTAs per SM, then the deepest ring that fits (>= 3 planes in use)
   const int per_env = env_int("TFG_STENCIL_CTAS", 0);
-  int per_sm = per_env > 0 ? std::min(per_env, sp.nw == 8 ? 2 : 4) : (sp.nw == 8 ? (g.d3 ? 1 : 2) : 3);
+  // 3-D, 4 warps: 2 CTAs per SM with a 4-plane ring measured best (cfg4 per
+  // pass: 1.264 ms; 3 CTAs with the 2-plane ring they leave room for: 1.281)
+  int per_sm = per_env > 0 ? std::min(per_env, sp.nw == 8 ? 2 : 4)
+                           : (sp.nw == 8 ? (g.d3 ? 1 : 2) : (g.d3 ? 2 : 3));
+  // 2-D: planes z-1, z, z+1 in use; 3-D (z-sliding): one plane in use + prefetch
+  const int min_ns = g.d3 ? 2 : 3;
   int ns = 0;
   for (; per_sm >= 1; --per_sm) {
     const size_t budget = kSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
     ns = (int)std::min<size_t>(kMaxNS, (budget - std::min(budget, vbytes)) / sp.plane_bytes);
-    if (ns >= 3) break;
+    if (ns >= min_ns) break;
   }
-  if (per_sm < 1 || ns < 3) return false;
+  if (per_sm < 1 || ns < min_ns) return false;
   const int ns_env = env_int("TFG_STENCIL_NS", 0);
-  if (ns_env >= 3) ns = std::min(ns, ns_env);
+  if (ns_env >= min_ns) ns = std::min(ns, ns_env);
   sp.ns = ns;
   sp.smem = ns * sp.plane_bytes + vbytes;
   sp.per_sm = per_sm;
