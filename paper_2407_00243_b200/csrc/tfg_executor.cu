@@ -624,7 +624,19 @@ __global__ void __launch_bounds__(256)
     const int col = (ch * LPR + gl) * VEC;
     T acc[VEC];
     ldv<T, VEC>(acc, partial + (size_t)s0 * cc + col);
-    for (int64_t sg = s0 + 1; sg < s1; ++sg) {
+    // the longest row has hundreds of segments: 8 independent loads in
+    // flight, then the adds in segment order (the same fixed order)
+    int64_t sg = s0 + 1;
+    for (; sg + 8 <= s1; sg += 8) {
+      T x[8][VEC];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ldv<T, VEC>(x[u], partial + (size_t)(sg + u) * cc + col);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = fops<T>::add(acc[v], x[u][v]);
+    }
+    for (; sg < s1; ++sg) {
       T x[VEC];
       ldv<T, VEC>(x, partial + (size_t)sg * cc + col);
 #pragma unroll
@@ -1874,6 +1886,7 @@ struct tfg_plan {
   bool fused_v2 = false;     // dense-B pipelined GEMM tiles with slot staging
   tfg::dbuf<int> slot;       // D1 row -> stage slot within its tile (-1 none)
   tfg::dbuf<uint8_t> ft_wide;
+  tfg::dbuf<int> ft_order;   // tc fused tiles: balanced tile order of the persistent grid
   int stage_cap = 0;
   int64_t n_wide = 0;
   // (c) wavefront 1 / unfused second op
@@ -2313,6 +2326,47 @@ void plan_create(const tfg_problem& pr, const tfg_schedule* s, cudaStream_t st,
         if (pl.tc.on) {
           tc_finalize(pl.tc, cap);
           pl.fused_smem = pl.tc.smem;
+          {
+            // balanced tile order for the persistent grid: tiles by estimated
+            // cost (B bytes streamed + fused-row gathers, L2 gathers of tiles
+            // too wide for the stage weighted 2x), longest first onto the
+            // least-loaded CTA (cfg3: per-SM active cycles max / avg 1.15)
+            const int64_t G = tc_grid(pl.tc, pl.n_ftiles);
+            std::vector<double> cost(pl.n_ftiles);
+            std::vector<int64_t> idx(pl.n_ftiles);
+            for (int64_t v = 0; v < pl.n_ftiles; ++v) {
+              const int64_t rows128 = ((int64_t)(f_ihi[v] - f_ilo[v]) + 127) / 128 * 128;
+              int64_t fnnz = 0;  // nonzeros of the tile's fused rows
+              for (int64_t q = f_joff[v]; q < f_joff[v + 1]; ++q)
+                fnnz += arp[f_rows[q] + 1] - arp[f_rows[q]];
+              cost[v] = (double)rows128 * bc * 4 + (wide[v] ? 2.0 : 1.0) * (double)fnnz * pl.tc.bn * 4;
+              idx[v] = v;
+            }
+            std::stable_sort(idx.begin(), idx.end(),
+                             [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
+            std::vector<std::vector<int>> per((size_t)G);
+            std::vector<std::pair<double, int64_t>> heap;  // (load, cta), min first
+            for (int64_t b = 0; b < G; ++b) heap.emplace_back(0.0, b);
+            auto cmp = [](const std::pair<double, int64_t>& x, const std::pair<double, int64_t>& y) {
+              return x.first > y.first || (x.first == y.first && x.second > y.second);
+            };
+            std::make_heap(heap.begin(), heap.end(), cmp);
+            size_t kmax = 0;
+            for (int64_t v : idx) {
+              std::pop_heap(heap.begin(), heap.end(), cmp);
+              auto& top = heap.back();
+              per[(size_t)top.second].push_back((int)v);
+              kmax = std::max(kmax, per[(size_t)top.second].size());
+              top.first += cost[v];
+              std::push_heap(heap.begin(), heap.end(), cmp);
+            }
+            std::vector<int> order(kmax * (size_t)G, -1);
+            for (int64_t b = 0; b < G; ++b)
+              for (size_t k = 0; k < per[(size_t)b].size(); ++k) order[k * (size_t)G + (size_t)b] = per[(size_t)b][k];
+            pl.ft_order.alloc(order.size());
+            h2d(pl.ft_order.p, order.data(), order.size(), st);
+            TFG_CUDA(cudaStreamSynchronize(st));  // order is a local
+          }
           // fused rows address the stage (or D1) directly: no slot lookup per
           // nonzero in the kernel
           std::vector<int64_t> off(f_rows.size() + 1, 0);
@@ -2601,7 +2655,7 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
       tc_run(pl.tc, pr.n, bc, cc, pl.n_ftiles, pl.ft_ilo.p, pl.ft_ihi.p, pl.ft_joff.p,
              pl.ft_jrows.p, pl.ft_wide.p, pl.slot.p, pl.spill.p, pl.fx_aoff.p, pl.fx_off.p,
              pl.fx_idx.p, static_cast<const float*>(pr.d_a_val), reinterpret_cast<float*>(D1),
-             reinterpret_cast<float*>(D), st);
+             reinterpret_cast<float*>(D), st, pl.ft_order.p, (int64_t)pl.ft_order.n);
   } else if (pl.n_ftiles && pl.fused_v2) {
     launch_fused_v2<T>(pl, D1, D, st);
   } else if (pl.n_ftiles) {

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
                const int* __restrict__ slot, const uint8_t* __restrict__ spill, int stage_cap,
                int cc, const int* __restrict__ fx_aoff, const int64_t* __restrict__ fx_off,
                const int* __restrict__ fx_idx, const float* __restrict__ av, float* D1,
-               float* __restrict__ D) {
+               float* __restrict__ D, const int* __restrict__ order) {
   using R = Roles<CONV, EPI>;
   constexpr int kConv = R::kConv, kEpi = R::kEpi, kMmaWarp = R::kMmaWarp, kEpi0 = R::kEpi0;
   constexpr int VEC = 4;
@@ -283,7 +283,9 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
                 reinterpret_cast<const unsigned char*>(csrc) + off,
                 (uint32_t)(cbytes - off < 16384 ? cbytes - off : 16384), c_full);
       uint32_t t = 0;
-      for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+      for (int64_t vi = blockIdx.x; vi < ntiles; vi += gridDim.x) {
+        const int64_t v = order ? order[vi] : vi;  // plan-time balanced tile order (-1: none)
+        if (v < 0) continue;
         const int ilo = t_ilo[v], ihi = t_ihi[v];
         for (int r0 = ilo; r0 < ihi; r0 += kBM)
           for (int kc = 0; kc < kchunks; ++kc, ++t) {
@@ -302,7 +304,9 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
     const int r = q * 32 + lane;
     const uint32_t lane_bits = (uint32_t)(q * 32) << 16;
     uint32_t t = 0;
-    for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+    for (int64_t vi = blockIdx.x; vi < ntiles; vi += gridDim.x) {
+        const int64_t v = order ? order[vi] : vi;  // plan-time balanced tile order (-1: none)
+        if (v < 0) continue;
       const int ilo = t_ilo[v], ihi = t_ihi[v];
       for (int r0 = ilo; r0 < ihi; r0 += kBM)
         for (int kc = 0; kc < kchunks; ++kc, ++t) {
@@ -350,7 +354,9 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
       bar_wait(c_full, 0);
       const uint32_t sc_addr = su32(sc);
       uint32_t t = 0, b = 0;
-      for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+      for (int64_t vi = blockIdx.x; vi < ntiles; vi += gridDim.x) {
+        const int64_t v = order ? order[vi] : vi;  // plan-time balanced tile order (-1: none)
+        if (v < 0) continue;
         const int ilo = t_ilo[v], ihi = t_ihi[v];
         for (int r0 = ilo; r0 < ihi; r0 += kBM, ++b) {
           const int a = b % NACC;
@@ -389,7 +395,9 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
     const unsigned gmask = group_mask(LPR2);
     const int group = et / LPR2, ngroups = kEpi * 32 / LPR2;
     uint32_t b = 0;
-    for (int64_t v = blockIdx.x; v < ntiles; v += gridDim.x) {
+    for (int64_t vi = blockIdx.x; vi < ntiles; vi += gridDim.x) {
+        const int64_t v = order ? order[vi] : vi;  // plan-time balanced tile order (-1: none)
+        if (v < 0) continue;
       const int ilo = t_ilo[v], ihi = t_ihi[v];
       const bool wide = first_op || t_wide[v] != 0;
       for (int r0 = ilo; r0 < ihi; r0 += kBM, ++b) {
@@ -548,10 +556,15 @@ void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st
   TFG_LAUNCH_CHECK();
 }
 
+int64_t tc_grid(const TcPlan& tc, int64_t ntiles) {
+  return std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
+}
+
 void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* ilo,
             const int* ihi, const int64_t* joff, const int* jrows, const uint8_t* wide,
             const int* slot, const uint8_t* spill, const int* fx_aoff, const int64_t* fx_off,
-            const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st) {
+            const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st,
+            const int* order, int64_t norder) {
   (void)n;
   (void)bc;
   if (!ntiles) return;
@@ -559,11 +572,10 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
     TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.smem));
     // all column slices of a tile run concurrently so B blocks are read from
     // HBM once and hit L2 for the other slices
-    const int64_t gx =
-        std::min<int64_t>(ntiles, std::max<int64_t>(1, sm_count() / std::max(tc.slices, 1)));
+    const int64_t gx = tc_grid(tc, ntiles);
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, tc.smem, st>>>(
-        tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, ntiles, ilo, ihi, joff, jrows, wide, slot, spill,
-        tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D);
+        tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, order ? norder : ntiles, ilo, ihi, joff, jrows, wide,
+        slot, spill, tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D, order);
   };
   const bool fused = joff != nullptr;
   using F = Roles<4, 16>;

@@ -49,7 +49,11 @@ void tc_prep_c(const TcPlan& tc, const float* C, int bc, int cc, cudaStream_t st
 void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* ilo,
             const int* ihi, const int64_t* joff, const int* jrows, const uint8_t* wide,
             const int* slot, const uint8_t* spill, const int* fx_aoff, const int64_t* fx_off,
-            const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st);
+            const int* fx_idx, const float* av, float* D1, float* D, cudaStream_t st,
+            const int* order = nullptr, int64_t norder = 0);
+// CTAs along x of a launch over ntiles tiles (the persistent grid); order, when
+// given, lists the tiles as order[k * tc_grid + b] = CTA b's k-th tile (-1: none)
+int64_t tc_grid(const TcPlan& tc, int64_t ntiles);
 int tc_env_enabled();  // TFG_TC (default 1)
 
 }  // namespace tfg
