@@ -59,3 +59,49 @@ def test_report_csv_and_json():
     assert csv[0] == R.HEADER and csv[1].endswith(",inf,,gpu") and csv[2].split(",")[12] == ""
     js = R.rows_to_json(rows)
     assert '"runs_to_amortize": "inf"' in js and '"fused_ratio": null' in js
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_loaded_mtx_through_gpu_path(tmp_path, cuda, oracle, symmetric):
+    """Row f3 end to end: a .mtx file written with the reference's rules
+    (matrix_market.cpp:21-89; symmetric files mirror the off-diagonal entries,
+    duplicates add) is loaded, scheduled by the GPU inspector and executed on
+    the B200; schedule and D are checked against the oracle on the same CSR."""
+    import paper_2407_00243_b200 as P
+    from helpers import max_rel_err, schedules_equal
+    from oracle.oracle import SchedulerConfig as OCfg
+
+    n = 600
+    rp, ci, v = oracle.gen_random_sparse(n, 0.015, 11)
+    p = tmp_path / ("sym.mtx" if symmetric else "gen.mtx")
+    if symmetric:
+        rows = np.repeat(np.arange(n), np.diff(rp))
+        keep = rows >= ci  # lower triangle; the loader mirrors it
+        lines = [f"{r + 1} {c + 1} {x:.17g}" for r, c, x in zip(rows[keep], ci[keep], v[keep])]
+        lines.append(lines[0])  # a duplicate entry: values add (matrix_market.cpp:70-85)
+        p.write_text("%%MatrixMarket matrix coordinate real symmetric\n% from test\n"
+                     f"{n} {n} {len(lines)}\n" + "\n".join(lines) + "\n")
+    else:
+        MM.write_matrix_market(P.Csr(n, n, rp, ci, v), str(p))
+    a = MM.load_matrix_market(str(p))
+    a.validate()
+    rng = np.random.default_rng(2)
+    b = rng.uniform(-1, 1, (n, 32))
+    c = rng.uniform(-1, 1, (32, 16))
+    cfg = P.SchedulerConfig(ct_size=64, num_workers=8, cache_size_words=4096, b_cols=32, c_cols=16)
+    sched = P.build_schedule(a, cfg)
+    want_s = oracle.build_schedule(n, n, a.row_ptr, a.col_idx, OCfg(**cfg.__dict__))
+    assert schedules_equal(sched.export(), want_s)
+    triple = (a.row_ptr, a.col_idx, a.values)
+    got = P.run(a, b, c, sched, np.float64)
+    assert max_rel_err(got, oracle.run(n, triple, b, c, want_s, np.float64)) <= 1e-12
+    # SpMM-SpMM with the loaded matrix on both sides: bit-exact with reference bits
+    cs = rng.uniform(-1, 1, (n, 8))
+    cfg2 = P.SchedulerConfig(ct_size=64, num_workers=8, cache_size_words=4096, b_cols=n, c_cols=8,
+                             b_is_dense=False)
+    s2 = P.build_schedule(a, cfg2)
+    w2 = oracle.build_schedule(n, n, a.row_ptr, a.col_idx, OCfg(**cfg2.__dict__))
+    assert schedules_equal(s2.export(), w2)
+    got2 = P.run(a, a, cs, s2, np.float64)
+    assert max_rel_err(got2, oracle.run(n, triple, triple + (n,), cs, w2, np.float64)) <= 1e-12
