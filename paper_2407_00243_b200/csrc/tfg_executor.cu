@@ -1820,9 +1820,37 @@ static void spmm_long(const SpmmWork& w, const int* ci, const T* av, const T* X,
   TFG_LAUNCH_CHECK();
 }
 
+// D rows of the empty rows of the list (no other kernel touches them)
+template <class T>
+static void spmm_zero_empty(const SpmmWork& w, int cc, T* out, cudaStream_t st) {
+  const int rb = cc * (int)sizeof(T);
+  const int64_t thr = w.n_empty * (rb / 16);
+  k_zero_rows<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
+      w.n_empty, w.empty_rows.p, rb, reinterpret_cast<unsigned char*>(out));
+  TFG_LAUNCH_CHECK();
+}
+
+// The empty rows of a forked list can be zeroed early, on the side stream,
+// beside whatever the main stream runs before this list (spmm_run then joins
+// the side stream as it does for the long rows).
+static bool spmm_can_zero_early(const SpmmWork& w) {
+  static const bool on = [] {  // TFG_ZERO_EARLY=0: keep the zero fill in front of wavefront 1
+    const char* e = getenv("TFG_ZERO_EARLY");
+    return !e || atoi(e) > 0;
+  }();
+  return on && !w.stencil && w.side && w.n_long && w.n_short && w.n_empty;
+}
+template <class T>
+static void spmm_zero_early(const SpmmWork& w, int cc, T* out, cudaStream_t st) {
+  TFG_CUDA(cudaEventRecord(w.ev_fork, st));
+  TFG_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
+  spmm_zero_empty<T>(w, cc, out, w.side);
+}
+
 template <class T>
 static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
-                     const T* av, const T* X, int cc, T* out, cudaStream_t st) {
+                     const T* av, const T* X, int cc, T* out, cudaStream_t st,
+                     bool empty_done = false) {
   if (w.stencil) {
     stencil_run(*w.stencil, rp, ci, av, out, st, w.exact);
     return;
@@ -1835,13 +1863,7 @@ static void spmm_run(const SpmmWork& w, const int* rp, const int* ci,
     TFG_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
   }
   if (w.n_long) spmm_long<T>(w, ci, av, X, cc, out, fork ? w.side : st);
-  if (w.n_empty) {
-    const int rb = cc * (int)sizeof(T);
-    const int64_t thr = w.n_empty * (rb / 16);
-    k_zero_rows<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
-        w.n_empty, w.empty_rows.p, rb, reinterpret_cast<unsigned char*>(out));
-    TFG_LAUNCH_CHECK();
-  }
+  if (w.n_empty && !empty_done) spmm_zero_empty<T>(w, cc, out, st);
   spmm_dispatch_short<T>(w, rp, ci, av, X, cc, out, st);
   if (fork) {
     TFG_CUDA(cudaEventRecord(w.ev_join, w.side));
@@ -2634,9 +2656,16 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
   const int cc = pr.c_cols, bc = pr.b_cols;
   T* D1 = reinterpret_cast<T*>(pl.d1.p);
   const T* C = static_cast<const T*>(pr.d_c);
+  bool empty_done = false;
   if (part == 1) goto wave1;
   if (pl.zero_d) TFG_CUDA(cudaMemsetAsync(D, 0, (size_t)pr.n * cc * sizeof(T), st));
   if (ev) TFG_CUDA(cudaEventRecord(ev[0], st));
+  // D rows of empty wavefront-1 rows: written beside the first op (its kernels
+  // leave HBM write bandwidth idle), not in front of the wavefront-1 gathers
+  if (part == -1 && spmm_can_zero_early(pl.second)) {
+    spmm_zero_early<T>(pl.second, cc, D, st);
+    empty_done = true;
+  }
   // (a)
   if constexpr (sizeof(T) == 4) {
     if (pl.tc.on && (pl.n_fo_blocks || pl.n_ftiles))
@@ -2676,7 +2705,7 @@ static void plan_execute_t(tfg_plan& pl, T* D, cudaStream_t st, cudaEvent_t* ev 
 wave1:
   // (c)
   spmm_run<T>(pl.second, pr.d_a_row_ptr, pr.d_a_col_idx,
-              static_cast<const T*>(pr.d_a_val), D1, cc, D, st);
+              static_cast<const T*>(pr.d_a_val), D1, cc, D, st, empty_done);
   if (ev) TFG_CUDA(cudaEventRecord(ev[3], st));
 }
 

@@ -109,6 +109,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
          ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// Both tcgen05.mma and tcgen05.commit are issued from warp-uniform code by the
+// lane elect.sync picks (the same lane every time for the full mask): inside
+// an `if (lane == 0)` region the compiler wraps every uniform-datapath
+// instruction in an ELECT / BRA.U.ANY loop, ~10 instructions per MMA that made
+// the issuing thread the slowest stage of the pipeline.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -174,6 +186,39 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   lo = hi == x ? 0.f : x - hi;
 }
+// 4 x 4 transpose of float4 across each quad of lanes: on entry lane 4k + j
+// holds v[c] = columns 4c .. 4c+3 of row 4k + j; on exit v[i] = columns
+// 4j .. 4j+3 of row 4k + i.  A warp store of v[i] then writes 8 rows x 64
+// contiguous bytes (8 lines) instead of 32 rows x 16 bytes (32 lines).
+__device__ __forceinline__ float4 shfl_xor4(const float4& a, int m) {
+  return make_float4(__shfl_xor_sync(0xffffffffu, a.x, m), __shfl_xor_sync(0xffffffffu, a.y, m),
+                     __shfl_xor_sync(0xffffffffu, a.z, m), __shfl_xor_sync(0xffffffffu, a.w, m));
+}
+__device__ __forceinline__ void quad_transpose(float4 (&v)[4], int lane) {
+  const bool b1 = (lane & 2) != 0, b0 = (lane & 1) != 0;
+  {  // exchange 2 x 2 blocks with lane ^ 2
+    const float4 s0 = b1 ? v[0] : v[2], s1 = b1 ? v[1] : v[3];
+    const float4 r0 = shfl_xor4(s0, 2), r1 = shfl_xor4(s1, 2);
+    if (b1) {
+      v[0] = r0;
+      v[1] = r1;
+    } else {
+      v[2] = r0;
+      v[3] = r1;
+    }
+  }
+  {  // exchange inside the 2 x 2 blocks with lane ^ 1
+    const float4 s0 = b0 ? v[0] : v[1], s1 = b0 ? v[2] : v[3];
+    const float4 r0 = shfl_xor4(s0, 1), r1 = shfl_xor4(s1, 1);
+    if (b0) {
+      v[0] = r0;
+      v[2] = r1;
+    } else {
+      v[1] = r0;
+      v[3] = r1;
+    }
+  }
+}
 // D[tmem] (+)= A[tmem] . B[smem desc]^T
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
                                             uint32_t idesc, uint32_t accumulate) {
@@ -204,7 +249,7 @@ __host__ __device__ constexpr int nacc() {
 
 template <int BN, int LPR, int CONV, int EPI>
 __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
-    k_tc_tiles(const __grid_constant__ CUtensorMap bmap, int kchunks, int raw_stages,
+    k_tc_tiles(const __grid_constant__ CUtensorMap bmap, int kchunks, int raw_stages, int dbg_arg,
                const float* __restrict__ cimg, int64_t ntiles, const int* __restrict__ t_ilo,
                const int* __restrict__ t_ihi, const int64_t* __restrict__ t_joff,
                const int* __restrict__ jrows, const uint8_t* __restrict__ t_wide,
@@ -212,6 +257,14 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
                int cc, const int* __restrict__ fx_aoff, const int64_t* __restrict__ fx_off,
                const int* __restrict__ fx_idx, const float* __restrict__ av, float* D1,
                float* __restrict__ D, const int* __restrict__ order) {
+  // timing experiments (wrong D): only in builds with -DTFG_TC_TIMING=1, where
+  // TFG_TC_DBGX selects pipeline stages to skip; 0 and folded away otherwise
+#ifdef TFG_TC_TIMING
+  const int dbg = dbg_arg;
+#else
+  constexpr int dbg = 0;
+  (void)dbg_arg;
+#endif
   using R = Roles<CONV, EPI>;
   constexpr int kConv = R::kConv, kEpi = R::kEpi, kMmaWarp = R::kMmaWarp, kEpi0 = R::kEpi0;
   constexpr int VEC = 4;
@@ -282,17 +335,23 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
         bulk_1d(reinterpret_cast<unsigned char*>(sc) + off,
                 reinterpret_cast<const unsigned char*>(csrc) + off,
                 (uint32_t)(cbytes - off < 16384 ? cbytes - off : 16384), c_full);
-      uint32_t t = 0;
+      int s = 0;
+      uint32_t ph = 1;  // parity of the slot's previous use (first round: nothing to wait for)
+      bool wrapped = false;
       for (int64_t vi = blockIdx.x; vi < ntiles; vi += gridDim.x) {
         const int64_t v = order ? order[vi] : vi;  // plan-time balanced tile order (-1: none)
         if (v < 0) continue;
         const int ilo = t_ilo[v], ihi = t_ihi[v];
         for (int r0 = ilo; r0 < ihi; r0 += kBM)
-          for (int kc = 0; kc < kchunks; ++kc, ++t) {
-            const int s = t % raw_stages;
-            if (t >= (uint32_t)raw_stages) bar_wait(&raw_empty[s], ((t / raw_stages) - 1) & 1);
+          for (int kc = 0; kc < kchunks; ++kc) {
+            if (wrapped) bar_wait(&raw_empty[s], ph);
             bar_expect(&raw_full[s], kChunkBytes);
             tma_2d(ring + (size_t)s * kChunkBytes, &bmap, kc * kKC, r0, &raw_full[s]);
+            if (++s == raw_stages) {
+              s = 0;
+              ph ^= 1u;
+              wrapped = true;
+            }
           }
       }
     }
@@ -303,54 +362,82 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
     const int q = warp & 3, hpart = (warp - 1) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_bits = (uint32_t)(q * 32) << 16;
-    uint32_t t = 0;
+    // The converters need no tile structure: the CTA's chunks are one flat
+    // sequence (chunk t lives in raw slot t % raw_stages, operand stage
+    // t % kOpStages).  A thread's work is split into units of 16 values (one
+    // 64-byte half row): both halves of every chunk (kConv = 4) or its own
+    // half (kConv = 8).  The shared-memory loads of unit u + 1 are issued
+    // before unit u is split and stored to TMEM, so the load latency (several
+    // hundred cycles beside the TMA writes and the MMA operand reads) is off
+    // the per-chunk critical path.
+    uint32_t nchunks = 0;
     for (int64_t vi = blockIdx.x; vi < ntiles; vi += gridDim.x) {
-        const int64_t v = order ? order[vi] : vi;  // plan-time balanced tile order (-1: none)
-        if (v < 0) continue;
-      const int ilo = t_ilo[v], ihi = t_ihi[v];
-      for (int r0 = ilo; r0 < ihi; r0 += kBM)
-        for (int kc = 0; kc < kchunks; ++kc, ++t) {
-          const int s = t % raw_stages, so = t % kOpStages;
-          bar_wait(&raw_full[s], (t / raw_stages) & 1);
-          const float4* src = reinterpret_cast<const float4*>(ring + (size_t)s * kChunkBytes +
-                                                              (size_t)r * 128);
-          constexpr int kHalves = kConv == 4 ? 2 : 1;
-          float h[kHalves][16], l[kHalves][16];
+      const int64_t v = order ? order[vi] : vi;
+      if (v < 0) continue;
+      nchunks += (uint32_t)((t_ihi[v] - t_ilo[v] + kBM - 1) / kBM) * (uint32_t)kchunks;
+    }
+    constexpr int kUnits = kConv == 4 ? 2 : 1;  // units per chunk and thread
+    const uint32_t nunits = nchunks * kUnits;
+    int ls = 0, cs = 0;       // raw slot of the chunk being loaded / converted
+    uint32_t lph = 0;         // raw_full parity of the chunk being loaded
+    const unsigned char* rowp = ring + (size_t)r * 128;
+    auto load = [&](uint32_t u, float4 (&x)[4]) {
+      const int hh = kUnits == 2 ? (int)(u & 1) : hpart;
+      if (kUnits == 1 || (u & 1) == 0) bar_wait(&raw_full[ls], lph);
+      const float4* src = reinterpret_cast<const float4*>(rowp + (size_t)ls * kChunkBytes);
 #pragma unroll
-          for (int hv = 0; hv < kHalves; ++hv) {
-            const int hh = kHalves == 2 ? hv : hpart;
-            float x[16];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 f = src[(hh * 4 + u) ^ (r & 7)];
-              x[4 * u] = f.x;
-              x[4 * u + 1] = f.y;
-              x[4 * u + 2] = f.z;
-              x[4 * u + 3] = f.w;
-            }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) split_tf32(x[i], h[hv][i], l[hv][i]);
-          }
-          // the slot is refilled by the TMA (async proxy): order these generic
-          // reads before that write, then release the slot
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          bar_arrive(&raw_empty[s]);
-          if (t >= (uint32_t)kOpStages) bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int hv = 0; hv < kHalves; ++hv) {
-            const int hh = kHalves == 2 ? hv : hpart;
-            const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64 + hh * 16;
-            tmem_st16(col, h[hv]);
-            tmem_st16(col + 32, l[hv]);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-          tc_fence_before();
-          bar_arrive(&op_full[so]);
+      for (int k = 0; k < 4; ++k) x[k] = src[(hh * 4 + k) ^ (r & 7)];
+      if (kUnits == 1 || (u & 1) == 1) {
+        if (++ls == raw_stages) {
+          ls = 0;
+          lph ^= 1u;
         }
+      }
+    };
+    auto convert = [&](uint32_t u, const float4 (&x)[4]) {
+      const uint32_t t = u / kUnits;
+      const int hh = kUnits == 2 ? (int)(u & 1) : hpart;
+      const bool first = kUnits == 1 || (u & 1) == 0, last = kUnits == 1 || (u & 1) == 1;
+      const int so = (int)(t % kOpStages);
+      float h[16], l[16];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        split_tf32(x[k].x, h[4 * k], l[4 * k]);
+        split_tf32(x[k].y, h[4 * k + 1], l[4 * k + 1]);
+        split_tf32(x[k].z, h[4 * k + 2], l[4 * k + 2]);
+        split_tf32(x[k].w, h[4 * k + 3], l[4 * k + 3]);
+      }
+      if (last) {
+        // the slot is refilled by the TMA (async proxy): order this thread's
+        // (completed) generic reads before that write, then release the slot
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        bar_arrive(&raw_empty[cs]);
+        if (++cs == raw_stages) cs = 0;
+      }
+      if (first && t >= (uint32_t)kOpStages)
+        bar_wait(&op_empty[so], ((t / kOpStages) - 1) & 1);
+      tc_fence_after();
+      const uint32_t col = tmem + lane_bits + op_col0 + (uint32_t)so * 64 + hh * 16;
+      if (!(dbg & 16)) {
+        tmem_st16(col, h);
+        tmem_st16(col + 32, l);
+      }
+      if (last) {
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        bar_arrive(&op_full[so]);
+      }
+    };
+    float4 xa[4], xb[4];
+    if (nunits) load(0, xa);
+    for (uint32_t u = 0; u < nunits; u += 2) {
+      if (u + 1 < nunits) load(u + 1, xb);
+      convert(u, xa);
+      if (u + 2 < nunits) load(u + 2, xa);
+      if (u + 1 < nunits) convert(u + 1, xb);
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
+    {  // the whole warp walks the loop; one elected lane issues (see mma_tf32_ts)
       bar_wait(c_full, 0);
       const uint32_t sc_addr = su32(sc);
       uint32_t t = 0, b = 0;
@@ -370,16 +457,22 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
             const uint32_t ah = tmem + op_col0 + (uint32_t)so * 64, al = ah + 32;
             const uint32_t ch = sc_addr + (uint32_t)(kc * 2 * BN * kKC * 4),
                            cl = ch + (uint32_t)(BN * kKC * 4);
+            // the C image is 1024-byte aligned and each plane a multiple of 1 KB:
+            // one descriptor per plane, the K step advances its address field
+            const uint64_t dh = sw128_desc(ch), dl = sw128_desc(cl);
+            if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < kKC / 8; ++ks) {
-              const uint32_t o = (uint32_t)ks * 32;  // 8 tf32 = 32 bytes of the swizzled row
-              mma_tf32_ts(d, al + ks * 8, sw128_desc(ch + o), kIdesc, (kc | ks) != 0);
-              mma_tf32_ts(d, ah + ks * 8, sw128_desc(cl + o), kIdesc, 1);
-              mma_tf32_ts(d, ah + ks * 8, sw128_desc(ch + o), kIdesc, 1);
+              for (int ks = 0; ks < kKC / 8; ++ks) {
+                const uint64_t o = (uint64_t)(ks * 32 >> 4);  // 8 tf32 = 32 bytes of the swizzled row
+                if (!(dbg & 1)) mma_tf32_ts(d, al + ks * 8, dh + o, kIdesc, (kc | ks) != 0);
+                if (!(dbg & 2)) mma_tf32_ts(d, ah + ks * 8, dl + o, kIdesc, 1);
+                if (!(dbg & 32)) mma_tf32_ts(d, ah + ks * 8, dh + o, kIdesc, (dbg & 1) ? (kc | ks) != 0 : 1);
+              }
+              mma_commit(&op_empty[so]);
+              if (kc == kchunks - 1) mma_commit(&acc_full[a]);
             }
-            mma_commit(&op_empty[so]);
+            __syncwarp();
           }
-          mma_commit(&acc_full[a]);
         }
       }
     }
@@ -406,23 +499,35 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
         tc_fence_after();
         const int row = r0 + m;
         const bool valid = row < ihi;
-        const bool sp = valid && (wide || spill[row]);
-        const int sl = (valid && !wide) ? slot[row] : -1;
+        const bool sp = valid && (wide || spill[row]) && !(dbg & 4);
+        const int sl = (valid && !wide && !(dbg & 8)) ? slot[row] : -1;
+        // D1 rows go out transposed inside lane quads: lane 4k + j writes
+        // columns 4j .. 4j+3 of rows 4k .. 4k+3 in turn (64 contiguous bytes
+        // per row and instruction; the per-lane pattern cost 4x the LSU
+        // store wavefronts, which the converters' shared-memory loads share)
+        const unsigned spmask = __ballot_sync(0xffffffffu, sp);
+        const int quad0 = lane & ~3, qj = lane & 3;
 #pragma unroll
         for (int c0 = g * 16; c0 < BN; c0 += 16 * kEpiGroups) {
           float x[16];
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0), x);
-          if (sp) {
-            float4* o = reinterpret_cast<float4*>(D1 + (size_t)row * cc + n0 + c0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-          }
           if (sl >= 0) {
             float4* o = reinterpret_cast<float4*>(stage + (size_t)sl * BN + c0);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               o[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          }
+          if (spmask) {
+            float4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              v[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+            quad_transpose(v, lane);
+            float* o = D1 + (size_t)(r0 + q * 32 + quad0) * cc + n0 + c0 + 4 * qj;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if ((spmask >> (quad0 + i)) & 1u)
+                *reinterpret_cast<float4*>(o + (size_t)i * cc) = v[i];
           }
         }
         tc_fence_before();
@@ -430,7 +535,7 @@ __global__ void __launch_bounds__(Roles<CONV, EPI>::kThreads, 1)
       }
       if (first_op) continue;
       const int64_t jb = t_joff[v], je = t_joff[v + 1];
-      if (je == jb) continue;
+      if (je == jb || (dbg & 8)) continue;
       named_sync();  // staged / spilled rows visible
       for (int64_t qq = jb + group; qq < je; qq += ngroups) {
         const int j = jrows[qq];
@@ -476,6 +581,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   });
   return fn;
+}
+
+int tc_timing_mask() {
+#ifdef TFG_TC_TIMING
+  const char* e = getenv("TFG_TC_DBGX");
+  return e ? atoi(e) : 0;
+#else
+  return 0;
+#endif
 }
 
 int env_raw_stages() {  // TFG_TC_RING: raw ring depth (tests stress 2)
@@ -574,7 +688,7 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
     // HBM once and hit L2 for the other slices
     const int64_t gx = tc_grid(tc, ntiles);
     kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, tc.smem, st>>>(
-        tc.bmap, tc.kchunks, tc.raw, tc.cimg.p, order ? norder : ntiles, ilo, ihi, joff, jrows, wide,
+        tc.bmap, tc.kchunks, tc.raw, tc_timing_mask(), tc.cimg.p, order ? norder : ntiles, ilo, ihi, joff, jrows, wide,
         slot, spill, tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D, order);
   };
   const bool fused = joff != nullptr;

@@ -7,6 +7,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_probe tools/tc_probe.cu
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 
@@ -18,7 +19,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
          ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-template <int KIND>  // 0: tf32, 1: bf16
+template <int KIND, int N = 256, bool TS = false>  // 0: tf32, 1: bf16; TS: A operand in TMEM
 __global__ void __launch_bounds__(128, 1) k_probe(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   unsigned char* base = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
@@ -31,7 +32,7 @@ __global__ void __launch_bounds__(128, 1) k_probe(int iters, unsigned long long*
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      su32(&tmem_base)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar)));
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(128, 1) k_probe(int iters, unsigned long long*
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t d = tmem_base;
   constexpr uint32_t fmt = KIND == 0 ? 2u : 1u;  // tf32 : bf16
-  constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(256 >> 3) << 17) |
+  constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
   unsigned long long t0 = 0, t1 = 0;
   if (threadIdx.x == 0) {
@@ -50,7 +51,12 @@ __global__ void __launch_bounds__(128, 1) k_probe(int iters, unsigned long long*
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 4 K steps of 32 bytes inside the 128-byte atom
         const uint64_t off = (uint64_t)(k * 32) >> 4;
-        if (KIND == 0)
+        if (KIND == 0 && TS)
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+              "r"(d + 256 + k * 8), "l"(db + off), "r"(idesc), "r"(it | k));
+        else if (KIND == 0)
           asm volatile(
               "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
               " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
@@ -76,27 +82,27 @@ __global__ void __launch_bounds__(128, 1) k_probe(int iters, unsigned long long*
   __syncthreads();
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   if (threadIdx.x < 32)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(d), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(d), "r"(512));
 }
 
-template <int KIND>
+template <int KIND, int N = 256, bool TS = false>
 double run(int sms, int iters) {
   const size_t smem = 48 * 1024 + 1024;
-  cudaFuncSetAttribute(k_probe<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_probe<KIND, N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned long long* cyc;
   cudaMalloc(&cyc, sms * sizeof(unsigned long long));
-  k_probe<KIND><<<sms, 128, smem>>>(16, cyc);  // warm-up
+  k_probe<KIND, N, TS><<<sms, 128, smem>>>(16, cyc);  // warm-up
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_probe<KIND><<<sms, 128, smem>>>(iters, cyc);
+  k_probe<KIND, N, TS><<<sms, 128, smem>>>(iters, cyc);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double k_per = KIND == 0 ? 8 : 16;
-  const double flops = 2.0 * 128 * 256 * k_per * 4 * (double)iters * sms;
+  const double flops = 2.0 * 128 * N * k_per * 4 * (double)iters * sms;
   cudaFree(cyc);
   return flops / (ms * 1e-3) / 1e12;
 }
@@ -111,6 +117,14 @@ int main() {
     tf = a > tf ? a : tf;
     bf = b > bf ? b : bf;
   }
+  double n64ss = 0, n64ts = 0, n128ts = 0;
+  for (int r = 0; r < 3; ++r) {
+    n64ss = fmax(n64ss, run<0, 64, false>(sms, iters));
+    n64ts = fmax(n64ts, run<0, 64, true>(sms, iters));
+    n128ts = fmax(n128ts, run<0, 128, true>(sms, iters));
+  }
+  printf("{\"tf32_M128_N64_SS_tflops\": %.1f, \"tf32_M128_N64_TS_tflops\": %.1f, "
+         "\"tf32_M128_N128_TS_tflops\": %.1f}\n", n64ss, n64ts, n128ts);
   printf("{\"sm_count\": %d, \"tcgen05_tf32_tflops\": %.1f, \"tcgen05_bf16_tflops\": %.1f, "
          "\"shape\": \"cta_group::1 M128 N256, SS operands, 1 CTA/SM, best of 3\", \"status\": \"%s\"}\n",
          sms, tf, bf, cudaGetErrorString(cudaDeviceSynchronize()));
