@@ -1,5 +1,6 @@
-"""A/B of an environment knob that the library reads once per process: runs
-tools/run_steps in fresh processes and prints per-stage and whole-step medians.
+"""A/B of environment knobs the library reads once per process: one fresh
+process per setting (joined with +), per-stage and whole-step medians, L2
+flushed between runs, and the sum of D as a cheap identity check.
 usage: python tools/step_ab.py cfg5 TFG_ZERO_EARLY=1 TFG_ZERO_EARLY=0 ..."""
 import json
 import os
