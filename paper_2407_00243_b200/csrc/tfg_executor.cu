@@ -724,6 +724,16 @@ struct GemmCfg {
   static_assert(BK % V == 0 && TN % V == 0, "vector widths");
 };
 
+// Column (inside the BN slice) of a thread's accumulator vector starting at j
+// (a multiple of V): the thread's TN / V vectors are BN / TN vectors apart, so
+// the 16-byte loads of the C chunk and the D1 stores of the BN / TN threads of
+// a row are contiguous (tx * TN + j put them 2 vectors apart: 2-way
+// shared-memory bank conflicts on every C load of the fp64 tile).
+template <int BN, int TN, int V>
+__device__ __forceinline__ int gemm_col(int tx, int j) {
+  return (j / V) * (BN / TN) * V + tx * V;
+}
+
 // acc[TM][TN] += B[r0 .. r0+cnt) x C[:, n0 .. n0+BN) ; rows >= cnt read zeros.
 template <class T, int BM, int BN, int BK, int TM, int TN, int STAGES>
 __device__ __forceinline__ void gemm_block(const T* __restrict__ B, int bc,
@@ -788,7 +798,7 @@ __device__ __forceinline__ void gemm_block(const T* __restrict__ B, int bc,
 #pragma unroll
           for (int j = 0; j < TN; j += V) {
             T tmp[V];
-            ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + tx * TN + j);
+            ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + gemm_col<BN, TN, V>(tx, j));
 #pragma unroll
             for (int q = 0; q < V; ++q) b[j + q] = tmp[q];
           }
@@ -848,7 +858,7 @@ __device__ __forceinline__ void gemm_compute_chunk(int bc, int kc, int stg, cons
 #pragma unroll
         for (int j = 0; j < TN; j += V) {
           T tmp[V];
-          ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + tx * TN + j);
+          ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + gemm_col<BN, TN, V>(tx, j));
 #pragma unroll
           for (int q = 0; q < V; ++q) b[j + q] = tmp[q];
         }
@@ -872,7 +882,7 @@ __device__ __forceinline__ void gemm_compute_chunk(int bc, int kc, int stg, cons
 #pragma unroll
         for (int j = 0; j < TN; j += V) {
           T tmp[V];
-          ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + tx * TN + j);
+          ldv<T, V>(tmp, cs + (k0 + kk) * G::C_LD + gemm_col<BN, TN, V>(tx, j));
 #pragma unroll
           for (int q = 0; q < V; ++q) b[j + q] = tmp[q];
         }
@@ -930,13 +940,13 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       for (int i = 0; i < TM; ++i) {
         const int m = ty * TM + i;
         if (m < cnt) {
-          T* o = D1 + (size_t)(r0 + m) * ldd + n0 + tx * TN;
+          T* o = D1 + (size_t)(r0 + m) * ldd + n0;
 #pragma unroll
           for (int j = 0; j < TN; j += V) {
             T tmp[V];
 #pragma unroll
             for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
-            stv<T, V>(o + j, tmp);
+            stv<T, V>(o + gemm_col<BN, TN, V>(tx, j), tmp);
           }
         }
 #pragma unroll
@@ -965,13 +975,13 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < TM; ++i) {
       const int m = ty * TM + i;
       if (m < cnt) {
-        T* o = D1 + (size_t)(r0 + m) * ldd + n0 + tx * TN;
+        T* o = D1 + (size_t)(r0 + m) * ldd + n0;
 #pragma unroll
         for (int j = 0; j < TN; j += V) {
           T tmp[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
-          stv<T, V>(o + j, tmp);
+          stv<T, V>(o + gemm_col<BN, TN, V>(tx, j), tmp);
         }
       }
     }
@@ -1186,8 +1196,9 @@ __global__ void __launch_bounds__(256)
             T tmp[V];
 #pragma unroll
             for (int q = 0; q < V; ++q) tmp[q] = acc[i][j + q];
-            if (sp) stv<T, V>(D1 + (size_t)row * cc + n0 + tx * TN + j, tmp);
-            if (sl >= 0) stv<T, V>(stage + (size_t)sl * BN + tx * TN + j, tmp);
+            const int col = gemm_col<BN, TN, V>(tx, j);
+            if (sp) stv<T, V>(D1 + (size_t)row * cc + n0 + col, tmp);
+            if (sl >= 0) stv<T, V>(stage + (size_t)sl * BN + col, tmp);
           }
         }
 #pragma unroll
