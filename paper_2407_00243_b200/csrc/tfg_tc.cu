@@ -682,16 +682,29 @@ void tc_run(const TcPlan& tc, int n, int bc, int cc, int64_t ntiles, const int* 
   (void)n;
   (void)bc;
   if (!ntiles) return;
+  const bool fused = joff != nullptr;
+  // first-op launches stage nothing: their shared memory goes to a deeper raw
+  // ring (6 slots at bCol 256: first op 0.65 -> 0.60 ms on cfg5); TFG_TC_RING pins both
+  int raw = tc.raw, stage_cap = tc.stage_cap;
+  size_t smem = tc.smem;
+  if (!fused) {
+    stage_cap = 0;
+    if (!getenv("TFG_TC_RING")) {
+      const size_t base = fixed_bytes(tc) - (size_t)tc.raw * kChunkBytes;
+      raw = (int)std::min<size_t>(8, (kSmemMax - base) / kChunkBytes);
+      raw = std::max(raw, tc.raw);
+    }
+    smem = fixed_bytes(tc) + (size_t)(raw - tc.raw) * kChunkBytes;
+  }
   auto launch = [&](auto kern, int threads) {
-    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.smem));
+    TFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // all column slices of a tile run concurrently so B blocks are read from
     // HBM once and hit L2 for the other slices
     const int64_t gx = tc_grid(tc, ntiles);
-    kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, tc.smem, st>>>(
-        tc.bmap, tc.kchunks, tc.raw, tc_timing_mask(), tc.cimg.p, order ? norder : ntiles, ilo, ihi, joff, jrows, wide,
-        slot, spill, tc.stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D, order);
+    kern<<<dim3((unsigned)gx, (unsigned)tc.slices), threads, smem, st>>>(
+        tc.bmap, tc.kchunks, raw, tc_timing_mask(), tc.cimg.p, order ? norder : ntiles, ilo, ihi, joff, jrows, wide,
+        slot, spill, stage_cap, cc, fx_aoff, fx_off, fx_idx, av, D1, D, order);
   };
-  const bool fused = joff != nullptr;
   using F = Roles<4, 16>;
   using U = Roles<8, 8>;
   if (tc.bn == 128)
